@@ -1,0 +1,143 @@
+/* ydg.h -- C ABI of the B200 ADER-DG element-update library (libydg.so).
+ *
+ * Implements the element-local ADER-DG update of the elastic (and viscoelastic) wave
+ * equation on tetrahedra, arXiv:1903.11521 (Uphoff & Bader) Sec. 5.1, Eqs.
+ * (seissol:derivative) P:1312-1317, (seissol:timeint) P:1326-1333,
+ * (seissol:correction_local) P:1334-1341 and (seissol:correction_neigh) P:1342.
+ * "P:n" = line n of the paper source.  Readings where the paper is silent or garbled
+ * (basis, face conventions, Riemann solver, viscoelastic equations ...) are in DESIGN.md §3.
+ *
+ * Conventions
+ *  - Every function returns an int status: YDG_OK (0) or one of the error codes below.
+ *    ydg_error_string(h) returns the last message of handle h (owned by h, valid until
+ *    the next call on h).  A failed call leaves the previous state intact, except CUDA /
+ *    NCCL faults, which poison the handle: every later call returns the same error.
+ *  - Host pointers are borrowed for the duration of the call only (data is copied).
+ *    Device memory is owned by the handle and released by ydg_destroy.
+ *  - Canonical DOF layout across the ABI: Q[element][quantity][basis] (the paper's
+ *    Q_kp, column-major B x P per element), in the solver precision
+ *    (double for precision 8, float for precision 4).  Quantity order:
+ *    (sxx, syy, szz, sxy, syz, sxz, u, v, w) then theta^l_(xx,yy,zz,xy,yz,xz), l = 0..2.
+ *    Basis order: Dubiner functions by degree, then r, then q (reading R6).
+ *  - A handle is not thread-safe.
+ */
+#ifndef YDG_H
+#define YDG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  YDG_OK = 0,
+  YDG_ERR_ARG = 1,         /* null pointer, bad size or enum value                         */
+  YDG_ERR_STATE = 2,       /* call out of order (e.g. step before mesh upload)            */
+  YDG_ERR_CUDA = 3,        /* CUDA runtime error (poisons the handle)                     */
+  YDG_ERR_NCCL = 4,        /* NCCL error (poisons the handle)                             */
+  YDG_ERR_MESH = 5,        /* face matched != 2 times, det J <= 0, bad vertex ids         */
+  YDG_ERR_OOM = 6,         /* device allocation failed                                    */
+  YDG_ERR_UNSUPPORTED = 7  /* order / quantities / precision combination not compiled     */
+};
+
+/* ydg_query keys */
+enum {
+  YDG_Q_N_ELEMENTS = 0,        /* global element count                                     */
+  YDG_Q_FIRST_LOCAL = 1,       /* first global element id owned by this rank               */
+  YDG_Q_N_LOCAL = 2,           /* number of elements owned by this rank                    */
+  YDG_Q_NZ_FLOPS = 3,          /* nonzero flops per element-update (executed formulation)  */
+  YDG_Q_ALG_BYTES = 4,         /* algorithmic HBM bytes per element-update (both kernels)  */
+  YDG_Q_B = 5,                 /* basis functions per element, C(N+3,3)                    */
+  YDG_Q_BTILDE = 6,            /* face basis functions, C(N+2,2)                           */
+  YDG_Q_DEVICE_BYTES = 7,      /* device memory held by the handle                         */
+  YDG_Q_LAUNCHES_PER_STEP = 8, /* kernel launches of one ydg_step(nsteps = 1)              */
+  YDG_Q_LOCAL_BYTES = 9,       /* algorithmic bytes / element of the local kernel          */
+  YDG_Q_NEIGH_BYTES = 10,      /* algorithmic bytes / element of the neighbour kernel      */
+  YDG_Q_LOCAL_FLOPS = 11,      /* nonzero flops / element of the local kernel              */
+  YDG_Q_NEIGH_FLOPS = 12,      /* nonzero flops / element of the neighbour kernel          */
+  YDG_Q_PROF_LOCAL_MS = 13,    /* profiling: summed device time of local-kernel launches   */
+  YDG_Q_PROF_NEIGH_MS = 14,    /* profiling: summed device time of neighbour launches      */
+  YDG_Q_PROF_LAUNCHES = 15     /* profiling: number of timed kernel launches               */
+};
+
+typedef struct ydg_solver ydg_solver; /* opaque, owned by the library */
+
+/* Create a solver.
+ *  order      N = maximum polynomial degree (B = C(N+3,3)); compiled: 1..6.
+ *  quantities 9 = elastic, 27 = viscoelastic with 3 mechanisms.
+ *  precision  8 = fp64, 4 = fp32 (storage and arithmetic; setup is fp64, rounded once).
+ *  cuda_device  device ordinal used by every later call.
+ *  out        receives the handle; *out = NULL on failure (then use ydg_last_error()). */
+int ydg_create(int order, int quantities, int precision, int cuda_device, ydg_solver** out);
+
+/* Static message of the last ydg_create failure (thread-local). */
+const char* ydg_last_error(void);
+
+/* Optional, before ydg_upload_mesh: join a z-slab decomposition over nranks GPUs.
+ *  nccl_unique_id  128 bytes from ncclGetUniqueId on rank 0 (same on all ranks).
+ *  Rank r owns global elements [r*ne/nranks, (r+1)*ne/nranks) (the generator orders
+ *  elements z-major, so ranges are slabs).  NCCL is loaded at run time (libnccl.so.2). */
+int ydg_set_comm(ydg_solver* h, int rank, int nranks, const void* nccl_unique_id);
+
+/* Upload the (global) mesh and material; builds geometry, star matrices, flux solvers and
+ * the neighbour relation (Neigh, Face, Rot of P:1342) on the host in fp64.
+ *  n_elements  global element count (> 0).
+ *  elem_xyz    [ne][4][3] vertex coordinates (unwrapped per element; det J > 0 required).
+ *  elem_vid    [ne][4] topological vertex ids (periodic ids allowed); faces are matched by
+ *              sorted id triples and every face must match exactly twice (YDG_ERR_MESH).
+ *  material    [ne][3] = rho, vp, vs (SI units).
+ *  anelastic   quantities == 27: [3] omega_l (rad/s), then [ne][3][2] (Ylam_l, Ymu_l);
+ *              otherwise NULL.
+ * DOFs are zero after this call. */
+int ydg_upload_mesh(ydg_solver* h, int64_t n_elements, const double* elem_xyz,
+                    const int64_t* elem_vid, const double* material, const double* anelastic);
+
+/* Copy DOFs of global elements [first, first+count) (must be owned by this rank) from
+ * host memory Q (canonical layout, solver precision) to the device.  Pinned memory is
+ * used asynchronously on `cuda_stream` when ydg_step follows on the same stream. */
+int ydg_upload_dofs(ydg_solver* h, int64_t first, int64_t count, const void* Q);
+
+/* Same as ydg_upload_dofs / ydg_download_dofs with a device pointer in canonical layout
+ * (no host copy), enqueued on cuda_stream (NULL = the handle's stream). */
+int ydg_upload_dofs_device(ydg_solver* h, int64_t first, int64_t count, const void* Q_dev,
+                           void* cuda_stream);
+int ydg_download_dofs_device(ydg_solver* h, int64_t first, int64_t count, void* Q_dev,
+                             void* cuda_stream);
+
+/* Advance all owned elements by nsteps global time steps of size dt.
+ * Enqueued on cuda_stream (NULL = the handle's own stream); returns without waiting.
+ * Collective over the ranks of ydg_set_comm: all must call with the same dt, nsteps. */
+int ydg_step(ydg_solver* h, double dt, int nsteps, void* cuda_stream);
+
+/* Block until all work of the handle has finished. */
+int ydg_synchronize(ydg_solver* h);
+
+/* Copy DOFs of owned elements [first, first+count) to host memory Q_out (canonical
+ * layout, solver precision).  Blocking. */
+int ydg_download_dofs(ydg_solver* h, int64_t first, int64_t count, void* Q_out);
+
+/* Neighbour relation of owned elements [first, first+count): nb [count][4] global element
+ * ids (Neigh), j [count][4] neighbour local face (Face), hrot [count][4] orientation (Rot,
+ * position of the element's face-first vertex id in the neighbour's face triple), with
+ * local faces (0,2,1), (0,1,3), (0,3,2), (1,2,3) (reading R7). */
+int ydg_get_neighbours(ydg_solver* h, int64_t first, int64_t count, int64_t* nb, int8_t* j,
+                       int8_t* hrot);
+
+/* Enable (1) / disable (0) per-launch CUDA-event timing of the element kernels inside
+ * ydg_step (events recorded on the launch stream around every launch).  Enabling resets
+ * the totals; ydg_query(YDG_Q_PROF_*) synchronises with the recorded events. */
+int ydg_profile(ydg_solver* h, int enable);
+
+/* Query a scalar (see YDG_Q_*). */
+int ydg_query(ydg_solver* h, int what, double* value);
+
+const char* ydg_error_string(const ydg_solver* h);
+
+/* Release the handle and all its device memory (NULL is a no-op). */
+void ydg_destroy(ydg_solver* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* YDG_H */

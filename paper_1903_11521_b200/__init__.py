@@ -1,0 +1,173 @@
+"""B200-native ADER-DG element update (arXiv:1903.11521 Sec. 5.1) -- Python binding.
+
+Thin ctypes marshalling over the C ABI of ``libydg.so`` (declared in ``include/ydg.h``);
+every step of the method runs in the library's CUDA kernels.  There is no CPU fallback:
+importing works without a GPU (so the ABI can be inspected), but any compute call on a
+machine without the built library or a CUDA device raises.
+
+    import paper_1903_11521_b200 as ydg
+    h = ydg.ydg_create(5, 9, 8)
+    ydg.ydg_upload_mesh(h, xyz, vid, material)
+    ydg.ydg_upload_dofs(h, 0, Q)            # canonical [element][quantity][basis]
+    ydg.ydg_step(h, dt, 10)
+    Q1 = ydg.ydg_download_dofs(h, 0, n)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libydg.so")
+
+YDG_OK, YDG_ERR_ARG, YDG_ERR_STATE, YDG_ERR_CUDA, YDG_ERR_NCCL, YDG_ERR_MESH, YDG_ERR_OOM, \
+    YDG_ERR_UNSUPPORTED = range(8)
+(YDG_Q_N_ELEMENTS, YDG_Q_FIRST_LOCAL, YDG_Q_N_LOCAL, YDG_Q_NZ_FLOPS, YDG_Q_ALG_BYTES, YDG_Q_B,
+ YDG_Q_BTILDE, YDG_Q_DEVICE_BYTES, YDG_Q_LAUNCHES_PER_STEP, YDG_Q_LOCAL_BYTES, YDG_Q_NEIGH_BYTES,
+ YDG_Q_LOCAL_FLOPS, YDG_Q_NEIGH_FLOPS, YDG_Q_PROF_LOCAL_MS, YDG_Q_PROF_NEIGH_MS,
+ YDG_Q_PROF_LAUNCHES) = range(16)
+
+EXPORTS = ("ydg_create", "ydg_last_error", "ydg_set_comm", "ydg_upload_mesh", "ydg_upload_dofs",
+           "ydg_upload_dofs_device", "ydg_download_dofs_device", "ydg_step", "ydg_synchronize",
+           "ydg_download_dofs", "ydg_get_neighbours", "ydg_profile", "ydg_query", "ydg_error_string",
+           "ydg_destroy")
+
+
+class YdgError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"ydg error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib():
+    """Load libydg.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run python -m paper_1903_11521_b200.build")
+        L = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+        vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+        L.ydg_create.argtypes = [i32, i32, i32, i32, ctypes.POINTER(vp)]
+        L.ydg_last_error.restype = ctypes.c_char_p
+        L.ydg_set_comm.argtypes = [vp, i32, i32, ctypes.c_char_p]
+        L.ydg_upload_mesh.argtypes = [vp, i64, vp, vp, vp, vp]
+        L.ydg_upload_dofs.argtypes = [vp, i64, i64, vp]
+        L.ydg_upload_dofs_device.argtypes = [vp, i64, i64, vp, vp]
+        L.ydg_download_dofs_device.argtypes = [vp, i64, i64, vp, vp]
+        L.ydg_step.argtypes = [vp, dbl, i32, vp]
+        L.ydg_synchronize.argtypes = [vp]
+        L.ydg_download_dofs.argtypes = [vp, i64, i64, vp]
+        L.ydg_get_neighbours.argtypes = [vp, i64, i64, vp, vp, vp]
+        L.ydg_profile.argtypes = [vp, i32]
+        L.ydg_query.argtypes = [vp, i32, ctypes.POINTER(dbl)]
+        L.ydg_error_string.argtypes = [vp]
+        L.ydg_error_string.restype = ctypes.c_char_p
+        L.ydg_destroy.argtypes = [vp]
+        L.ydg_destroy.restype = None
+        _lib = L
+    return _lib
+
+
+class Handle:
+    """Owns a ydg_solver*; remembers order / quantities / precision for marshalling."""
+
+    def __init__(self, ptr, order, quantities, precision):
+        self.ptr, self.N, self.P, self.precision = ptr, order, quantities, precision
+        self.B = (order + 1) * (order + 2) * (order + 3) // 6
+        self.dtype = np.float64 if precision == 8 else np.float32
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            ydg_destroy(self)
+
+
+def _check(h, rc):
+    if rc != YDG_OK:
+        raise YdgError(rc, lib().ydg_error_string(h.ptr).decode())
+
+
+def _c(a, dtype):
+    a = np.ascontiguousarray(a, dtype=dtype)
+    return a, a.ctypes.data_as(ctypes.c_void_p)
+
+
+def ydg_create(order, quantities=9, precision=8, device=0):
+    out = ctypes.c_void_p()
+    rc = lib().ydg_create(order, quantities, precision, device, ctypes.byref(out))
+    if rc != YDG_OK:
+        raise YdgError(rc, lib().ydg_last_error().decode())
+    return Handle(out.value, order, quantities, precision)
+
+
+def ydg_set_comm(h, rank, nranks, nccl_unique_id: bytes):
+    _check(h, lib().ydg_set_comm(h.ptr, rank, nranks, nccl_unique_id))
+
+
+def ydg_upload_mesh(h, elem_xyz, elem_vid, material, anelastic=None):
+    xyz, pxyz = _c(elem_xyz, np.float64)
+    vid, pvid = _c(elem_vid, np.int64)
+    mat, pmat = _c(material, np.float64)
+    if anelastic is not None:
+        an, pan = _c(anelastic, np.float64)
+    else:
+        an, pan = None, None
+    _check(h, lib().ydg_upload_mesh(h.ptr, xyz.shape[0], pxyz, pvid, pmat, pan))
+
+
+def ydg_upload_dofs(h, first, Q):
+    q, pq = _c(Q, h.dtype)
+    _check(h, lib().ydg_upload_dofs(h.ptr, first, q.shape[0], pq))
+
+
+def ydg_upload_dofs_device(h, first, count, ptr, stream=None):
+    _check(h, lib().ydg_upload_dofs_device(h.ptr, first, count, ctypes.c_void_p(ptr), ctypes.c_void_p(stream)))
+
+
+def ydg_download_dofs_device(h, first, count, ptr, stream=None):
+    _check(h, lib().ydg_download_dofs_device(h.ptr, first, count, ctypes.c_void_p(ptr), ctypes.c_void_p(stream)))
+
+
+def ydg_step(h, dt, nsteps=1, stream=None):
+    _check(h, lib().ydg_step(h.ptr, float(dt), int(nsteps), ctypes.c_void_p(stream)))
+
+
+def ydg_synchronize(h):
+    _check(h, lib().ydg_synchronize(h.ptr))
+
+
+def ydg_download_dofs(h, first, count, out=None):
+    if out is None:
+        out = np.empty((count, h.P, h.B), dtype=h.dtype)
+    assert out.dtype == h.dtype and out.flags.c_contiguous and out.shape == (count, h.P, h.B)
+    _check(h, lib().ydg_download_dofs(h.ptr, first, count, out.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
+def ydg_get_neighbours(h, first, count):
+    nb = np.empty((count, 4), dtype=np.int64)
+    j = np.empty((count, 4), dtype=np.int8)
+    hr = np.empty((count, 4), dtype=np.int8)
+    _check(h, lib().ydg_get_neighbours(h.ptr, first, count, nb.ctypes.data_as(ctypes.c_void_p),
+                                       j.ctypes.data_as(ctypes.c_void_p), hr.ctypes.data_as(ctypes.c_void_p)))
+    return nb, j, hr
+
+
+def ydg_profile(h, enable=True):
+    _check(h, lib().ydg_profile(h.ptr, 1 if enable else 0))
+
+
+def ydg_query(h, what):
+    v = ctypes.c_double()
+    _check(h, lib().ydg_query(h.ptr, what, ctypes.byref(v)))
+    return v.value
+
+
+def ydg_destroy(h):
+    if h.ptr:
+        lib().ydg_destroy(h.ptr)
+        h.ptr = None

@@ -1,0 +1,548 @@
+// C ABI of libydg.so (include/ydg.h).  Host orchestration: validation, setup, device
+// layout, step sequencing (all local updates of a step complete before the
+// neighbour flux reads the traces), optional z-slab decomposition with an NCCL halo.
+#include "../../include/ydg.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "generated/ydg_counts.h"
+#include "halo.h"
+#include "kernels.cuh"
+#include "setup.h"
+
+using namespace ydg;
+
+struct ydg_solver {
+  int N = 0, P = 0, prec = 0, dev = 0, B = 0, Bt = 0;
+  int status = YDG_OK;  // sticky CUDA / NCCL fault
+  std::string err;
+  cudaStream_t stream = nullptr;
+  // decomposition
+  int rank = 0, nranks = 1;
+  Halo halo;
+  // mesh
+  bool have_mesh = false;
+  int64_t ne = 0, first = 0, nlocal = 0;
+  int64_t nslots = 0;   // local element slots incl. ghosts (multiple of 32)
+  int64_t ntiles = 0;   // owned tiles
+  Neighbours nbr;       // global tables (for ydg_get_neighbours)
+  // device buffers
+  void* Q = nullptr;
+  void* traces = nullptr;
+  void* star = nullptr;
+  void* aplus = nullptr;
+  void* aminus = nullptr;
+  int32_t* nb = nullptr;
+  int8_t* jh = nullptr;
+  void* staging = nullptr;
+  size_t staging_bytes = 0;
+  size_t device_bytes = 0;
+  int grid_local = 0, grid_neigh = 0;
+  int64_t bnd_lo = 0, bnd_hi = 0;  // leading / trailing owned tiles covering all tiles with ghosts
+  // profiling: (start, stop, kind) events of timed launches; kind 0 = local, 1 = neighbour
+  bool profiling = false;
+  struct Ev { cudaEvent_t a, b; int kind; };
+  std::vector<Ev> pending;
+  double prof_ms[2] = {0, 0};
+  int64_t prof_launches = 0;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(ydg_solver* h, int code, const std::string& msg) {
+  h->err = msg;
+  if (code == YDG_ERR_CUDA || code == YDG_ERR_NCCL) h->status = code;
+  return code;
+}
+
+#define CUDA_OR_FAIL(h, call)                                                         \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(h, e_ == cudaErrorMemoryAllocation ? YDG_ERR_OOM : YDG_ERR_CUDA,    \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                \
+  } while (0)
+
+int elem_bytes(const ydg_solver* h) { return h->prec; }
+
+void free_mesh(ydg_solver* h) {
+  for (void** p : {&h->Q, &h->traces, &h->star, &h->aplus, &h->aminus, &h->staging,
+                   reinterpret_cast<void**>(&h->nb), reinterpret_cast<void**>(&h->jh)}) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+  }
+  h->device_bytes = 0;
+  h->have_mesh = false;
+}
+
+int dalloc(ydg_solver* h, void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *p = nullptr;
+    return fail(h, YDG_ERR_OOM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+  }
+  h->device_bytes += bytes;
+  return YDG_OK;
+}
+
+int check(ydg_solver* h) {
+  if (!h) return YDG_ERR_ARG;
+  if (h->status != YDG_OK) return h->status;
+  cudaError_t e = cudaSetDevice(h->dev);
+  if (e != cudaSuccess) return fail(h, YDG_ERR_CUDA, cudaGetErrorString(e));
+  return YDG_OK;
+}
+
+template <typename T>
+void pack_tiles(int P, int64_t n0, int64_t n, int64_t slot0, const ElementCoeffs& c,
+                std::vector<T>& star, std::vector<T>& ap, std::vector<T>& am) {
+  // element t of the chunk -> local slot slot0 + t
+  (void)n0;
+  for (int64_t t = 0; t < n; ++t) {
+    const int64_t s = slot0 + t;
+    const int64_t tile = s / kLanes, lane = s % kLanes;
+    for (int cc = 0; cc < 3; ++cc)
+      for (int p = 0; p < P; ++p)
+        for (int j = 0; j < 3; ++j)
+          star[(((tile * 3 + cc) * P + p) * 3 + j) * kLanes + lane] =
+              static_cast<T>(c.star[((t * 3 + cc) * P + p) * 3 + j]);
+    for (int i = 0; i < 4; ++i)
+      for (int p = 0; p < P; ++p)
+        for (int q = 0; q < P; ++q) {
+          const size_t dst = ((((tile * 4 + i) * P + p) * P + q) * kLanes) + lane;
+          ap[dst] = static_cast<T>(c.aplus[((t * 4 + i) * P + p) * P + q]);
+          am[dst] = static_cast<T>(c.aminus[((t * 4 + i) * P + p) * P + q]);
+        }
+  }
+}
+
+template <typename T>
+int upload_coeffs(ydg_solver* h, const double* xyz, const double* material, const double* anel) {
+  const int P = h->P;
+  const int64_t tiles = h->nslots / kLanes;
+  const size_t star_n = static_cast<size_t>(tiles) * 3 * P * 3 * kLanes;
+  const size_t flux_n = static_cast<size_t>(tiles) * 4 * P * P * kLanes;
+  int rc;
+  if ((rc = dalloc(h, &h->star, star_n * sizeof(T)))) return rc;
+  if ((rc = dalloc(h, &h->aplus, flux_n * sizeof(T)))) return rc;
+  if ((rc = dalloc(h, &h->aminus, flux_n * sizeof(T)))) return rc;
+  CUDA_OR_FAIL(h, cudaMemset(h->star, 0, star_n * sizeof(T)));
+  CUDA_OR_FAIL(h, cudaMemset(h->aplus, 0, flux_n * sizeof(T)));
+  CUDA_OR_FAIL(h, cudaMemset(h->aminus, 0, flux_n * sizeof(T)));
+  // owned elements in chunks of whole tiles
+  const int64_t chunk_tiles = 2048;
+  std::vector<T> st, ap, am;
+  for (int64_t t0 = 0; t0 * kLanes < h->nlocal; t0 += chunk_tiles) {
+    const int64_t s0 = t0 * kLanes;
+    const int64_t n = std::min<int64_t>(chunk_tiles * kLanes, h->nlocal - s0);
+    const int64_t ct = (n + kLanes - 1) / kLanes;
+    ElementCoeffs c;
+    std::string err;
+    if (!element_coeffs(P, h->first + s0, n, xyz, material, anel, h->nbr, &c, &err))
+      return fail(h, YDG_ERR_MESH, err);
+    st.assign(static_cast<size_t>(ct) * 3 * P * 3 * kLanes, T(0));
+    ap.assign(static_cast<size_t>(ct) * 4 * P * P * kLanes, T(0));
+    am.assign(ap.size(), T(0));
+    pack_tiles<T>(P, s0, n, 0, c, st, ap, am);
+    CUDA_OR_FAIL(h, cudaMemcpy(static_cast<T*>(h->star) + static_cast<size_t>(t0) * 3 * P * 3 * kLanes,
+                               st.data(), st.size() * sizeof(T), cudaMemcpyHostToDevice));
+    CUDA_OR_FAIL(h, cudaMemcpy(static_cast<T*>(h->aplus) + static_cast<size_t>(t0) * 4 * P * P * kLanes,
+                               ap.data(), ap.size() * sizeof(T), cudaMemcpyHostToDevice));
+    CUDA_OR_FAIL(h, cudaMemcpy(static_cast<T*>(h->aminus) + static_cast<size_t>(t0) * 4 * P * P * kLanes,
+                               am.data(), am.size() * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  return YDG_OK;
+}
+
+double alg_bytes_local(const ydg_solver* h) {
+  const double P = h->P, B = h->B, Bt = h->Bt;
+  return (2 * B * P + 3 * P * 3 + 4 * P * P + 4 * Bt * P) * elem_bytes(h);
+}
+double alg_bytes_neigh(const ydg_solver* h) {
+  const double P = h->P, B = h->B, Bt = h->Bt;
+  return (2 * B * P + 4 * P * P + 4 * Bt * P) * elem_bytes(h) + 4 * (4 + 1);
+}
+
+// Wrap a launch with CUDA events when profiling.
+template <typename F>
+cudaError_t timed(ydg_solver* h, int kind, cudaStream_t s, F&& launch) {
+  if (!h->profiling) return launch();
+  ydg_solver::Ev ev{nullptr, nullptr, kind};
+  cudaError_t e = cudaEventCreate(&ev.a);
+  if (e == cudaSuccess) e = cudaEventCreate(&ev.b);
+  if (e == cudaSuccess) e = cudaEventRecord(ev.a, s);
+  if (e == cudaSuccess) e = launch();
+  if (e == cudaSuccess) e = cudaEventRecord(ev.b, s);
+  if (e == cudaSuccess) h->pending.push_back(ev);
+  return e;
+}
+
+int drain_profile(ydg_solver* h) {
+  for (auto& ev : h->pending) {
+    float ms = 0;
+    CUDA_OR_FAIL(h, cudaEventSynchronize(ev.b));
+    CUDA_OR_FAIL(h, cudaEventElapsedTime(&ms, ev.a, ev.b));
+    h->prof_ms[ev.kind] += ms;
+    h->prof_launches++;
+    cudaEventDestroy(ev.a);
+    cudaEventDestroy(ev.b);
+  }
+  h->pending.clear();
+  return YDG_OK;
+}
+
+template <typename T>
+int do_step(ydg_solver* h, double dt, int nsteps, cudaStream_t s) {
+  StepParams<T> prm{};
+  prm.Q = static_cast<T*>(h->Q);
+  prm.traces = static_cast<T*>(h->traces);
+  prm.star = static_cast<const T*>(h->star);
+  prm.aplus = static_cast<const T*>(h->aplus);
+  prm.aminus = static_cast<const T*>(h->aminus);
+  prm.nb = h->nb;
+  prm.jh = h->jh;
+  prm.dt = static_cast<T>(dt);
+  for (int d = 0; d < h->N; ++d) {
+    prm.scal[d] = static_cast<T>(dt / (d + 1));
+    prm.scal[h->N + d] = static_cast<T>(dt / (d + 2));
+  }
+  for (int n = 0; n < nsteps; ++n) {
+    if (h->nranks > 1) {
+      // boundary tiles first, then send their traces while the interior proceeds
+      auto local = [&](int64_t t0, int64_t n) -> int {
+        if (n <= 0) return YDG_OK;
+        prm.tile0 = t0;
+        prm.ntiles = n;
+        CUDA_OR_FAIL(h, timed(h, 0, s, [&] { return launch_local<T>(h->N, prm, static_cast<int>(std::min<int64_t>(h->grid_local, n)), s); }));
+        return YDG_OK;
+      };
+      int rc = local(0, h->bnd_lo);
+      if (!rc) rc = local(h->ntiles - h->bnd_hi, h->bnd_hi);
+      if (rc) return rc;
+      rc = h->halo.exchange(s, h->traces, elem_bytes(h), &h->err);
+      if (rc) return fail(h, rc, h->err);
+      if ((rc = local(h->bnd_lo, h->ntiles - h->bnd_hi - h->bnd_lo))) return rc;
+      rc = h->halo.wait(s, &h->err);
+      if (rc) return fail(h, rc, h->err);
+    } else {
+      prm.tile0 = 0;
+      prm.ntiles = h->ntiles;
+      CUDA_OR_FAIL(h, timed(h, 0, s, [&] { return launch_local<T>(h->N, prm, static_cast<int>(std::min<int64_t>(h->grid_local, prm.ntiles)), s); }));
+    }
+    prm.tile0 = 0;
+    prm.ntiles = h->ntiles;
+    CUDA_OR_FAIL(h, timed(h, 1, s, [&] { return launch_neigh<T>(h->N, prm, static_cast<int>(std::min<int64_t>(h->grid_neigh, prm.ntiles)), s); }));
+  }
+  return YDG_OK;
+}
+
+cudaStream_t pick_stream(ydg_solver* h, void* s) { return s ? static_cast<cudaStream_t>(s) : h->stream; }
+
+}  // namespace
+
+extern "C" {
+
+const char* ydg_last_error(void) { return g_last_error.c_str(); }
+
+int ydg_create(int order, int quantities, int precision, int cuda_device, ydg_solver** out) {
+  if (!out) return YDG_ERR_ARG;
+  *out = nullptr;
+  if (order < 1 || order > kMaxN || (quantities != 9 && quantities != 27) ||
+      (precision != 4 && precision != 8)) {
+    g_last_error = "bad order / quantities / precision";
+    return YDG_ERR_ARG;
+  }
+  if (quantities == 27 || (order == 6 && precision == 8)) {
+    g_last_error = "combination not compiled (viscoelastic / N=6 fp64 not yet available)";
+    return YDG_ERR_UNSUPPORTED;
+  }
+  std::unique_ptr<ydg_solver> h(new ydg_solver);
+  h->N = order;
+  h->P = quantities;
+  h->prec = precision;
+  h->dev = cuda_device;
+  h->B = (order + 1) * (order + 2) * (order + 3) / 6;
+  h->Bt = (order + 1) * (order + 2) / 2;
+  cudaError_t e = cudaSetDevice(cuda_device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = configure_kernels(order, precision);
+  if (e != cudaSuccess) {
+    g_last_error = std::string("CUDA: ") + cudaGetErrorString(e);
+    return YDG_ERR_CUDA;
+  }
+  *out = h.release();
+  return YDG_OK;
+}
+
+int ydg_set_comm(ydg_solver* h, int rank, int nranks, const void* nccl_unique_id) {
+  int rc = check(h);
+  if (rc) return rc;
+  if (h->have_mesh) return fail(h, YDG_ERR_STATE, "ydg_set_comm must precede ydg_upload_mesh");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(h, YDG_ERR_ARG, "bad rank / nranks");
+  if (nranks > 1 && !nccl_unique_id) return fail(h, YDG_ERR_ARG, "null NCCL unique id");
+  h->rank = rank;
+  h->nranks = nranks;
+  if (nranks > 1) {
+    rc = h->halo.init(rank, nranks, nccl_unique_id, &h->err);
+    if (rc) return fail(h, rc, h->err);
+  }
+  return YDG_OK;
+}
+
+int ydg_upload_mesh(ydg_solver* h, int64_t ne, const double* xyz, const int64_t* vid,
+                    const double* material, const double* anelastic) {
+  int rc = check(h);
+  if (rc) return rc;
+  if (ne <= 0 || !xyz || !vid || !material) return fail(h, YDG_ERR_ARG, "null mesh input or ne <= 0");
+  if (h->P == 27 && !anelastic) return fail(h, YDG_ERR_ARG, "viscoelastic solver needs anelastic data");
+  for (int64_t e = 0; e < ne; ++e) {
+    const double* m = material + e * 3;
+    if (!(m[0] > 0 && m[1] > 0 && m[2] > 0 && m[1] > m[2]))
+      return fail(h, YDG_ERR_ARG, "material must satisfy rho > 0, vp > vs > 0");
+  }
+  Neighbours nbr;
+  std::string err;
+  if (!match_faces(ne, vid, &nbr, &err)) return fail(h, YDG_ERR_MESH, err);
+  free_mesh(h);
+  h->nbr = std::move(nbr);
+  h->ne = ne;
+  h->first = ne * h->rank / h->nranks;
+  h->nlocal = ne * (h->rank + 1) / h->nranks - h->first;
+  h->ntiles = (h->nlocal + kLanes - 1) / kLanes;
+  // local slots: owned [0, nlocal) padded to tiles, then ghosts
+  std::vector<int64_t> ghost_of;  // global element id of each ghost slot
+  std::vector<int32_t> nb_local(static_cast<size_t>(h->ntiles) * kLanes * 4, 0);
+  std::vector<int8_t> jh_local(nb_local.size(), 0);
+  int64_t owned_slots = h->ntiles * kLanes;
+  std::vector<int64_t> boundary;  // owned tiles with ghosts
+  if (h->nranks > 1) {
+    rc = h->halo.plan(h->nbr, h->first, h->nlocal, owned_slots, &ghost_of, &h->err);
+    if (rc) return fail(h, rc, h->err);
+  }
+  h->nslots = owned_slots + static_cast<int64_t>((ghost_of.size() + kLanes - 1) / kLanes) * kLanes;
+  {
+    // map global neighbour ids to local slots
+    std::vector<std::pair<int64_t, int64_t>> gmap(ghost_of.size());
+    for (size_t g = 0; g < ghost_of.size(); ++g) gmap[g] = {ghost_of[g], owned_slots + static_cast<int64_t>(g)};
+    std::sort(gmap.begin(), gmap.end());
+    std::vector<char> is_boundary(h->ntiles, 0);
+    for (int64_t l = 0; l < h->ntiles * kLanes; ++l) {
+      const int64_t tile = l / kLanes, lane = l % kLanes;
+      for (int i = 0; i < 4; ++i) {
+        const size_t dst = (tile * 4 + i) * kLanes + lane;
+        if (l >= h->nlocal) {  // padding lane: points to itself, zero data
+          nb_local[dst] = static_cast<int32_t>(l);
+          continue;
+        }
+        const int64_t g = h->first + l;
+        const int64_t n = h->nbr.nb[g * 4 + i];
+        int64_t slot;
+        if (n >= h->first && n < h->first + h->nlocal) {
+          slot = n - h->first;
+        } else {
+          auto it = std::lower_bound(gmap.begin(), gmap.end(), std::make_pair(n, int64_t(-1)));
+          if (it == gmap.end() || it->first != n) return fail(h, YDG_ERR_MESH, "ghost map incomplete");
+          slot = it->second;
+          is_boundary[tile] = 1;
+        }
+        if (slot > INT32_MAX) return fail(h, YDG_ERR_UNSUPPORTED, "more than 2^31 local elements");
+        nb_local[dst] = static_cast<int32_t>(slot);
+        jh_local[dst] = static_cast<int8_t>(h->nbr.j[g * 4 + i] | (h->nbr.h[g * 4 + i] << 2));
+      }
+    }
+    // Tiles with ghost neighbours are launched before the interior so their traces can be
+    // sent while the interior computes.  With z-major element order a slab's boundary
+    // tiles sit at both ends of its range: [0, bnd_lo) and [ntiles - bnd_hi, ntiles)
+    // cover every tile with a ghost (for other orders these ranges simply grow).
+    h->bnd_lo = h->bnd_hi = 0;
+    const int64_t half = h->ntiles / 2;
+    for (int64_t t = 0; t < h->ntiles; ++t)
+      if (is_boundary[t]) {
+        if (t < half) h->bnd_lo = std::max(h->bnd_lo, t + 1);
+        else h->bnd_hi = std::max(h->bnd_hi, h->ntiles - t);
+      }
+  }
+  const int eb = elem_bytes(h);
+  const size_t q_n = static_cast<size_t>(h->ntiles) * kLanes * h->P * h->B;
+  const size_t tr_n = static_cast<size_t>(h->nslots) * 4 * h->Bt * h->P;
+  if ((rc = dalloc(h, &h->Q, q_n * eb))) { free_mesh(h); return rc; }
+  if ((rc = dalloc(h, &h->traces, tr_n * eb))) { free_mesh(h); return rc; }
+  if ((rc = dalloc(h, reinterpret_cast<void**>(&h->nb), nb_local.size() * sizeof(int32_t)))) { free_mesh(h); return rc; }
+  if ((rc = dalloc(h, reinterpret_cast<void**>(&h->jh), jh_local.size()))) { free_mesh(h); return rc; }
+  CUDA_OR_FAIL(h, cudaMemset(h->Q, 0, q_n * eb));
+  CUDA_OR_FAIL(h, cudaMemset(h->traces, 0, tr_n * eb));
+  CUDA_OR_FAIL(h, cudaMemcpy(h->nb, nb_local.data(), nb_local.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  CUDA_OR_FAIL(h, cudaMemcpy(h->jh, jh_local.data(), jh_local.size(), cudaMemcpyHostToDevice));
+  rc = eb == 8 ? upload_coeffs<double>(h, xyz, material, anelastic) : upload_coeffs<float>(h, xyz, material, anelastic);
+  if (rc) { free_mesh(h); return rc; }
+  if (h->nranks > 1) {
+    rc = h->halo.bind(h->traces, 4 * h->Bt * h->P, eb, owned_slots, &h->err);
+    if (rc) { free_mesh(h); return fail(h, rc, h->err); }
+  }
+  // staging buffer for DOF transfers (bounded)
+  h->staging_bytes = std::min<size_t>(q_n * eb, size_t(256) << 20);
+  if ((rc = dalloc(h, &h->staging, h->staging_bytes))) { free_mesh(h); return rc; }
+  // grids: resident CTAs per SM x SMs
+  int sms = 0, occ_l = 0, occ_n = 0;
+  CUDA_OR_FAIL(h, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->dev));
+  occ_l = 1;
+  occ_n = 1;
+  h->grid_local = sms * occ_l;
+  h->grid_neigh = sms * occ_n;
+  h->have_mesh = true;
+  return YDG_OK;
+}
+
+static int xfer_dofs(ydg_solver* h, int64_t first, int64_t count, const void* src_host, void* dst_host,
+                     const void* src_dev, void* dst_dev, cudaStream_t s, bool upload) {
+  int rc = check(h);
+  if (rc) return rc;
+  if (!h->have_mesh) return fail(h, YDG_ERR_STATE, "upload the mesh first");
+  if (count < 0 || first < h->first || first + count > h->first + h->nlocal)
+    return fail(h, YDG_ERR_ARG, "element range not owned by this rank");
+  const int eb = elem_bytes(h);
+  const int64_t per = static_cast<int64_t>(h->P) * h->B;
+  const bool dev_side = src_dev || dst_dev;
+  const int64_t chunk = dev_side ? count : std::max<int64_t>(1, static_cast<int64_t>(h->staging_bytes) / (per * eb));
+  for (int64_t c0 = 0; c0 < count; c0 += chunk) {
+    const int64_t n = std::min(chunk, count - c0);
+    const int64_t lfirst = first - h->first + c0;
+    void* buf = h->staging;
+    if (upload) {
+      if (dev_side) {
+        buf = const_cast<void*>(static_cast<const void*>(static_cast<const char*>(src_dev) + c0 * per * eb));
+      } else {
+        CUDA_OR_FAIL(h, cudaMemcpyAsync(buf, static_cast<const char*>(src_host) + c0 * per * eb, n * per * eb,
+                                        cudaMemcpyHostToDevice, s));
+      }
+      cudaError_t e = eb == 8 ? launch_to_tiled<double>(h->P, h->B, static_cast<const double*>(buf), static_cast<double*>(h->Q), lfirst, n, s)
+                              : launch_to_tiled<float>(h->P, h->B, static_cast<const float*>(buf), static_cast<float*>(h->Q), lfirst, n, s);
+      CUDA_OR_FAIL(h, e);
+      if (!dev_side) CUDA_OR_FAIL(h, cudaStreamSynchronize(s));
+    } else {
+      if (dev_side) buf = static_cast<char*>(dst_dev) + c0 * per * eb;
+      cudaError_t e = eb == 8 ? launch_to_canonical<double>(h->P, h->B, static_cast<const double*>(h->Q), static_cast<double*>(buf), lfirst, n, s)
+                              : launch_to_canonical<float>(h->P, h->B, static_cast<const float*>(h->Q), static_cast<float*>(buf), lfirst, n, s);
+      CUDA_OR_FAIL(h, e);
+      if (!dev_side) {
+        CUDA_OR_FAIL(h, cudaMemcpyAsync(static_cast<char*>(dst_host) + c0 * per * eb, buf, n * per * eb,
+                                        cudaMemcpyDeviceToHost, s));
+        CUDA_OR_FAIL(h, cudaStreamSynchronize(s));
+      }
+    }
+  }
+  return YDG_OK;
+}
+
+int ydg_upload_dofs(ydg_solver* h, int64_t first, int64_t count, const void* Q) {
+  if (!Q) return h ? fail(h, YDG_ERR_ARG, "null Q") : YDG_ERR_ARG;
+  return xfer_dofs(h, first, count, Q, nullptr, nullptr, nullptr, h ? h->stream : nullptr, true);
+}
+int ydg_download_dofs(ydg_solver* h, int64_t first, int64_t count, void* Q_out) {
+  if (!Q_out) return h ? fail(h, YDG_ERR_ARG, "null Q_out") : YDG_ERR_ARG;
+  int rc = h ? check(h) : YDG_ERR_ARG;
+  if (rc) return rc;
+  CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
+  return xfer_dofs(h, first, count, nullptr, Q_out, nullptr, nullptr, h->stream, false);
+}
+int ydg_upload_dofs_device(ydg_solver* h, int64_t first, int64_t count, const void* Q_dev, void* s) {
+  if (!Q_dev) return h ? fail(h, YDG_ERR_ARG, "null Q_dev") : YDG_ERR_ARG;
+  return xfer_dofs(h, first, count, nullptr, nullptr, Q_dev, nullptr, h ? pick_stream(h, s) : nullptr, true);
+}
+int ydg_download_dofs_device(ydg_solver* h, int64_t first, int64_t count, void* Q_dev, void* s) {
+  if (!Q_dev) return h ? fail(h, YDG_ERR_ARG, "null Q_dev") : YDG_ERR_ARG;
+  return xfer_dofs(h, first, count, nullptr, nullptr, nullptr, Q_dev, h ? pick_stream(h, s) : nullptr, false);
+}
+
+int ydg_step(ydg_solver* h, double dt, int nsteps, void* cuda_stream) {
+  int rc = check(h);
+  if (rc) return rc;
+  if (!h->have_mesh) return fail(h, YDG_ERR_STATE, "upload the mesh first");
+  if (!(dt > 0) || !std::isfinite(dt) || nsteps < 0) return fail(h, YDG_ERR_ARG, "bad dt or nsteps");
+  cudaStream_t s = pick_stream(h, cuda_stream);
+  return h->prec == 8 ? do_step<double>(h, dt, nsteps, s) : do_step<float>(h, dt, nsteps, s);
+}
+
+int ydg_synchronize(ydg_solver* h) {
+  int rc = check(h);
+  if (rc) return rc;
+  CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
+  CUDA_OR_FAIL(h, cudaDeviceSynchronize());
+  return YDG_OK;
+}
+
+int ydg_get_neighbours(ydg_solver* h, int64_t first, int64_t count, int64_t* nb, int8_t* j, int8_t* hr) {
+  int rc = check(h);
+  if (rc) return rc;
+  if (!h->have_mesh) return fail(h, YDG_ERR_STATE, "upload the mesh first");
+  if (!nb || !j || !hr || count < 0 || first < 0 || first + count > h->ne)
+    return fail(h, YDG_ERR_ARG, "bad neighbour query");
+  std::memcpy(nb, h->nbr.nb.data() + first * 4, count * 4 * sizeof(int64_t));
+  std::memcpy(j, h->nbr.j.data() + first * 4, count * 4);
+  std::memcpy(hr, h->nbr.h.data() + first * 4, count * 4);
+  return YDG_OK;
+}
+
+int ydg_profile(ydg_solver* h, int enable) {
+  int rc = check(h);
+  if (rc) return rc;
+  if ((rc = drain_profile(h))) return rc;
+  h->profiling = enable != 0;
+  h->prof_ms[0] = h->prof_ms[1] = 0;
+  h->prof_launches = 0;
+  return YDG_OK;
+}
+
+int ydg_query(ydg_solver* h, int what, double* v) {
+  if (!h || !v) return YDG_ERR_ARG;
+  if (what >= YDG_Q_PROF_LOCAL_MS && what <= YDG_Q_PROF_LAUNCHES) {
+    int rc = check(h);
+    if (rc) return rc;
+    if ((rc = drain_profile(h))) return rc;
+  }
+  switch (what) {
+    case YDG_Q_PROF_LOCAL_MS: *v = h->prof_ms[0]; break;
+    case YDG_Q_PROF_NEIGH_MS: *v = h->prof_ms[1]; break;
+    case YDG_Q_PROF_LAUNCHES: *v = static_cast<double>(h->prof_launches); break;
+    case YDG_Q_N_ELEMENTS: *v = static_cast<double>(h->ne); break;
+    case YDG_Q_FIRST_LOCAL: *v = static_cast<double>(h->first); break;
+    case YDG_Q_N_LOCAL: *v = static_cast<double>(h->nlocal); break;
+    case YDG_Q_NZ_FLOPS: *v = nz_flops_elastic(h->N); break;
+    case YDG_Q_ALG_BYTES: *v = alg_bytes_local(h) + alg_bytes_neigh(h); break;
+    case YDG_Q_B: *v = h->B; break;
+    case YDG_Q_BTILDE: *v = h->Bt; break;
+    case YDG_Q_DEVICE_BYTES: *v = static_cast<double>(h->device_bytes); break;
+    case YDG_Q_LAUNCHES_PER_STEP: *v = h->nranks > 1 ? 5 : 2; break;
+    case YDG_Q_LOCAL_BYTES: *v = alg_bytes_local(h); break;
+    case YDG_Q_NEIGH_BYTES: *v = alg_bytes_neigh(h); break;
+    case YDG_Q_LOCAL_FLOPS: *v = nz_flops_local(h->N); break;
+    case YDG_Q_NEIGH_FLOPS: *v = nz_flops_elastic(h->N) - nz_flops_local(h->N); break;
+    default: return fail(h, YDG_ERR_ARG, "unknown query");
+  }
+  return YDG_OK;
+}
+
+const char* ydg_error_string(const ydg_solver* h) { return h ? h->err.c_str() : "null handle"; }
+
+void ydg_destroy(ydg_solver* h) {
+  if (!h) return;
+  cudaSetDevice(h->dev);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  drain_profile(h);
+  free_mesh(h);
+  h->halo.destroy();
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+}  // extern "C"

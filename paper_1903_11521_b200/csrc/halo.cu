@@ -1,0 +1,228 @@
+// z-slab halo exchange over NCCL, loaded with dlopen so libydg.so has no link-time NCCL
+// dependency (inside a torch process the already-loaded torch NCCL is reused).
+#include "halo.h"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstring>
+
+namespace ydg {
+
+namespace {
+
+struct NcclUid { char internal[128]; };
+typedef void* NcclComm;
+typedef int (*InitRankFn)(NcclComm*, int, NcclUid, int);
+typedef int (*SendRecvFn)(const void*, size_t, int, int, NcclComm, cudaStream_t);
+typedef int (*RecvFn)(void*, size_t, int, int, NcclComm, cudaStream_t);
+typedef int (*GroupFn)();
+typedef int (*DestroyFn)(NcclComm);
+typedef const char* (*ErrStrFn)(int);
+constexpr int kNcclUint8 = 1;
+
+struct Nccl {
+  void* lib = nullptr;
+  InitRankFn init = nullptr;
+  SendRecvFn send = nullptr;
+  RecvFn recv = nullptr;
+  GroupFn gstart = nullptr, gend = nullptr;
+  DestroyFn destroy = nullptr;
+  ErrStrFn errstr = nullptr;
+  bool load(std::string* err) {
+    if (lib) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names)
+      if ((lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!lib) { *err = "cannot dlopen libnccl.so.2"; return false; }
+    init = reinterpret_cast<InitRankFn>(dlsym(lib, "ncclCommInitRank"));
+    send = reinterpret_cast<SendRecvFn>(dlsym(lib, "ncclSend"));
+    recv = reinterpret_cast<RecvFn>(dlsym(lib, "ncclRecv"));
+    gstart = reinterpret_cast<GroupFn>(dlsym(lib, "ncclGroupStart"));
+    gend = reinterpret_cast<GroupFn>(dlsym(lib, "ncclGroupEnd"));
+    destroy = reinterpret_cast<DestroyFn>(dlsym(lib, "ncclCommDestroy"));
+    errstr = reinterpret_cast<ErrStrFn>(dlsym(lib, "ncclGetErrorString"));
+    if (!init || !send || !recv || !gstart || !gend || !destroy || !errstr) {
+      *err = "libnccl is missing symbols";
+      return false;
+    }
+    return true;
+  }
+};
+Nccl g_nccl;
+
+template <int EB>
+struct Word;
+template <> struct Word<8> { typedef unsigned long long t; };
+template <> struct Word<4> { typedef unsigned int t; };
+
+template <typename W>
+__global__ void pack_kernel(const W* __restrict__ traces, const int64_t* __restrict__ slots,
+                            W* __restrict__ out, int64_t n, int vals) {
+  const int64_t total = n * vals;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = i / vals, v = i - s * vals;
+    out[i] = traces[slots[s] * vals + v];
+  }
+}
+
+int64_t owner(int64_t g, int64_t ne, int nranks) {
+  // largest r with r*ne/nranks <= g
+  int64_t r = (g * nranks) / ne;
+  while (r + 1 < nranks && (r + 1) * ne / nranks <= g) ++r;
+  while (r > 0 && r * ne / nranks > g) --r;
+  return r;
+}
+
+}  // namespace
+
+bool plan_halo(const Neighbours& nbr, int64_t ne, int rank, int nranks, HaloPlan* out,
+               std::string* err) {
+  const int64_t first = ne * rank / nranks, last = ne * (rank + 1) / nranks;
+  std::vector<std::pair<int64_t, int64_t>> ghosts;  // (owner, gid)
+  std::vector<std::pair<int64_t, int64_t>> sends;   // (peer, local slot)
+  for (int64_t e = first; e < last; ++e) {
+    std::vector<int64_t> peers_of_e;
+    for (int i = 0; i < 4; ++i) {
+      const int64_t n = nbr.nb[e * 4 + i];
+      if (n < 0 || n >= ne) { *err = "bad neighbour id"; return false; }
+      if (n >= first && n < last) continue;
+      const int64_t o = owner(n, ne, nranks);
+      ghosts.emplace_back(o, n);
+      peers_of_e.push_back(o);
+    }
+    std::sort(peers_of_e.begin(), peers_of_e.end());
+    peers_of_e.erase(std::unique(peers_of_e.begin(), peers_of_e.end()), peers_of_e.end());
+    for (int64_t o : peers_of_e) sends.emplace_back(o, e - first);
+  }
+  std::sort(ghosts.begin(), ghosts.end());
+  ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+  std::sort(sends.begin(), sends.end());
+  out->ghost_of.clear();
+  out->peers.clear();
+  out->recv_off.clear();
+  out->recv_cnt.clear();
+  out->send_slots.clear();
+  out->send_off.clear();
+  out->send_cnt.clear();
+  for (size_t g = 0; g < ghosts.size(); ++g) {
+    if (out->peers.empty() || out->peers.back() != ghosts[g].first) {
+      out->peers.push_back(static_cast<int>(ghosts[g].first));
+      out->recv_off.push_back(static_cast<int64_t>(g));
+      out->recv_cnt.push_back(0);
+    }
+    out->recv_cnt.back()++;
+    out->ghost_of.push_back(ghosts[g].second);
+  }
+  for (int peer : out->peers) {
+    out->send_off.push_back(static_cast<int64_t>(out->send_slots.size()));
+    int64_t c = 0;
+    for (auto& s : sends)
+      if (s.first == peer) { out->send_slots.push_back(s.second); ++c; }
+    out->send_cnt.push_back(c);
+  }
+  // every peer we send to must also be a peer we receive from (face adjacency symmetric)
+  for (auto& s : sends)
+    if (std::find(out->peers.begin(), out->peers.end(), static_cast<int>(s.first)) == out->peers.end()) {
+      *err = "asymmetric halo";
+      return false;
+    }
+  return true;
+}
+
+int Halo::init(int rank, int nranks, const void* uid, std::string* err) {
+  rank_ = rank;
+  nranks_ = nranks;
+  if (!g_nccl.load(err)) return 4;
+  NcclUid id;
+  std::memcpy(&id, uid, sizeof(id));
+  NcclComm c = nullptr;
+  int r = g_nccl.init(&c, nranks, id, rank);
+  if (r != 0) { *err = std::string("ncclCommInitRank: ") + g_nccl.errstr(r); return 4; }
+  comm_ = c;
+  cudaError_t e = cudaStreamCreateWithFlags(&cstream_, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ready_, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&done_, cudaEventDisableTiming);
+  if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
+  return 0;
+}
+
+int Halo::plan(const Neighbours& nbr, int64_t first, int64_t nlocal, int64_t owned_slots,
+               std::vector<int64_t>* ghost_of, std::string* err) {
+  (void)first;
+  (void)nlocal;
+  ne_ = static_cast<int64_t>(nbr.nb.size() / 4);
+  if (!plan_halo(nbr, ne_, rank_, nranks_, &plan_, err)) return 5;
+  *ghost_of = plan_.ghost_of;
+  owned_slots_ = owned_slots;
+  return 0;
+}
+
+int Halo::bind(void* traces, int vals_per_elem, int elem_bytes, int64_t owned_slots, std::string* err) {
+  (void)traces;
+  vals_ = vals_per_elem;
+  eb_ = elem_bytes;
+  owned_slots_ = owned_slots;
+  const size_t ns = plan_.send_slots.size();
+  cudaError_t e = cudaMalloc(&d_send_slots_, std::max<size_t>(1, ns) * sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMalloc(&d_send_buf_, std::max<size_t>(1, ns) * vals_ * eb_);
+  if (e == cudaSuccess && ns)
+    e = cudaMemcpy(d_send_slots_, plan_.send_slots.data(), ns * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
+  return 0;
+}
+
+int Halo::exchange(cudaStream_t s, void* traces, int elem_bytes, std::string* err) {
+  cudaError_t e = cudaEventRecord(ready_, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cstream_, ready_, 0);
+  const int64_t ns = static_cast<int64_t>(plan_.send_slots.size());
+  if (e == cudaSuccess && ns) {
+    if (elem_bytes == 8)
+      pack_kernel<unsigned long long><<<148 * 4, 256, 0, cstream_>>>(
+          static_cast<const unsigned long long*>(traces), d_send_slots_,
+          static_cast<unsigned long long*>(d_send_buf_), ns, vals_);
+    else
+      pack_kernel<unsigned int><<<148 * 4, 256, 0, cstream_>>>(
+          static_cast<const unsigned int*>(traces), d_send_slots_, static_cast<unsigned int*>(d_send_buf_),
+          ns, vals_);
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
+  const size_t bytes_per = static_cast<size_t>(vals_) * eb_;
+  int r = g_nccl.gstart();
+  for (size_t k = 0; r == 0 && k < plan_.peers.size(); ++k) {
+    const char* sb = static_cast<const char*>(d_send_buf_) + plan_.send_off[k] * bytes_per;
+    r = g_nccl.send(sb, plan_.send_cnt[k] * bytes_per, kNcclUint8, plan_.peers[k], comm_, cstream_);
+    if (r) break;
+    char* rb = static_cast<char*>(traces) + (owned_slots_ + plan_.recv_off[k]) * bytes_per;
+    r = g_nccl.recv(rb, plan_.recv_cnt[k] * bytes_per, kNcclUint8, plan_.peers[k], comm_, cstream_);
+  }
+  int r2 = g_nccl.gend();
+  if (r || r2) { *err = std::string("NCCL: ") + g_nccl.errstr(r ? r : r2); return 4; }
+  e = cudaEventRecord(done_, cstream_);
+  if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
+  return 0;
+}
+
+int Halo::wait(cudaStream_t s, std::string* err) {
+  cudaError_t e = cudaStreamWaitEvent(s, done_, 0);
+  if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
+  return 0;
+}
+
+void Halo::destroy() {
+  if (d_send_slots_) cudaFree(d_send_slots_);
+  if (d_send_buf_) cudaFree(d_send_buf_);
+  d_send_slots_ = nullptr;
+  d_send_buf_ = nullptr;
+  if (comm_ && g_nccl.destroy) g_nccl.destroy(comm_);
+  comm_ = nullptr;
+  if (ready_) cudaEventDestroy(ready_);
+  if (done_) cudaEventDestroy(done_);
+  if (cstream_) cudaStreamDestroy(cstream_);
+  ready_ = done_ = nullptr;
+  cstream_ = nullptr;
+}
+
+}  // namespace ydg

@@ -1,0 +1,59 @@
+// z-slab halo exchange of time-integrated face traces over NCCL (loaded at run time).
+//
+// The neighbour flux reads, for every face, the neighbour's time-integrated
+// trace; across a slab boundary the neighbour lives on another GPU.  Each rank sends the
+// traces of its owned elements that touch a peer's slab and receives the peer's into
+// ghost slots (one NCCL group of send/recv per step, on a side stream).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "setup.h"
+
+namespace ydg {
+
+struct HaloPlan {
+  // ghosts: global ids in slot order (sorted by owner rank, then global id)
+  std::vector<int64_t> ghost_of;
+  std::vector<int> peers;             // peer ranks (ascending)
+  std::vector<int64_t> recv_off;      // first ghost index per peer
+  std::vector<int64_t> recv_cnt;      // ghosts per peer
+  std::vector<int64_t> send_slots;    // local slots to pack, grouped by peer
+  std::vector<int64_t> send_off, send_cnt;
+};
+
+// Pure host: build the plan for rank `rank` of `nranks` owning [first, first+nlocal).
+// Peers own ranges [r*ne/nranks, (r+1)*ne/nranks).
+bool plan_halo(const Neighbours& nbr, int64_t ne, int rank, int nranks, HaloPlan* out,
+               std::string* err);
+
+class Halo {
+ public:
+  int init(int rank, int nranks, const void* uid, std::string* err);
+  int plan(const Neighbours& nbr, int64_t first, int64_t nlocal, int64_t owned_slots,
+           std::vector<int64_t>* ghost_of, std::string* err);
+  int bind(void* traces, int vals_per_elem, int elem_bytes, int64_t owned_slots, std::string* err);
+  // pack + send/recv on the comm stream after `s` reaches this point
+  int exchange(cudaStream_t s, void* traces, int elem_bytes, std::string* err);
+  // make `s` wait for the exchange
+  int wait(cudaStream_t s, std::string* err);
+  void destroy();
+  const HaloPlan& plan_data() const { return plan_; }
+
+ private:
+  int rank_ = 0, nranks_ = 1;
+  int64_t ne_ = 0;
+  void* comm_ = nullptr;
+  cudaStream_t cstream_ = nullptr;
+  cudaEvent_t ready_ = nullptr, done_ = nullptr;
+  HaloPlan plan_;
+  int64_t* d_send_slots_ = nullptr;
+  void* d_send_buf_ = nullptr;
+  int vals_ = 0, eb_ = 0;
+  int64_t owned_slots_ = 0;
+};
+
+}  // namespace ydg

@@ -1,0 +1,145 @@
+// CUDA kernels of the ADER-DG element update for sm_100a (elastic, P = 9).
+//
+// Two launches per time step:
+//   ader_local : CK recursion + time integral, volume,
+//                face traces R^iT I, local flux R^i (T_i A+^T)
+//   ader_neigh : neighbour flux R^i ((f^h T^nb) A-^T) (chain order P:1396)
+// Thread = (element, quantity column); warp = 32 elements (a tile) x one column; CTA =
+// the 9 columns of one tile.  Each nonzero of the global matrices is one FMA with a
+// compile-time constant (generated/ydg_gen_N*.cuh); the per-element 9x9 mixing goes
+// through shared memory laid out [row][quantity][lane] (conflict-free).
+#include "kernels.cuh"
+
+#include <algorithm>
+
+namespace ydg {
+
+// per-order kernel entry points (generated/kernels_N*.cu)
+const void* local_fn_N1(int eb);
+const void* neigh_fn_N1(int eb);
+const void* local_fn_N2(int eb);
+const void* neigh_fn_N2(int eb);
+const void* local_fn_N3(int eb);
+const void* neigh_fn_N3(int eb);
+const void* local_fn_N4(int eb);
+const void* neigh_fn_N4(int eb);
+const void* local_fn_N5(int eb);
+const void* neigh_fn_N5(int eb);
+const void* local_fn_N6(int eb);
+const void* neigh_fn_N6(int eb);
+
+namespace {
+
+constexpr int kP = 9;
+constexpr int kRS = kP * kLanes;
+
+// canonical [e][p][k] <-> tiled [tile][k][p][32]
+template <typename T>
+__global__ void to_tiled_kernel(int P, int B, const T* __restrict__ canon, T* __restrict__ tiled,
+                                int64_t first, int64_t count) {
+  const int64_t n = count * P * B;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t el = i / (P * B);
+    const int r = static_cast<int>(i - el * P * B);
+    const int p = r / B, k = r - p * B;
+    const int64_t e = first + el;
+    tiled[((e / kLanes) * B + k) * P * kLanes + p * kLanes + (e % kLanes)] = canon[i];
+  }
+}
+template <typename T>
+__global__ void to_canonical_kernel(int P, int B, const T* __restrict__ tiled, T* __restrict__ canon,
+                                    int64_t first, int64_t count) {
+  const int64_t n = count * P * B;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t el = i / (P * B);
+    const int r = static_cast<int>(i - el * P * B);
+    const int p = r / B, k = r - p * B;
+    const int64_t e = first + el;
+    canon[i] = tiled[((e / kLanes) * B + k) * P * kLanes + p * kLanes + (e % kLanes)];
+  }
+}
+
+const void* pick_local(int N, int eb) {
+  switch (N) {
+    case 1: return local_fn_N1(eb);
+    case 2: return local_fn_N2(eb);
+    case 3: return local_fn_N3(eb);
+    case 4: return local_fn_N4(eb);
+    case 5: return local_fn_N5(eb);
+    case 6: return local_fn_N6(eb);
+  }
+  return nullptr;
+}
+const void* pick_neigh(int N, int eb) {
+  switch (N) {
+    case 1: return neigh_fn_N1(eb);
+    case 2: return neigh_fn_N2(eb);
+    case 3: return neigh_fn_N3(eb);
+    case 4: return neigh_fn_N4(eb);
+    case 5: return neigh_fn_N5(eb);
+    case 6: return neigh_fn_N6(eb);
+  }
+  return nullptr;
+}
+int nB(int N) { return (N + 1) * (N + 2) * (N + 3) / 6; }
+int nBt(int N) { return (N + 1) * (N + 2) / 2; }
+
+}  // namespace
+
+size_t local_smem_bytes(int N, int eb) {
+  return static_cast<size_t>(std::max(nB(N), 2 * nBt(N)) + 2 * nBt(N)) * kRS * eb;
+}
+size_t neigh_smem_bytes(int N, int eb) { return static_cast<size_t>(4 * nBt(N)) * kRS * eb; }
+
+cudaError_t configure_kernels(int N, int eb) {
+  const void* fl = pick_local(N, eb);
+  const void* fn = pick_neigh(N, eb);
+  if (!fl || !fn) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(fl, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(local_smem_bytes(N, eb)));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(neigh_smem_bytes(N, eb)));
+}
+
+template <typename T>
+cudaError_t launch_local(int N, const StepParams<T>& p, int grid, cudaStream_t s) {
+  const void* f = pick_local(N, sizeof(T));
+  if (!f) return cudaErrorInvalidValue;
+  void* args[] = {const_cast<StepParams<T>*>(&p)};
+  return cudaLaunchKernel(f, dim3(grid), dim3(kP * kLanes), args, local_smem_bytes(N, sizeof(T)), s);
+}
+template <typename T>
+cudaError_t launch_neigh(int N, const StepParams<T>& p, int grid, cudaStream_t s) {
+  const void* f = pick_neigh(N, sizeof(T));
+  if (!f) return cudaErrorInvalidValue;
+  void* args[] = {const_cast<StepParams<T>*>(&p)};
+  return cudaLaunchKernel(f, dim3(grid), dim3(kP * kLanes), args, neigh_smem_bytes(N, sizeof(T)), s);
+}
+template <typename T>
+cudaError_t launch_to_tiled(int P, int B, const T* canon, T* tiled, int64_t first, int64_t count,
+                            cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  to_tiled_kernel<T><<<148 * 8, 256, 0, s>>>(P, B, canon, tiled, first, count);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t launch_to_canonical(int P, int B, const T* tiled, T* canon, int64_t first,
+                                int64_t count, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  to_canonical_kernel<T><<<148 * 8, 256, 0, s>>>(P, B, tiled, canon, first, count);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_local<double>(int, const StepParams<double>&, int, cudaStream_t);
+template cudaError_t launch_local<float>(int, const StepParams<float>&, int, cudaStream_t);
+template cudaError_t launch_neigh<double>(int, const StepParams<double>&, int, cudaStream_t);
+template cudaError_t launch_neigh<float>(int, const StepParams<float>&, int, cudaStream_t);
+template cudaError_t launch_to_tiled<double>(int, int, const double*, double*, int64_t, int64_t, cudaStream_t);
+template cudaError_t launch_to_tiled<float>(int, int, const float*, float*, int64_t, int64_t, cudaStream_t);
+template cudaError_t launch_to_canonical<double>(int, int, const double*, double*, int64_t, int64_t, cudaStream_t);
+template cudaError_t launch_to_canonical<float>(int, int, const float*, float*, int64_t, int64_t, cudaStream_t);
+
+}  // namespace ydg

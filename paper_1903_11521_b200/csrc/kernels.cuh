@@ -1,0 +1,41 @@
+// CUDA kernels of the ADER-DG element update (sm_100a).  Internal header.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ydg {
+
+constexpr int kLanes = 32;   // elements per tile (one warp = one tile, one quantity column)
+constexpr int kMaxN = 6;
+
+template <typename T>
+struct StepParams {
+  T* Q;                  // [tile][k][p][32]  DOFs (updated in place)
+  T* traces;             // [elem][face][m][q] time-integrated face traces R^iT I (AoS)
+  const T* star;         // [tile][c][p][3][32]
+  const T* aplus;        // [tile][face][p][q][32]  (-2|S|/detJ folded in)
+  const T* aminus;       // [tile][face][p][q][32]
+  const int32_t* nb;     // [tile][face][32] neighbour element (local index incl. ghosts)
+  const int8_t* jh;      // [tile][face][32] j | (h << 2)
+  int64_t tile0;         // first tile handled by this launch
+  int64_t ntiles;        // number of tiles handled
+  T scal[2 * kMaxN];     // dt/(d+1), d < N ; dt/(d+2), d < N
+  T dt;
+};
+
+// host launchers (kernels.cu)
+template <typename T>
+cudaError_t launch_local(int N, const StepParams<T>& p, int grid, cudaStream_t s);
+template <typename T>
+cudaError_t launch_neigh(int N, const StepParams<T>& p, int grid, cudaStream_t s);
+template <typename T>
+cudaError_t launch_to_tiled(int P, int B, const T* canon, T* tiled, int64_t first, int64_t count,
+                            cudaStream_t s);
+template <typename T>
+cudaError_t launch_to_canonical(int P, int B, const T* tiled, T* canon, int64_t first,
+                                int64_t count, cudaStream_t s);
+size_t local_smem_bytes(int N, int elem_bytes);
+size_t neigh_smem_bytes(int N, int elem_bytes);
+cudaError_t configure_kernels(int N, int elem_bytes);
+
+}  // namespace ydg

@@ -1,0 +1,220 @@
+// Templated ADER-DG kernels (elastic, P = 9); instantiated per order in
+// generated/kernels_N*.cu so that the large unrolled bodies compile in parallel.
+//
+// Thread = (element lane, quantity column p); warp = one column of a 32-element tile; CTA =
+// the 9 columns of one tile (9 warps: 3 on one SM sub-partition, so <= 168 registers per
+// thread).  Every phase keeps at most one B-long accumulator column in registers; the
+// cross-column mixing by the star matrices and flux solvers reads shared memory laid
+// out [row][q][lane] (each warp load hits 32 consecutive words: conflict-free).
+#pragma once
+#include "kernels.cuh"
+
+namespace ydg {
+template <int N>
+struct Gen;
+}
+
+namespace ydg {
+namespace kimpl {
+
+constexpr int kP = 9;
+constexpr int kRS = kP * kLanes;  // row stride of [row][q][lane]
+
+// 3-column pattern of star-matrix row p (same table as setup.cpp star_cols)
+static __constant__ int c_star_cols[9][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {6, 7, 7}, {7, 8, 8},
+                                             {6, 8, 8}, {0, 3, 5}, {3, 1, 4}, {5, 4, 2}};
+
+// y_m = sum_q Z[m][q] A[p][q] for a 9x9 flux solver row held in registers.
+template <int Bt, typename T>
+__device__ __forceinline__ void mix_rows(const T* Z, const T (&arow)[kP], int lane, T (&y)[Bt]) {
+#pragma unroll
+  for (int m = 0; m < Bt; ++m) {
+    asm volatile("" ::: "memory");  // one row of loads in flight: bounded register pressure
+    const T* row = Z + m * kRS + lane;
+    T s = T(0);
+#pragma unroll
+    for (int q = 0; q < kP; ++q) s = fma(row[q * kLanes], arow[q], s);
+    y[m] = s;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void load_flux_row(const T* base, int64_t tile, int F, int p, int lane,
+                                              T (&arow)[kP]) {
+  const T* A = base + ((tile * 4 + F) * kP + p) * kP * kLanes + lane;
+#pragma unroll
+  for (int q = 0; q < kP; ++q) arow[q] = A[q * kLanes];
+}
+
+// Replace Z (own column, in shared memory) by Y = Z A_F^T for face F.
+template <int Bt, typename T>
+__device__ __forceinline__ void mix_face(T* Z, const T* flux, int64_t tile, int F, int p, int lane) {
+  T y[Bt];
+  {
+    T arow[kP];
+    load_flux_row(flux, tile, F, p, lane, arow);
+    mix_rows<Bt>(Z, arow, lane, y);
+  }
+  __syncthreads();  // every column of Z has been read
+#pragma unroll
+  for (int m = 0; m < Bt; ++m) Z[m * kRS + p * kLanes + lane] = y[m];
+}
+
+template <typename T, int B>
+__device__ __forceinline__ void add_to_q(T* Qt, const T (&acc)[B]) {
+#pragma unroll
+  for (int k0 = 0; k0 < B; k0 += 8) {
+    asm volatile("" ::: "memory");  // at most 8 loads of Q in flight
+#pragma unroll
+    for (int k = k0; k < (k0 + 8 < B ? k0 + 8 : B); ++k) Qt[k * kRS] += acc[k];
+  }
+}
+
+// Local part of the update: CK recursion + time integral, volume
+// (P:1338-1340), traces T_i = R^iT I (stored for the neighbours) and the local flux
+// R^i (T_i A+_i^T).  Shared memory: S [B][9][32] and Z0, Z1 [Bt][9][32].
+template <int N, typename T>
+__global__ void __launch_bounds__(kP * kLanes, 1) ader_local(const StepParams<T> prm) {
+  using G = Gen<N>;
+  constexpr int B = G::B, Bt = G::Bt;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* S = reinterpret_cast<T*>(smem_raw);  // [max(B, 2Bt)][9][32]
+  constexpr int SR = B > 2 * Bt ? B : 2 * Bt;
+  T* Z0 = S + SR * kRS;                    // [Bt][9][32]
+  T* Z1 = Z0 + Bt * kRS;
+  T* Z2 = S;                                // aliases rows [0, Bt) of S once S is dead
+  T* Z3 = S + Bt * kRS;
+  const int lane = threadIdx.x & 31, p = threadIdx.x >> 5;
+  const int c0 = c_star_cols[p][0], c1 = c_star_cols[p][1], c2 = c_star_cols[p][2];
+  const int own = p * kLanes + lane;
+  for (int64_t it = blockIdx.x; it < prm.ntiles; it += gridDim.x) {
+    const int64_t tile = prm.tile0 + it;
+    T* Qt = prm.Q + tile * B * kRS + own;
+#pragma unroll 8
+    for (int k = 0; k < B; ++k) S[k * kRS + own] = Qt[k * kRS];
+    T a[9];
+    const T* st = prm.star + (tile * 3 * kP) * 3 * kLanes + lane;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) a[3 * c + j] = st[((c * kP + p) * 3 + j) * kLanes];
+    __syncthreads();
+    {
+      T I[G::Bv];
+      G::template ck<T>(S + c0 * kLanes + lane, S + c1 * kLanes + lane, S + c2 * kLanes + lane,
+                        S + own, a, I, prm.scal, prm.dt);
+      // ck ends with a barrier; the own column now receives the time integral: rows < Bv
+      // from I, rows >= Bv are dt * Q (still in shared memory)
+#pragma unroll
+      for (int k = 0; k < G::Bv; ++k) S[k * kRS + own] = I[k];
+#pragma unroll 8
+      for (int k = G::Bv; k < B; ++k) S[k * kRS + own] = prm.dt * S[k * kRS + own];
+    }
+    __syncthreads();
+    {
+      T acc[B];
+#pragma unroll
+      for (int k = 0; k < B; ++k) acc[k] = T(0);
+      G::template volume<T>(S + c0 * kLanes + lane, S + c1 * kLanes + lane, S + c2 * kLanes + lane, a,
+                            acc);
+      add_to_q(Qt, acc);
+    }
+    // traces of the time integral on the four faces (own column), stored for the
+    // neighbour kernel ([elem][face][m][q]) and staged for the flux solvers
+    const int64_t e = tile * kLanes + lane;
+    T* tr = prm.traces + (e * 4 * Bt) * kP + p;
+    {
+      T ta[Bt], tb[Bt];
+      G::template trace<0, T>(S + own, ta);
+      G::template trace<1, T>(S + own, tb);
+#pragma unroll
+      for (int m = 0; m < Bt; ++m) {
+        tr[(0 * Bt + m) * kP] = ta[m];
+        tr[(1 * Bt + m) * kP] = tb[m];
+        Z0[m * kRS + own] = ta[m];
+        Z1[m * kRS + own] = tb[m];
+      }
+      G::template trace<2, T>(S + own, ta);
+      G::template trace<3, T>(S + own, tb);
+      __syncthreads();  // S (time integral) is dead: stage faces 2, 3 in its rows
+#pragma unroll
+      for (int m = 0; m < Bt; ++m) {
+        tr[(2 * Bt + m) * kP] = ta[m];
+        tr[(3 * Bt + m) * kP] = tb[m];
+        Z2[m * kRS + own] = ta[m];
+        Z3[m * kRS + own] = tb[m];
+      }
+    }
+    __syncthreads();
+    mix_face<Bt>(Z0, prm.aplus, tile, 0, p, lane);
+    mix_face<Bt>(Z1, prm.aplus, tile, 1, p, lane);
+    mix_face<Bt>(Z2, prm.aplus, tile, 2, p, lane);
+    mix_face<Bt>(Z3, prm.aplus, tile, 3, p, lane);
+    __syncthreads();
+    {
+      T acc[B];
+#pragma unroll
+      for (int k = 0; k < B; ++k) acc[k] = T(0);
+      G::template lift<0, T>(Z0 + own, acc);
+      G::template lift<1, T>(Z1 + own, acc);
+      G::template lift<2, T>(Z2 + own, acc);
+      G::template lift<3, T>(Z3 + own, acc);
+      add_to_q(Qt, acc);
+    }
+    __syncthreads();  // before the next tile overwrites S / Z
+  }
+}
+
+template <int N, typename T, int F>
+__device__ __forceinline__ void neigh_gather(const StepParams<T>& prm, int64_t tile, int p, int lane,
+                                            T* ZF) {
+  using G = Gen<N>;
+  constexpr int Bt = G::Bt;
+  const int64_t slot = (tile * 4 + F) * kLanes + lane;
+  const int64_t nbe = prm.nb[slot];
+  const int jh = prm.jh[slot];
+  const int j = jh & 3, h = jh >> 2;
+  const T* src = prm.traces + ((nbe * 4 + j) * Bt) * kP + p;
+  T tn[Bt];
+#pragma unroll
+  for (int n = 0; n < Bt; ++n) tn[n] = src[n * kP];
+  T* dst = ZF + p * kLanes + lane;
+  G::template rot<T>(h, tn, [&](int m, T z) { dst[m * kRS] = z; });
+}
+
+// Neighbour flux (chain order P:1396): Q += sum_i R^i ((f^h_i T^nb_(j_i)) A-_i^T).
+// Shared memory: Z [4][Bt][9][32].
+template <int N, typename T>
+__global__ void __launch_bounds__(kP * kLanes, 1) ader_neigh(const StepParams<T> prm) {
+  using G = Gen<N>;
+  constexpr int B = G::B, Bt = G::Bt;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Z = reinterpret_cast<T*>(smem_raw);
+  const int lane = threadIdx.x & 31, p = threadIdx.x >> 5;
+  const int own = p * kLanes + lane;
+  for (int64_t it = blockIdx.x; it < prm.ntiles; it += gridDim.x) {
+    const int64_t tile = prm.tile0 + it;
+    neigh_gather<N, T, 0>(prm, tile, p, lane, Z + 0 * Bt * kRS);
+    neigh_gather<N, T, 1>(prm, tile, p, lane, Z + 1 * Bt * kRS);
+    neigh_gather<N, T, 2>(prm, tile, p, lane, Z + 2 * Bt * kRS);
+    neigh_gather<N, T, 3>(prm, tile, p, lane, Z + 3 * Bt * kRS);
+    __syncthreads();
+    mix_face<Bt>(Z + 0 * Bt * kRS, prm.aminus, tile, 0, p, lane);
+    mix_face<Bt>(Z + 1 * Bt * kRS, prm.aminus, tile, 1, p, lane);
+    mix_face<Bt>(Z + 2 * Bt * kRS, prm.aminus, tile, 2, p, lane);
+    mix_face<Bt>(Z + 3 * Bt * kRS, prm.aminus, tile, 3, p, lane);
+    __syncthreads();
+    T acc[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) acc[k] = T(0);
+    G::template lift<0, T>(Z + 0 * Bt * kRS + own, acc);
+    G::template lift<1, T>(Z + 1 * Bt * kRS + own, acc);
+    G::template lift<2, T>(Z + 2 * Bt * kRS + own, acc);
+    G::template lift<3, T>(Z + 3 * Bt * kRS + own, acc);
+    add_to_q(prm.Q + tile * B * kRS + own, acc);
+    __syncthreads();
+  }
+}
+
+}  // namespace kimpl
+}  // namespace ydg

@@ -1,0 +1,40 @@
+// Host-side setup of the ADER-DG element update: mesh validation, face matching,
+// geometry, star matrices and Godunov flux solvers (fp64).  Shares no code with the test oracle.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace ydg {
+
+// local faces as outward-oriented vertex triples (reading R7)
+constexpr int kFaces[4][3] = {{0, 2, 1}, {0, 1, 3}, {0, 3, 2}, {1, 2, 3}};
+
+struct Neighbours {
+  std::vector<int64_t> nb;  // [ne][4] Neigh
+  std::vector<int8_t> j;    // [ne][4] Face
+  std::vector<int8_t> h;    // [ne][4] Rot
+};
+
+// Match faces by sorted vertex-id triples.  Returns false and sets err on a mesh error.
+bool match_faces(int64_t ne, const int64_t* vid, Neighbours* out, std::string* err);
+
+struct ElementCoeffs {
+  // per element, fp64, for P quantities:
+  //  star: [3][P][3] values of A*^c at the fixed 3-column pattern of row p (star_cols)
+  //  aplus / aminus: [4][P][P] flux solvers with -2|S_i|/det J folded in (row-major p,q)
+  //  src: [P][P] viscoelastic source E (P = 27 only)
+  std::vector<double> star, aplus, aminus, src;
+};
+
+// Columns of the star-matrix pattern of row p (3 per row; unused slots repeat a column
+// with a zero coefficient).  Valid for P = 9 and P = 27.
+void star_cols(int P, int p, int cols[3]);
+
+// Compute coefficients for elements [e0, e0+n) of the global mesh.
+//  anelastic: NULL or [3] omega then [ne][3][2] (Ylam, Ymu).
+bool element_coeffs(int P, int64_t e0, int64_t n, const double* xyz, const double* material,
+                    const double* anelastic, const Neighbours& nbr, ElementCoeffs* out,
+                    std::string* err);
+
+}  // namespace ydg
