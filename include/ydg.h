@@ -129,6 +129,17 @@ int ydg_get_neighbours(ydg_solver* h, int64_t first, int64_t count, int64_t* nb,
  * the totals; ydg_query(YDG_Q_PROF_*) synchronises with the recorded events. */
 int ydg_profile(ydg_solver* h, int enable);
 
+/* Host-only helper (no device needed): the z-slab halo plan ydg_set_comm + ydg_upload_mesh
+ * would build for `rank` of `nranks` on the mesh given by elem_vid [ne][4].
+ *  counts[3] <- (number of peers, number of ghost elements, number of sent elements).
+ *  If the array arguments are non-NULL they must hold counts[] entries and receive:
+ *  peers[np] (ascending), recv_cnt[np], send_cnt[np], ghost_of[ng] (global ids of the
+ *  ghost slots, grouped by peer, ascending within a peer) and send_elem[ns] (global ids
+ *  sent, grouped by peer, ascending) -- a peer's send list equals our ghost list from it. */
+int ydg_halo_plan(int64_t n_elements, const int64_t* elem_vid, int rank, int nranks,
+                  int64_t* counts, int32_t* peers, int64_t* recv_cnt, int64_t* send_cnt,
+                  int64_t* ghost_of, int64_t* send_elem);
+
 /* Query a scalar (see YDG_Q_*). */
 int ydg_query(ydg_solver* h, int what, double* value);
 

@@ -31,8 +31,8 @@ YDG_OK, YDG_ERR_ARG, YDG_ERR_STATE, YDG_ERR_CUDA, YDG_ERR_NCCL, YDG_ERR_MESH, YD
 
 EXPORTS = ("ydg_create", "ydg_last_error", "ydg_set_comm", "ydg_upload_mesh", "ydg_upload_dofs",
            "ydg_upload_dofs_device", "ydg_download_dofs_device", "ydg_step", "ydg_synchronize",
-           "ydg_download_dofs", "ydg_get_neighbours", "ydg_profile", "ydg_query", "ydg_error_string",
-           "ydg_destroy")
+           "ydg_download_dofs", "ydg_get_neighbours", "ydg_halo_plan", "ydg_profile", "ydg_query",
+           "ydg_error_string", "ydg_destroy")
 
 
 class YdgError(RuntimeError):
@@ -64,6 +64,7 @@ def lib():
         L.ydg_download_dofs.argtypes = [vp, i64, i64, vp]
         L.ydg_get_neighbours.argtypes = [vp, i64, i64, vp, vp, vp]
         L.ydg_profile.argtypes = [vp, i32]
+        L.ydg_halo_plan.argtypes = [i64, vp, i32, i32, vp, vp, vp, vp, vp, vp]
         L.ydg_query.argtypes = [vp, i32, ctypes.POINTER(dbl)]
         L.ydg_error_string.argtypes = [vp]
         L.ydg_error_string.restype = ctypes.c_char_p
@@ -155,6 +156,29 @@ def ydg_get_neighbours(h, first, count):
     _check(h, lib().ydg_get_neighbours(h.ptr, first, count, nb.ctypes.data_as(ctypes.c_void_p),
                                        j.ctypes.data_as(ctypes.c_void_p), hr.ctypes.data_as(ctypes.c_void_p)))
     return nb, j, hr
+
+
+def ydg_halo_plan(elem_vid, rank, nranks):
+    """Host-only: the z-slab halo plan of `rank` (dict of numpy arrays); no GPU needed."""
+    vid, pvid = _c(elem_vid, np.int64)
+    counts = np.zeros(3, dtype=np.int64)
+    P = ctypes.c_void_p
+    rc = lib().ydg_halo_plan(vid.shape[0], pvid, rank, nranks, counts.ctypes.data_as(P), None, None, None,
+                             None, None)
+    if rc != YDG_OK:
+        raise YdgError(rc, lib().ydg_last_error().decode())
+    npeer, ng, ns = (int(x) for x in counts)
+    peers = np.zeros(npeer, dtype=np.int32)
+    rcnt = np.zeros(npeer, dtype=np.int64)
+    scnt = np.zeros(npeer, dtype=np.int64)
+    ghost = np.zeros(ng, dtype=np.int64)
+    send = np.zeros(ns, dtype=np.int64)
+    rc = lib().ydg_halo_plan(vid.shape[0], pvid, rank, nranks, counts.ctypes.data_as(P), peers.ctypes.data_as(P),
+                             rcnt.ctypes.data_as(P), scnt.ctypes.data_as(P), ghost.ctypes.data_as(P),
+                             send.ctypes.data_as(P))
+    if rc != YDG_OK:
+        raise YdgError(rc, lib().ydg_last_error().decode())
+    return {"peers": peers, "recv_cnt": rcnt, "send_cnt": scnt, "ghost_of": ghost, "send_elem": send}
 
 
 def ydg_profile(h, enable=True):

@@ -410,6 +410,8 @@ static int xfer_dofs(ydg_solver* h, int64_t first, int64_t count, const void* sr
   if (!h->have_mesh) return fail(h, YDG_ERR_STATE, "upload the mesh first");
   if (count < 0 || first < h->first || first + count > h->first + h->nlocal)
     return fail(h, YDG_ERR_ARG, "element range not owned by this rank");
+  // host transfers are blocking: wait for steps enqueued on any stream
+  if (!src_dev && !dst_dev) CUDA_OR_FAIL(h, cudaDeviceSynchronize());
   const int eb = elem_bytes(h);
   const int64_t per = static_cast<int64_t>(h->P) * h->B;
   const bool dev_side = src_dev || dst_dev;
@@ -450,10 +452,7 @@ int ydg_upload_dofs(ydg_solver* h, int64_t first, int64_t count, const void* Q) 
 }
 int ydg_download_dofs(ydg_solver* h, int64_t first, int64_t count, void* Q_out) {
   if (!Q_out) return h ? fail(h, YDG_ERR_ARG, "null Q_out") : YDG_ERR_ARG;
-  int rc = h ? check(h) : YDG_ERR_ARG;
-  if (rc) return rc;
-  CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
-  return xfer_dofs(h, first, count, nullptr, Q_out, nullptr, nullptr, h->stream, false);
+  return xfer_dofs(h, first, count, nullptr, Q_out, nullptr, nullptr, h ? h->stream : nullptr, false);
 }
 int ydg_upload_dofs_device(ydg_solver* h, int64_t first, int64_t count, const void* Q_dev, void* s) {
   if (!Q_dev) return h ? fail(h, YDG_ERR_ARG, "null Q_dev") : YDG_ERR_ARG;
@@ -490,6 +489,37 @@ int ydg_get_neighbours(ydg_solver* h, int64_t first, int64_t count, int64_t* nb,
   std::memcpy(nb, h->nbr.nb.data() + first * 4, count * 4 * sizeof(int64_t));
   std::memcpy(j, h->nbr.j.data() + first * 4, count * 4);
   std::memcpy(hr, h->nbr.h.data() + first * 4, count * 4);
+  return YDG_OK;
+}
+
+int ydg_halo_plan(int64_t ne, const int64_t* vid, int rank, int nranks, int64_t* counts,
+                  int32_t* peers, int64_t* recv_cnt, int64_t* send_cnt, int64_t* ghost_of,
+                  int64_t* send_elem) {
+  if (ne <= 0 || !vid || !counts || nranks < 1 || rank < 0 || rank >= nranks) return YDG_ERR_ARG;
+  Neighbours nbr;
+  std::string err;
+  if (!match_faces(ne, vid, &nbr, &err)) {
+    g_last_error = err;
+    return YDG_ERR_MESH;
+  }
+  HaloPlan plan;
+  if (!plan_halo(nbr, ne, rank, nranks, &plan, &err)) {
+    g_last_error = err;
+    return YDG_ERR_MESH;
+  }
+  counts[0] = static_cast<int64_t>(plan.peers.size());
+  counts[1] = static_cast<int64_t>(plan.ghost_of.size());
+  counts[2] = static_cast<int64_t>(plan.send_slots.size());
+  const int64_t first = ne * rank / nranks;
+  if (peers && recv_cnt && send_cnt)
+    for (size_t k = 0; k < plan.peers.size(); ++k) {
+      peers[k] = plan.peers[k];
+      recv_cnt[k] = plan.recv_cnt[k];
+      send_cnt[k] = plan.send_cnt[k];
+    }
+  if (ghost_of) std::copy(plan.ghost_of.begin(), plan.ghost_of.end(), ghost_of);
+  if (send_elem)
+    for (size_t k = 0; k < plan.send_slots.size(); ++k) send_elem[k] = first + plan.send_slots[k];
   return YDG_OK;
 }
 
