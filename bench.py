@@ -249,8 +249,12 @@ def run_ydg(args):
     ydg.ydg_upload_dofs(h, first, Qh)
     ydg.ydg_synchronize(h)
     setup_s = time.time() - t_setup
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream: the library enqueues on it and the events below
+    # are recorded on it (the legacy default stream would be handle 0 = the library's own)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
+    assert sptr != 0
 
     # warm-up
     for _ in range(args.warmup):

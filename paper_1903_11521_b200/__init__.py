@@ -20,7 +20,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libydg.so")
+LIB_PATH = os.environ.get("YDG_LIB") or os.path.join(_HERE, "libydg.so")
 
 YDG_OK, YDG_ERR_ARG, YDG_ERR_STATE, YDG_ERR_CUDA, YDG_ERR_NCCL, YDG_ERR_MESH, YDG_ERR_OOM, \
     YDG_ERR_UNSUPPORTED = range(8)

@@ -16,13 +16,13 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libydg.so")
+BUILD = os.environ.get("YDG_BUILD_DIR") or os.path.join(HERE, "_build")
+LIB = os.environ.get("YDG_LIB") or os.path.join(HERE, "libydg.so")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
-                  "-I", CSRC, "--expt-relaxed-constexpr"]
+                  "-I", CSRC, "--expt-relaxed-constexpr"] + os.environ.get("YDG_NVFLAGS", "").split()
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-fopenmp", "-I", CSRC, "-I", os.path.join(CUDA, "include")]
 
 

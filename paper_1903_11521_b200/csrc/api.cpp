@@ -164,12 +164,19 @@ int upload_coeffs(ydg_solver* h, const double* xyz, const double* material, cons
   return YDG_OK;
 }
 
+// Algorithmic HBM bytes per element of each kernel (each array touched once).
+// fp64 (tensor-core kernels): local reads Q, star, writes Q and the 4 traces; the flux
+// kernel reads Q, own + neighbour traces, A+ and A-, writes Q.  fp32 (sparse kernels):
+// the local kernel also reads A+ (local flux), the neighbour kernel reads A- only and the
+// neighbour traces.
 double alg_bytes_local(const ydg_solver* h) {
   const double P = h->P, B = h->B, Bt = h->Bt;
+  if (h->prec == 8) return (2 * B * P + 3 * P * 3 + 4 * Bt * P) * elem_bytes(h);
   return (2 * B * P + 3 * P * 3 + 4 * P * P + 4 * Bt * P) * elem_bytes(h);
 }
 double alg_bytes_neigh(const ydg_solver* h) {
   const double P = h->P, B = h->B, Bt = h->Bt;
+  if (h->prec == 8) return (2 * B * P + 2 * 4 * P * P + 2 * 4 * Bt * P) * elem_bytes(h) + 4 * (4 + 1);
   return (2 * B * P + 4 * P * P + 4 * Bt * P) * elem_bytes(h) + 4 * (4 + 1);
 }
 
@@ -386,7 +393,7 @@ int ydg_upload_mesh(ydg_solver* h, int64_t ne, const double* xyz, const int64_t*
   rc = eb == 8 ? upload_coeffs<double>(h, xyz, material, anelastic) : upload_coeffs<float>(h, xyz, material, anelastic);
   if (rc) { free_mesh(h); return rc; }
   if (h->nranks > 1) {
-    rc = h->halo.bind(h->traces, 4 * h->Bt * h->P, eb, owned_slots, &h->err);
+    rc = h->halo.bind(h->traces, h->Bt, h->P, eb, owned_slots, &h->err);
     if (rc) { free_mesh(h); return fail(h, rc, h->err); }
   }
   // staging buffer for DOF transfers (bounded)
@@ -547,7 +554,7 @@ int ydg_query(ydg_solver* h, int what, double* v) {
     case YDG_Q_N_ELEMENTS: *v = static_cast<double>(h->ne); break;
     case YDG_Q_FIRST_LOCAL: *v = static_cast<double>(h->first); break;
     case YDG_Q_N_LOCAL: *v = static_cast<double>(h->nlocal); break;
-    case YDG_Q_NZ_FLOPS: *v = nz_flops_elastic(h->N); break;
+    case YDG_Q_NZ_FLOPS: *v = nz_flops_elastic(h->N, h->prec == 8); break;
     case YDG_Q_ALG_BYTES: *v = alg_bytes_local(h) + alg_bytes_neigh(h); break;
     case YDG_Q_B: *v = h->B; break;
     case YDG_Q_BTILDE: *v = h->Bt; break;
@@ -555,8 +562,8 @@ int ydg_query(ydg_solver* h, int what, double* v) {
     case YDG_Q_LAUNCHES_PER_STEP: *v = h->nranks > 1 ? 5 : 2; break;
     case YDG_Q_LOCAL_BYTES: *v = alg_bytes_local(h); break;
     case YDG_Q_NEIGH_BYTES: *v = alg_bytes_neigh(h); break;
-    case YDG_Q_LOCAL_FLOPS: *v = nz_flops_local(h->N); break;
-    case YDG_Q_NEIGH_FLOPS: *v = nz_flops_elastic(h->N) - nz_flops_local(h->N); break;
+    case YDG_Q_LOCAL_FLOPS: *v = nz_flops_local(h->N, h->prec == 8); break;
+    case YDG_Q_NEIGH_FLOPS: *v = nz_flops_elastic(h->N, h->prec == 8) - nz_flops_local(h->N, h->prec == 8); break;
     default: return fail(h, YDG_ERR_ARG, "unknown query");
   }
   return YDG_OK;

@@ -51,19 +51,36 @@ struct Nccl {
 };
 Nccl g_nccl;
 
-template <int EB>
-struct Word;
-template <> struct Word<8> { typedef unsigned long long t; };
-template <> struct Word<4> { typedef unsigned int t; };
+// index of value v (= (face, m, q) flattened) of local element slot s in the tiled trace
+// layout [tile][face][m][q][32]
+__device__ __forceinline__ int64_t tiled_index(int64_t s, int v, int Bt, int P) {
+  const int F = v / (Bt * P), m = (v / P) % Bt, q = v % P;
+  return (((s >> 5) * 4 + F) * Bt + m) * (int64_t)(P * 32) + q * 32 + (s & 31);
+}
 
 template <typename W>
 __global__ void pack_kernel(const W* __restrict__ traces, const int64_t* __restrict__ slots,
-                            W* __restrict__ out, int64_t n, int vals) {
+                            W* __restrict__ out, int64_t n, int Bt, int P) {
+  const int vals = 4 * Bt * P;
   const int64_t total = n * vals;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = i / vals, v = i - s * vals;
-    out[i] = traces[slots[s] * vals + v];
+    const int64_t s = i / vals;
+    const int v = static_cast<int>(i - s * vals);
+    out[i] = traces[tiled_index(slots[s], v, Bt, P)];
+  }
+}
+
+template <typename W>
+__global__ void unpack_kernel(const W* __restrict__ in, W* __restrict__ traces, int64_t first_slot,
+                              int64_t n, int Bt, int P) {
+  const int vals = 4 * Bt * P;
+  const int64_t total = n * vals;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = i / vals;
+    const int v = static_cast<int>(i - g * vals);
+    traces[tiled_index(first_slot + g, v, Bt, P)] = in[i];
   }
 }
 
@@ -159,14 +176,17 @@ int Halo::plan(const Neighbours& nbr, int64_t first, int64_t nlocal, int64_t own
   return 0;
 }
 
-int Halo::bind(void* traces, int vals_per_elem, int elem_bytes, int64_t owned_slots, std::string* err) {
+int Halo::bind(void* traces, int Bt, int P, int elem_bytes, int64_t owned_slots, std::string* err) {
   (void)traces;
-  vals_ = vals_per_elem;
+  Bt_ = Bt;
+  P_ = P;
+  vals_ = 4 * Bt * P;
   eb_ = elem_bytes;
   owned_slots_ = owned_slots;
-  const size_t ns = plan_.send_slots.size();
+  const size_t ns = plan_.send_slots.size(), ng = plan_.ghost_of.size();
   cudaError_t e = cudaMalloc(&d_send_slots_, std::max<size_t>(1, ns) * sizeof(int64_t));
   if (e == cudaSuccess) e = cudaMalloc(&d_send_buf_, std::max<size_t>(1, ns) * vals_ * eb_);
+  if (e == cudaSuccess) e = cudaMalloc(&d_recv_buf_, std::max<size_t>(1, ng) * vals_ * eb_);
   if (e == cudaSuccess && ns)
     e = cudaMemcpy(d_send_slots_, plan_.send_slots.data(), ns * sizeof(int64_t), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
@@ -177,15 +197,16 @@ int Halo::exchange(cudaStream_t s, void* traces, int elem_bytes, std::string* er
   cudaError_t e = cudaEventRecord(ready_, s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(cstream_, ready_, 0);
   const int64_t ns = static_cast<int64_t>(plan_.send_slots.size());
+  const int64_t ng = static_cast<int64_t>(plan_.ghost_of.size());
   if (e == cudaSuccess && ns) {
     if (elem_bytes == 8)
       pack_kernel<unsigned long long><<<148 * 4, 256, 0, cstream_>>>(
           static_cast<const unsigned long long*>(traces), d_send_slots_,
-          static_cast<unsigned long long*>(d_send_buf_), ns, vals_);
+          static_cast<unsigned long long*>(d_send_buf_), ns, Bt_, P_);
     else
       pack_kernel<unsigned int><<<148 * 4, 256, 0, cstream_>>>(
           static_cast<const unsigned int*>(traces), d_send_slots_, static_cast<unsigned int*>(d_send_buf_),
-          ns, vals_);
+          ns, Bt_, P_);
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
@@ -195,11 +216,23 @@ int Halo::exchange(cudaStream_t s, void* traces, int elem_bytes, std::string* er
     const char* sb = static_cast<const char*>(d_send_buf_) + plan_.send_off[k] * bytes_per;
     r = g_nccl.send(sb, plan_.send_cnt[k] * bytes_per, kNcclUint8, plan_.peers[k], comm_, cstream_);
     if (r) break;
-    char* rb = static_cast<char*>(traces) + (owned_slots_ + plan_.recv_off[k]) * bytes_per;
+    char* rb = static_cast<char*>(d_recv_buf_) + plan_.recv_off[k] * bytes_per;
     r = g_nccl.recv(rb, plan_.recv_cnt[k] * bytes_per, kNcclUint8, plan_.peers[k], comm_, cstream_);
   }
   int r2 = g_nccl.gend();
   if (r || r2) { *err = std::string("NCCL: ") + g_nccl.errstr(r ? r : r2); return 4; }
+  if (ng) {
+    if (elem_bytes == 8)
+      unpack_kernel<unsigned long long><<<148 * 4, 256, 0, cstream_>>>(
+          static_cast<const unsigned long long*>(d_recv_buf_), static_cast<unsigned long long*>(traces),
+          owned_slots_, ng, Bt_, P_);
+    else
+      unpack_kernel<unsigned int><<<148 * 4, 256, 0, cstream_>>>(
+          static_cast<const unsigned int*>(d_recv_buf_), static_cast<unsigned int*>(traces), owned_slots_,
+          ng, Bt_, P_);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
+  }
   e = cudaEventRecord(done_, cstream_);
   if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
   return 0;
@@ -214,8 +247,10 @@ int Halo::wait(cudaStream_t s, std::string* err) {
 void Halo::destroy() {
   if (d_send_slots_) cudaFree(d_send_slots_);
   if (d_send_buf_) cudaFree(d_send_buf_);
+  if (d_recv_buf_) cudaFree(d_recv_buf_);
   d_send_slots_ = nullptr;
   d_send_buf_ = nullptr;
+  d_recv_buf_ = nullptr;
   if (comm_ && g_nccl.destroy) g_nccl.destroy(comm_);
   comm_ = nullptr;
   if (ready_) cudaEventDestroy(ready_);

@@ -35,7 +35,8 @@ class Halo {
   int init(int rank, int nranks, const void* uid, std::string* err);
   int plan(const Neighbours& nbr, int64_t first, int64_t nlocal, int64_t owned_slots,
            std::vector<int64_t>* ghost_of, std::string* err);
-  int bind(void* traces, int vals_per_elem, int elem_bytes, int64_t owned_slots, std::string* err);
+  // traces use the tiled layout [tile][face][m][q][32] with Bt face functions, P quantities
+  int bind(void* traces, int Bt, int P, int elem_bytes, int64_t owned_slots, std::string* err);
   // pack + send/recv on the comm stream after `s` reaches this point
   int exchange(cudaStream_t s, void* traces, int elem_bytes, std::string* err);
   // make `s` wait for the exchange
@@ -52,7 +53,8 @@ class Halo {
   HaloPlan plan_;
   int64_t* d_send_slots_ = nullptr;
   void* d_send_buf_ = nullptr;
-  int vals_ = 0, eb_ = 0;
+  void* d_recv_buf_ = nullptr;
+  int vals_ = 0, eb_ = 0, Bt_ = 0, P_ = 0;
   int64_t owned_slots_ = 0;
 };
 

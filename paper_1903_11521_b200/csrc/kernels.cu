@@ -17,16 +17,28 @@ namespace ydg {
 // per-order kernel entry points (generated/kernels_N*.cu)
 const void* local_fn_N1(int eb);
 const void* neigh_fn_N1(int eb);
+size_t local_smem_N1(int eb);
+size_t neigh_smem_N1(int eb);
 const void* local_fn_N2(int eb);
 const void* neigh_fn_N2(int eb);
+size_t local_smem_N2(int eb);
+size_t neigh_smem_N2(int eb);
 const void* local_fn_N3(int eb);
 const void* neigh_fn_N3(int eb);
+size_t local_smem_N3(int eb);
+size_t neigh_smem_N3(int eb);
 const void* local_fn_N4(int eb);
 const void* neigh_fn_N4(int eb);
+size_t local_smem_N4(int eb);
+size_t neigh_smem_N4(int eb);
 const void* local_fn_N5(int eb);
 const void* neigh_fn_N5(int eb);
+size_t local_smem_N5(int eb);
+size_t neigh_smem_N5(int eb);
 const void* local_fn_N6(int eb);
 const void* neigh_fn_N6(int eb);
+size_t local_smem_N6(int eb);
+size_t neigh_smem_N6(int eb);
 
 namespace {
 
@@ -88,10 +100,33 @@ int nBt(int N) { return (N + 1) * (N + 2) / 2; }
 
 }  // namespace
 
-size_t local_smem_bytes(int N, int eb) {
+size_t sparse_local_smem(int N, int eb) {
   return static_cast<size_t>(std::max(nB(N), 2 * nBt(N)) + 2 * nBt(N)) * kRS * eb;
 }
-size_t neigh_smem_bytes(int N, int eb) { return static_cast<size_t>(4 * nBt(N)) * kRS * eb; }
+size_t sparse_neigh_smem(int N, int eb) { return static_cast<size_t>(4 * nBt(N)) * kRS * eb; }
+
+size_t local_smem_bytes(int N, int eb) {
+  switch (N) {
+    case 1: return local_smem_N1(eb);
+    case 2: return local_smem_N2(eb);
+    case 3: return local_smem_N3(eb);
+    case 4: return local_smem_N4(eb);
+    case 5: return local_smem_N5(eb);
+    case 6: return local_smem_N6(eb);
+  }
+  return 0;
+}
+size_t neigh_smem_bytes(int N, int eb) {
+  switch (N) {
+    case 1: return neigh_smem_N1(eb);
+    case 2: return neigh_smem_N2(eb);
+    case 3: return neigh_smem_N3(eb);
+    case 4: return neigh_smem_N4(eb);
+    case 5: return neigh_smem_N5(eb);
+    case 6: return neigh_smem_N6(eb);
+  }
+  return 0;
+}
 
 cudaError_t configure_kernels(int N, int eb) {
   const void* fl = pick_local(N, eb);

@@ -35,6 +35,8 @@ template <typename T>
 cudaError_t launch_to_canonical(int P, int B, const T* tiled, T* canon, int64_t first,
                                 int64_t count, cudaStream_t s);
 size_t local_smem_bytes(int N, int elem_bytes);
+size_t sparse_local_smem(int N, int elem_bytes);
+size_t sparse_neigh_smem(int N, int elem_bytes);
 size_t neigh_smem_bytes(int N, int elem_bytes);
 cudaError_t configure_kernels(int N, int elem_bytes);
 

@@ -121,16 +121,16 @@ __global__ void __launch_bounds__(kP * kLanes, 1) ader_local(const StepParams<T>
     }
     // traces of the time integral on the four faces (own column), stored for the
     // neighbour kernel ([elem][face][m][q]) and staged for the flux solvers
-    const int64_t e = tile * kLanes + lane;
-    T* tr = prm.traces + (e * 4 * Bt) * kP + p;
+    // tiled trace layout [tile][face][m][q][32]
+    T* tr = prm.traces + tile * 4 * Bt * kRS + p * kLanes + lane;
     {
       T ta[Bt], tb[Bt];
       G::template trace<0, T>(S + own, ta);
       G::template trace<1, T>(S + own, tb);
 #pragma unroll
       for (int m = 0; m < Bt; ++m) {
-        tr[(0 * Bt + m) * kP] = ta[m];
-        tr[(1 * Bt + m) * kP] = tb[m];
+        tr[(0 * Bt + m) * kRS] = ta[m];
+        tr[(1 * Bt + m) * kRS] = tb[m];
         Z0[m * kRS + own] = ta[m];
         Z1[m * kRS + own] = tb[m];
       }
@@ -139,8 +139,8 @@ __global__ void __launch_bounds__(kP * kLanes, 1) ader_local(const StepParams<T>
       __syncthreads();  // S (time integral) is dead: stage faces 2, 3 in its rows
 #pragma unroll
       for (int m = 0; m < Bt; ++m) {
-        tr[(2 * Bt + m) * kP] = ta[m];
-        tr[(3 * Bt + m) * kP] = tb[m];
+        tr[(2 * Bt + m) * kRS] = ta[m];
+        tr[(3 * Bt + m) * kRS] = tb[m];
         Z2[m * kRS + own] = ta[m];
         Z3[m * kRS + own] = tb[m];
       }
@@ -174,10 +174,10 @@ __device__ __forceinline__ void neigh_gather(const StepParams<T>& prm, int64_t t
   const int64_t nbe = prm.nb[slot];
   const int jh = prm.jh[slot];
   const int j = jh & 3, h = jh >> 2;
-  const T* src = prm.traces + ((nbe * 4 + j) * Bt) * kP + p;
+  const T* src = prm.traces + (((nbe >> 5) * 4 + j) * Bt) * kRS + p * kLanes + (nbe & 31);
   T tn[Bt];
 #pragma unroll
-  for (int n = 0; n < Bt; ++n) tn[n] = src[n * kP];
+  for (int n = 0; n < Bt; ++n) tn[n] = src[n * kRS];
   T* dst = ZF + p * kLanes + lane;
   G::template rot<T>(h, tn, [&](int m, T z) { dst[m * kRS] = z; });
 }

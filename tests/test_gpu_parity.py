@@ -81,7 +81,7 @@ def test_constant_state_is_steady_on_gpu():
     # the volume and face terms that cancel are ~1e6 here (lambda dt |Q| / h): 1e-8 absolute
     # is ~1e-14 relative; several steps at the (unstable, reading R13) config dt amplify
     # the rounding noise, so one step is checked
-    assert np.abs(out - Qc).max() < 1e-8
+    assert np.abs(out - Qc).max() < 1e-7  # the oracle gives 1.02e-8 on the same input
 
 
 def test_errors_and_state():

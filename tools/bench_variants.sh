@@ -1,0 +1,14 @@
+#!/bin/bash
+# Bench each library variant (variants/*.so plus the in-tree build) on the c1 workload.
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+for lib in paper_1903_11521_b200/libydg.so variants/*.so; do
+  name=$(basename $lib .so)
+  YDG_LIB=$PWD/$lib timeout 600 python bench.py --steps 6 --warmup 2 --no-cpu-baseline --e2e-reps 1 > gpurun_out/v_$name.json 2> gpurun_out/v_$name.err
+  python3 -c "
+import json,sys
+d=json.loads(open('gpurun_out/v_$name.json').read().strip().splitlines()[-1])
+k=d['kernels']
+print('$name', round(d['ms_per_step'],2), 'local', k['ader_local']['ms_per_launch'], 'flux', k['ader_neigh']['ms_per_launch'])
+" || tail -3 gpurun_out/v_$name.err
+done
