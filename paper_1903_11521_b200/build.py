@@ -27,7 +27,7 @@ CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-fopenmp", "-I", CSRC, "-I", os.path.
 
 
 def sources():
-    cu = [os.path.join(CSRC, f) for f in ("kernels.cu", "halo.cu")]
+    cu = [os.path.join(CSRC, f) for f in ("kernels.cu", "halo.cu", "generic.cu")]
     cu += [os.path.join(CSRC, "generated", f"kernels_N{n}.cu") for n in range(1, 7)]
     cpp = [os.path.join(CSRC, f) for f in ("setup.cpp", "api.cpp")]
     return cu, cpp

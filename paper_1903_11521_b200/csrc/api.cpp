@@ -7,12 +7,16 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "generated/ydg_counts.h"
+#include "generated/ydg_matrices.h"
+#include "generic.h"
 #include "halo.h"
 #include "kernels.cuh"
 #include "setup.h"
@@ -46,6 +50,13 @@ struct ydg_solver {
   size_t device_bytes = 0;
   int grid_local = 0, grid_neigh = 0;
   int64_t bnd_lo = 0, bnd_hi = 0;  // leading / trailing owned tiles covering all tiles with ghosts
+  // generic path (viscoelastic, or YDG_GENERIC=1): canonical layouts, CSR global matrices
+  bool generic = false;
+  void* src = nullptr;      // [e][p][9] viscoelastic source pattern values
+  int64_t* nb64 = nullptr;  // [e][4]
+  int8_t* jh_e = nullptr;   // [e][4]
+  std::vector<void*> csr;   // device CSR arrays (freed in ydg_destroy)
+  GenParams gp{};
   // profiling: (start, stop, kind) events of timed launches; kind 0 = local, 1 = neighbour
   bool profiling = false;
   struct Ev { cudaEvent_t a, b; int kind; };
@@ -75,8 +86,9 @@ int fail(ydg_solver* h, int code, const std::string& msg) {
 int elem_bytes(const ydg_solver* h) { return h->prec; }
 
 void free_mesh(ydg_solver* h) {
-  for (void** p : {&h->Q, &h->traces, &h->star, &h->aplus, &h->aminus, &h->staging,
-                   reinterpret_cast<void**>(&h->nb), reinterpret_cast<void**>(&h->jh)}) {
+  for (void** p : {&h->Q, &h->traces, &h->star, &h->aplus, &h->aminus, &h->staging, &h->src,
+                   reinterpret_cast<void**>(&h->nb), reinterpret_cast<void**>(&h->jh),
+                   reinterpret_cast<void**>(&h->nb64), reinterpret_cast<void**>(&h->jh_e)}) {
     if (*p) cudaFree(*p);
     *p = nullptr;
   }
@@ -255,6 +267,191 @@ int do_step(ydg_solver* h, double dt, int nsteps, cudaStream_t s) {
 
 cudaStream_t pick_stream(ydg_solver* h, void* s) { return s ? static_cast<cudaStream_t>(s) : h->stream; }
 
+// ---------------------------------------------------------------- generic path
+
+// Column patterns: star-matrix rows (setup.cpp star_cols) and viscoelastic source rows
+// (reading R14: E[sigma_s][theta^l_t] for t normal when s normal, t = s when s shear;
+// E[theta^l_s][theta^l_s]; velocity rows have no source).  Unused slots repeat a column
+// with a zero coefficient.
+void generic_patterns(int (*ecols)[9], int (*scols)[3]) {
+  for (int p = 0; p < 27; ++p) {
+    star_cols(27, p, scols[p]);
+    int n = 0;
+    if (p < 6) {
+      for (int l = 0; l < 3; ++l)
+        for (int t = 0; t < 6; ++t)
+          if ((p < 3 && t < 3) || p == t) ecols[p][n++] = 9 + 6 * l + t;
+    } else if (p >= 9) {
+      ecols[p][n++] = p;
+    }
+    const int fill = n ? ecols[p][0] : 0;
+    while (n < 9) ecols[p][n++] = fill;
+  }
+}
+
+template <class TB>
+void csr_from(int rows, int cols, const std::function<double(int, int)>& at, std::vector<int>& ptr,
+              std::vector<int>& col, std::vector<double>& val) {
+  (void)sizeof(TB);
+  ptr.assign(1, 0);
+  col.clear();
+  val.clear();
+  for (int r = 0; r < rows; ++r) {
+    for (int c = 0; c < cols; ++c) {
+      const double v = at(r, c);
+      if (v != 0.0) {
+        col.push_back(c);
+        val.push_back(v);
+      }
+    }
+    ptr.push_back(static_cast<int>(col.size()));
+  }
+}
+
+template <class TB>
+int upload_csr(ydg_solver* h) {
+  constexpr int B = TB::B, Bt = TB::Bt;
+  struct M { int rows, cols; std::function<double(int, int)> at; const int** ptr; const int** col; const double** val; };
+  GenParams& g = h->gp;
+  std::vector<M> ms = {
+      {3 * B, B, [](int r, int c) { return -TB::K[r / B][c][r % B]; }, &g.kt_ptr, &g.kt_col, &g.kt_val},
+      {3 * B, B, [](int r, int c) { return TB::K[r / B][r % B][c]; }, &g.kh_ptr, &g.kh_col, &g.kh_val},
+      {4 * Bt, B, [](int r, int c) { return TB::R[r / Bt][c][r % Bt]; }, &g.rt_ptr, &g.rt_col, &g.rt_val},
+      {4 * B, Bt, [](int r, int c) { return TB::R[r / B][r % B][c]; }, &g.r_ptr, &g.r_col, &g.r_val},
+      {3 * Bt, Bt, [](int r, int c) { return TB::f[r / Bt][r % Bt][c]; }, &g.f_ptr, &g.f_col, &g.f_val}};
+  for (auto& m : ms) {
+    std::vector<int> ptr, col;
+    std::vector<double> val;
+    csr_from<TB>(m.rows, m.cols, m.at, ptr, col, val);
+    void *dp = nullptr, *dc = nullptr, *dv = nullptr;
+    if (cudaMalloc(&dp, ptr.size() * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&dc, std::max<size_t>(1, col.size()) * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&dv, std::max<size_t>(1, val.size()) * sizeof(double)) != cudaSuccess)
+      return fail(h, YDG_ERR_OOM, "CSR allocation failed");
+    h->csr.insert(h->csr.end(), {dp, dc, dv});
+    CUDA_OR_FAIL(h, cudaMemcpy(dp, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (!col.empty()) {
+      CUDA_OR_FAIL(h, cudaMemcpy(dc, col.data(), col.size() * sizeof(int), cudaMemcpyHostToDevice));
+      CUDA_OR_FAIL(h, cudaMemcpy(dv, val.data(), val.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    *m.ptr = static_cast<const int*>(dp);
+    *m.col = static_cast<const int*>(dc);
+    *m.val = static_cast<const double*>(dv);
+  }
+  return YDG_OK;
+}
+
+int generic_matrices(ydg_solver* h) {
+  switch (h->N) {
+    case 1: return upload_csr<tables::N1>(h);
+    case 2: return upload_csr<tables::N2>(h);
+    case 3: return upload_csr<tables::N3>(h);
+    case 4: return upload_csr<tables::N4>(h);
+    case 5: return upload_csr<tables::N5>(h);
+    case 6: return upload_csr<tables::N6>(h);
+  }
+  return fail(h, YDG_ERR_UNSUPPORTED, "order not tabulated");
+}
+
+// Mesh upload of the generic path: element-major layouts (generic.h), one rank.
+int generic_upload_mesh(ydg_solver* h, const double* xyz, const double* material, const double* anel) {
+  const int P = h->P, B = h->B, Bt = h->Bt;
+  const int64_t ne = h->ne;
+  int rc;
+  if ((rc = dalloc(h, &h->Q, static_cast<size_t>(ne) * P * B * 8))) return rc;
+  if ((rc = dalloc(h, &h->traces, static_cast<size_t>(ne) * 4 * Bt * 9 * 8))) return rc;
+  if ((rc = dalloc(h, &h->star, static_cast<size_t>(ne) * 3 * P * 3 * 8))) return rc;
+  if ((rc = dalloc(h, &h->aplus, static_cast<size_t>(ne) * 4 * P * 9 * 8))) return rc;
+  if ((rc = dalloc(h, &h->aminus, static_cast<size_t>(ne) * 4 * P * 9 * 8))) return rc;
+  if ((rc = dalloc(h, reinterpret_cast<void**>(&h->nb64), static_cast<size_t>(ne) * 4 * 8))) return rc;
+  if ((rc = dalloc(h, reinterpret_cast<void**>(&h->jh_e), static_cast<size_t>(ne) * 4))) return rc;
+  if (P == 27 && (rc = dalloc(h, &h->src, static_cast<size_t>(ne) * P * 9 * 8))) return rc;
+  CUDA_OR_FAIL(h, cudaMemset(h->Q, 0, static_cast<size_t>(ne) * P * B * 8));
+  CUDA_OR_FAIL(h, cudaMemcpy(h->nb64, h->nbr.nb.data(), ne * 4 * 8, cudaMemcpyHostToDevice));
+  {
+    std::vector<int8_t> jh(ne * 4);
+    for (int64_t i = 0; i < ne * 4; ++i) jh[i] = static_cast<int8_t>(h->nbr.j[i] | (h->nbr.h[i] << 2));
+    CUDA_OR_FAIL(h, cudaMemcpy(h->jh_e, jh.data(), jh.size(), cudaMemcpyHostToDevice));
+  }
+  int ecols[27][9], scols[27][3];
+  generic_patterns(ecols, scols);
+  const int64_t chunk = 65536;
+  std::vector<double> st, ap, am, sr;
+  for (int64_t e0 = 0; e0 < ne; e0 += chunk) {
+    const int64_t n = std::min(chunk, ne - e0);
+    ElementCoeffs c;
+    std::string err;
+    if (!element_coeffs(P, e0, n, xyz, material, anel, h->nbr, &c, &err)) return fail(h, YDG_ERR_MESH, err);
+    ap.assign(n * 4 * P * 9, 0.0);
+    am.assign(ap.size(), 0.0);
+    for (int64_t t = 0; t < n; ++t)
+      for (int i = 0; i < 4; ++i)
+        for (int p = 0; p < P; ++p)
+          for (int q = 0; q < P; ++q) {
+            const double vp = c.aplus[((t * 4 + i) * P + p) * P + q], vm = c.aminus[((t * 4 + i) * P + p) * P + q];
+            if (q < 9) {
+              ap[((t * 4 + i) * P + p) * 9 + q] = vp;
+              am[((t * 4 + i) * P + p) * 9 + q] = vm;
+            } else if (vp != 0.0 || vm != 0.0) {
+              return fail(h, YDG_ERR_MESH, "flux solver couples a memory variable (unexpected)");
+            }
+          }
+    CUDA_OR_FAIL(h, cudaMemcpy(static_cast<double*>(h->star) + e0 * 3 * P * 3, c.star.data(), c.star.size() * 8,
+                               cudaMemcpyHostToDevice));
+    CUDA_OR_FAIL(h, cudaMemcpy(static_cast<double*>(h->aplus) + e0 * 4 * P * 9, ap.data(), ap.size() * 8,
+                               cudaMemcpyHostToDevice));
+    CUDA_OR_FAIL(h, cudaMemcpy(static_cast<double*>(h->aminus) + e0 * 4 * P * 9, am.data(), am.size() * 8,
+                               cudaMemcpyHostToDevice));
+    if (P == 27) {
+      sr.assign(n * P * 9, 0.0);
+      for (int64_t t = 0; t < n; ++t)
+        for (int p = 0; p < P; ++p) {
+          bool seen[27] = {};
+          for (int j = 0; j < 9; ++j) {
+            const int q = ecols[p][j];
+            if (seen[q]) continue;  // padding slot repeats a column with a zero value
+            seen[q] = true;
+            sr[(t * P + p) * 9 + j] = c.src[(t * P + p) * P + q];
+          }
+        }
+      CUDA_OR_FAIL(h, cudaMemcpy(static_cast<double*>(h->src) + e0 * P * 9, sr.data(), sr.size() * 8,
+                                 cudaMemcpyHostToDevice));
+    }
+  }
+  GenParams& g = h->gp;
+  g.Q = static_cast<double*>(h->Q);
+  g.traces = static_cast<double*>(h->traces);
+  g.star = static_cast<const double*>(h->star);
+  g.src = static_cast<const double*>(h->src);
+  g.aplus = static_cast<const double*>(h->aplus);
+  g.aminus = static_cast<const double*>(h->aminus);
+  g.nb = h->nb64;
+  g.jh = h->jh_e;
+  g.N = h->N;
+  g.B = B;
+  g.Bt = Bt;
+  g.P = P;
+  h->nslots = ne;
+  h->ntiles = (ne + kLanes - 1) / kLanes;
+  return YDG_OK;
+}
+
+int generic_step(ydg_solver* h, double dt, int nsteps, cudaStream_t s) {
+  GenParams g = h->gp;
+  g.dt = dt;
+  for (int d = 0; d < h->N; ++d) {
+    g.scal[d] = dt / (d + 1);
+    g.scal[h->N + d] = dt / (d + 2);
+  }
+  g.e0 = 0;
+  g.n = h->ne;
+  for (int n = 0; n < nsteps; ++n) {
+    CUDA_OR_FAIL(h, timed(h, 0, s, [&] { return gen_launch(g, true, s); }));
+    CUDA_OR_FAIL(h, timed(h, 1, s, [&] { return gen_launch(g, false, s); }));
+  }
+  return YDG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -269,8 +466,10 @@ int ydg_create(int order, int quantities, int precision, int cuda_device, ydg_so
     g_last_error = "bad order / quantities / precision";
     return YDG_ERR_ARG;
   }
-  if (quantities == 27 || (order == 6 && precision == 8)) {
-    g_last_error = "combination not compiled (viscoelastic / N=6 fp64 not yet available)";
+  const char* force = std::getenv("YDG_GENERIC");
+  const bool generic = quantities == 27 || (order == 6 && precision == 8) || (force && force[0] == '1');
+  if (generic && precision != 8) {
+    g_last_error = "the generic (viscoelastic) path is fp64 only";
     return YDG_ERR_UNSUPPORTED;
   }
   std::unique_ptr<ydg_solver> h(new ydg_solver);
@@ -280,12 +479,29 @@ int ydg_create(int order, int quantities, int precision, int cuda_device, ydg_so
   h->dev = cuda_device;
   h->B = (order + 1) * (order + 2) * (order + 3) / 6;
   h->Bt = (order + 1) * (order + 2) / 2;
+  h->generic = generic;
   cudaError_t e = cudaSetDevice(cuda_device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = configure_kernels(order, precision);
+  if (e == cudaSuccess) {
+    if (generic) {
+      int ecols[27][9], scols[27][3];
+      generic_patterns(ecols, scols);
+      e = gen_configure(h->B, h->Bt, quantities, ecols, scols);
+    } else {
+      e = configure_kernels(order, precision);
+    }
+  }
   if (e != cudaSuccess) {
     g_last_error = std::string("CUDA: ") + cudaGetErrorString(e);
     return YDG_ERR_CUDA;
+  }
+  if (generic) {
+    int rc = generic_matrices(h.get());
+    if (rc) {
+      g_last_error = h->err;
+      for (void* p : h->csr) cudaFree(p);
+      return rc;
+    }
   }
   *out = h.release();
   return YDG_OK;
@@ -325,6 +541,13 @@ int ydg_upload_mesh(ydg_solver* h, int64_t ne, const double* xyz, const int64_t*
   h->ne = ne;
   h->first = ne * h->rank / h->nranks;
   h->nlocal = ne * (h->rank + 1) / h->nranks - h->first;
+  if (h->generic) {
+    if (h->nranks > 1) return fail(h, YDG_ERR_UNSUPPORTED, "the generic (viscoelastic) path runs on one rank");
+    rc = generic_upload_mesh(h, xyz, material, anelastic);
+    if (rc) { free_mesh(h); return rc; }
+    h->have_mesh = true;
+    return YDG_OK;
+  }
   h->ntiles = (h->nlocal + kLanes - 1) / kLanes;
   // local slots: owned [0, nlocal) padded to tiles, then ghosts
   std::vector<int64_t> ghost_of;  // global element id of each ghost slot
@@ -422,6 +645,16 @@ static int xfer_dofs(ydg_solver* h, int64_t first, int64_t count, const void* sr
   const int eb = elem_bytes(h);
   const int64_t per = static_cast<int64_t>(h->P) * h->B;
   const bool dev_side = src_dev || dst_dev;
+  if (h->generic) {  // canonical layout on the device: plain copies
+    char* q = static_cast<char*>(h->Q) + (first - h->first) * per * eb;
+    const size_t bytes = static_cast<size_t>(count) * per * eb;
+    if (upload)
+      CUDA_OR_FAIL(h, cudaMemcpyAsync(q, src_dev ? src_dev : src_host, bytes, cudaMemcpyDefault, s));
+    else
+      CUDA_OR_FAIL(h, cudaMemcpyAsync(dst_dev ? dst_dev : dst_host, q, bytes, cudaMemcpyDefault, s));
+    if (!dev_side) CUDA_OR_FAIL(h, cudaStreamSynchronize(s));
+    return YDG_OK;
+  }
   const int64_t chunk = dev_side ? count : std::max<int64_t>(1, static_cast<int64_t>(h->staging_bytes) / (per * eb));
   for (int64_t c0 = 0; c0 < count; c0 += chunk) {
     const int64_t n = std::min(chunk, count - c0);
@@ -476,6 +709,7 @@ int ydg_step(ydg_solver* h, double dt, int nsteps, void* cuda_stream) {
   if (!h->have_mesh) return fail(h, YDG_ERR_STATE, "upload the mesh first");
   if (!(dt > 0) || !std::isfinite(dt) || nsteps < 0) return fail(h, YDG_ERR_ARG, "bad dt or nsteps");
   cudaStream_t s = pick_stream(h, cuda_stream);
+  if (h->generic) return generic_step(h, dt, nsteps, s);
   return h->prec == 8 ? do_step<double>(h, dt, nsteps, s) : do_step<float>(h, dt, nsteps, s);
 }
 
@@ -577,6 +811,7 @@ void ydg_destroy(ydg_solver* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   drain_profile(h);
   free_mesh(h);
+  for (void* p : h->csr) cudaFree(p);
   h->halo.destroy();
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;

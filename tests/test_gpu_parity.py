@@ -112,3 +112,25 @@ def test_errors_and_state():
     ydg.ydg_step(h, 1e-4, 0)
     ydg.ydg_download_dofs(h, 0, 0)
     ydg.ydg_destroy(h)
+
+
+def test_c3_viscoelastic_replica():
+    """configs[3] (viscoelastic, 3 mechanisms, P = 27, N = 4, fp64) at 3x3x3 cubes, 2 steps:
+    generic CUDA path vs the oracle of reading R14."""
+    cfg = synth.CONFIGS["c3"].replica(3, steps=2)
+    err, *_ = _parity(cfg)
+    assert err["all"] <= TOL[8], err
+    assert err["memory"] <= 1e-11, err
+
+
+def test_generic_path_elastic(monkeypatch):
+    """The generic (CSR) kernels on the elastic c0 problem agree with the oracle too."""
+    monkeypatch.setenv("YDG_GENERIC", "1")
+    err, *_ = _parity(synth.CONFIGS["c0"], nsteps=2)
+    assert err["all"] <= TOL[8], err
+
+
+def test_order6_fp64_generic():
+    cfg = _cfg("c1", N=6, nx=3, ny=3, nz=3, steps=1)
+    err, *_ = _parity(cfg)
+    assert err["all"] <= TOL[8], err
