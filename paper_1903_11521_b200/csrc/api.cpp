@@ -85,6 +85,11 @@ int fail(ydg_solver* h, int code, const std::string& msg) {
 
 int elem_bytes(const ydg_solver* h) { return h->prec; }
 
+// Values per element-face trace block of the fp64 tensor-core kernels (layout
+// [tile][face][lane][TS], block [m][q] padded to 16 bytes); 0 = the fp32 layout
+// [tile][face][m][q][32].
+int trace_block(const ydg_solver* h) { return h->prec == 8 ? (h->Bt * h->P + 1) / 2 * 2 : 0; }
+
 void free_mesh(ydg_solver* h) {
   for (void** p : {&h->Q, &h->traces, &h->star, &h->aplus, &h->aminus, &h->staging, &h->src,
                    reinterpret_cast<void**>(&h->nb), reinterpret_cast<void**>(&h->jh),
@@ -604,7 +609,7 @@ int ydg_upload_mesh(ydg_solver* h, int64_t ne, const double* xyz, const int64_t*
   }
   const int eb = elem_bytes(h);
   const size_t q_n = static_cast<size_t>(h->ntiles) * kLanes * h->P * h->B;
-  const size_t tr_n = static_cast<size_t>(h->nslots) * 4 * h->Bt * h->P;
+  const size_t tr_n = static_cast<size_t>(h->nslots) * 4 * (trace_block(h) ? trace_block(h) : h->Bt * h->P);
   if ((rc = dalloc(h, &h->Q, q_n * eb))) { free_mesh(h); return rc; }
   if ((rc = dalloc(h, &h->traces, tr_n * eb))) { free_mesh(h); return rc; }
   if ((rc = dalloc(h, reinterpret_cast<void**>(&h->nb), nb_local.size() * sizeof(int32_t)))) { free_mesh(h); return rc; }
@@ -616,7 +621,7 @@ int ydg_upload_mesh(ydg_solver* h, int64_t ne, const double* xyz, const int64_t*
   rc = eb == 8 ? upload_coeffs<double>(h, xyz, material, anelastic) : upload_coeffs<float>(h, xyz, material, anelastic);
   if (rc) { free_mesh(h); return rc; }
   if (h->nranks > 1) {
-    rc = h->halo.bind(h->traces, h->Bt, h->P, eb, owned_slots, &h->err);
+    rc = h->halo.bind(h->traces, h->Bt, h->P, trace_block(h), eb, owned_slots, &h->err);
     if (rc) { free_mesh(h); return fail(h, rc, h->err); }
   }
   // staging buffer for DOF transfers (bounded)

@@ -1,4 +1,4 @@
-// FP64 tensor-core (DMMA m8n8k4) kernels of the ADER-DG update (sm_100a, fp64).
+// FP64 tensor-core (DMMA m8n8k4) kernels of the ADER-DG update (sm_100a, fp64, P = 9).
 //
 // Data of a 32-element tile live in shared memory as [row][col] with col = p*32 + e
 // (quantity-major), rows swizzled (col ^ 8*(row & 1)) so that the 4-row x 8-column DMMA
@@ -6,7 +6,11 @@
 // conflict-free.  Warp p owns the four 8-column tiles of quantity p: every B operand it
 // feeds to a DMMA is warp-private; only the per-element quantity mixing (star matrices
 // A*, flux solvers A+-) reads other warps' columns.  Global matrices are the DMMA A
-// operands (generated 8x4 tiles, zero tiles skipped: gen/dmma.py).
+// operands: generated 8x4 tiles over freely grouped rows (gen/dmma.py, gen/tiling.py).
+//
+// Face traces T_i = R^iT I live in HBM as [tile][face][lane][TS] with an element-face
+// block [m][q] of TS = even(9*Bt) doubles: the producer writes a face of a tile with one
+// TMA bulk store, the consumer gathers a neighbour's face with one TMA bulk copy.
 #pragma once
 #include "kernels.cuh"
 
@@ -24,6 +28,7 @@ __device__ __forceinline__ int swz(int row, int col) { return row * kRS + (col ^
 
 struct Ctx {
   int lane, p;
+  int sh4, sh8;       // 8 * (lane & 3), 8 * (lane >> 2): byte of a k-set / m-tile row word
   double* S;          // [SROWS][288]  D^d, d >= 1
   double* I;          // [IROWS][288]  time integral rows < IROWS
   double* xb;         // warp-private [3][4][kXB]
@@ -42,6 +47,11 @@ template <int N>
 __device__ const double* frag_table();
 
 __device__ __forceinline__ double afrag(const Ctx& x, int tid) { return __ldg(x.frags + tid * kL + x.lane); }
+
+__device__ __forceinline__ int krow(const Ctx& x, unsigned w) { return static_cast<int>((w >> x.sh4) & 0xffu); }
+__device__ __forceinline__ int mrow(const Ctx& x, unsigned long long w) {
+  return static_cast<int>((w >> x.sh8) & 0xffull);
+}
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -65,21 +75,23 @@ template <Src SRC, int B>
 __device__ __forceinline__ double load_data(const Ctx& x, int row, int col) {
   // Q^n of the tile is staged in shared memory at the rows of I (rows >= IROWS continue
   // into S) for the first CK step
-  if constexpr (SRC == SRC_Q) return row < B ? x.I[swz(row, col)] : 0.0;
+  if constexpr (SRC == SRC_Q) return x.I[swz(row, col)];
   else if constexpr (SRC == SRC_S) return x.S[swz(row, col)];
   else return x.I[swz(row, col)];
 }
 
-// X^c = D A*^cT for rows l0..l0+3 of the thread's own column (element lane, quantity p),
-// staged in the warp-private buffer [c][r][kXB]; xb_b then reads one c's B fragments
-// for the warp's four column tiles.  The caller ends the k-step with __syncwarp().
+// X^c = D A*^cT for the 4 rows r0..r3 (compile-time, uniform over the warp) of the
+// thread's own column (element lane, quantity p), staged in the warp-private buffer
+// [c][r][kXB]; xb_b then reads one c's B fragments for the warp's four column tiles.
+// The caller ends the k-set with __syncwarp().
 template <Src SRC, int B>
-__device__ __forceinline__ void xchunk(Ctx& x, int l0) {
+__device__ __forceinline__ void xchunk(Ctx& x, int r0, int r1, int r2, int r3) {
+  const int rr[4] = {r0, r1, r2, r3};
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
-    const double d0 = load_data<SRC, B>(x, l0 + r, x.q0 * kL + x.lane);
-    const double d1 = load_data<SRC, B>(x, l0 + r, x.q1 * kL + x.lane);
-    const double d2 = load_data<SRC, B>(x, l0 + r, x.q2 * kL + x.lane);
+    const double d0 = load_data<SRC, B>(x, rr[r], x.q0 * kL + x.lane);
+    const double d1 = load_data<SRC, B>(x, rr[r], x.q1 * kL + x.lane);
+    const double d2 = load_data<SRC, B>(x, rr[r], x.q2 * kL + x.lane);
 #pragma unroll
     for (int c = 0; c < 3; ++c)
       x.xb[(c * 4 + r) * kXB + x.lane] = fma(x.a[3 * c + 2], d2, fma(x.a[3 * c + 1], d1, x.a[3 * c] * d0));
@@ -91,157 +103,83 @@ __device__ __forceinline__ void xb_b(const Ctx& x, int c, double (&bf)[4]) {
   for (int ct = 0; ct < 4; ++ct) bf[ct] = x.xb[(c * 4 + (x.lane & 3)) * kXB + 8 * ct + (x.lane >> 2)];
 }
 
-// B fragments of the time integral (own quantity p): rows < IROWS from shared memory
-// (ismem_b); the remaining rows are dt * Q (only D^0 contributes to them), read from global
-// memory (gq_b) at the start of each trace so that their latency overlaps the DMMAs.
-__device__ __forceinline__ void ismem_b(const Ctx& x, int l0, double (&bf)[4]) {
-  const int row = l0 + (x.lane & 3);
+// Gathered B fragments of the own quantity column: lane row = byte (lane & 3) of w.
+__device__ __forceinline__ void ismem_b(const Ctx& x, unsigned w, double (&bf)[4]) {
+  const int row = krow(x, w);
 #pragma unroll
   for (int ct = 0; ct < 4; ++ct) bf[ct] = x.I[swz(row, x.p * kL + 8 * ct + (x.lane >> 2))];
 }
+// rows >= IROWS of the time integral are dt * Q (only D^0 contributes), from global memory
 template <int B>
-__device__ __forceinline__ void gq_b(const Ctx& x, int l0, double (&bf)[4]) {
-  const int row = l0 + (x.lane & 3);
+__device__ __forceinline__ void gq_b(const Ctx& x, unsigned w, double (&bf)[4]) {
+  const int row = krow(x, w);
 #pragma unroll
-  for (int ct = 0; ct < 4; ++ct)
-    bf[ct] = row < B ? x.dt * x.Qt[row * kRS + x.p * kL + 8 * ct + (x.lane >> 2)] : 0.0;
+  for (int ct = 0; ct < 4; ++ct) bf[ct] = x.dt * x.Qt[row * kRS + x.p * kL + 8 * ct + (x.lane >> 2)];
 }
-
-__device__ __forceinline__ void smem_b(const Ctx& x, const double* Y, int l0, double (&bf)[4]) {
-  const int row = l0 + (x.lane & 3);
+__device__ __forceinline__ void smem_b(const Ctx& x, const double* Y, unsigned w, double (&bf)[4]) {
+  const int row = krow(x, w);
 #pragma unroll
   for (int ct = 0; ct < 4; ++ct) bf[ct] = Y[swz(row, x.p * kL + 8 * ct + (x.lane >> 2))];
 }
 
-// Write D^{d+1} = dt/(d+1) acc into S and accumulate the time integral;
-// at d = 0 the integral starts from dt * Q.
-template <int MT, int FIRST, int B>
-__device__ __forceinline__ void ck_writeback(Ctx& x, const double (&acc)[MT][4][2], int d) {
+// Write D^{d+1} = dt/(d+1) acc of one m-tile (rows from the word w) into S and accumulate
+// the time integral; at d = 0 the integral starts from dt * Q.
+template <int FIRST, int B>
+__device__ __forceinline__ void ck_wb(Ctx& x, const double (&acc)[4][2], int d, unsigned long long w) {
+  const int row = mrow(x, w);
+  if (row == 0xff) return;
   const double sc = x.scal[d], ic = x.scal[x.N + d];
 #pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int ct = 0; ct < 4; ++ct) {
-      const int row = 8 * mt + (x.lane >> 2);
-      const int col = x.p * kL + 8 * ct + 2 * (x.lane & 3);
-      const int s = swz(row, col);
-      const double v0 = sc * acc[mt][ct][0], v1 = sc * acc[mt][ct][1];
-      *reinterpret_cast<double2*>(x.S + s) = make_double2(v0, v1);
-      double2 i2;
-      if (FIRST) {
-        const double2 q = row < B ? *reinterpret_cast<const double2*>(x.I + s) : make_double2(0.0, 0.0);
-        i2 = make_double2(fma(ic, v0, x.dt * q.x), fma(ic, v1, x.dt * q.y));
-      } else {
-        i2 = *reinterpret_cast<const double2*>(x.I + s);
-        i2.x = fma(ic, v0, i2.x);
-        i2.y = fma(ic, v1, i2.y);
-      }
-      *reinterpret_cast<double2*>(x.I + s) = i2;
+  for (int ct = 0; ct < 4; ++ct) {
+    const int col = x.p * kL + 8 * ct + 2 * (x.lane & 3);
+    const int s = swz(row, col);
+    const double v0 = sc * acc[ct][0], v1 = sc * acc[ct][1];
+    *reinterpret_cast<double2*>(x.S + s) = make_double2(v0, v1);
+    double2 i2 = *reinterpret_cast<const double2*>(x.I + s);
+    if (FIRST) {
+      i2 = make_double2(fma(ic, v0, x.dt * i2.x), fma(ic, v1, x.dt * i2.y));
+    } else {
+      i2.x = fma(ic, v0, i2.x);
+      i2.y = fma(ic, v1, i2.y);
     }
+    *reinterpret_cast<double2*>(x.I + s) = i2;
+  }
+}
+// Rows [LO, HI) of the time-integral region receive no derivative: I = dt * Q (own column).
+template <int LO, int HI>
+__device__ __forceinline__ void scale_irows(Ctx& x) {
+#pragma unroll
+  for (int r = LO; r < HI; ++r) {
+    double* v = x.I + swz(r, x.p * kL + x.lane);
+    *v = x.dt * *v;
+  }
 }
 
-// Q += acc, direct read-modify-write of the C fragments in global memory.
-template <int MT, int B>
-__device__ __forceinline__ void add_q(const Ctx& x, double* Qt, const double (&acc)[MT][4][2]) {
+// Q += acc of one m-tile (rows from the word w): read-modify-write of the C fragments
+// in global memory (16-byte, two elements).
+__device__ __forceinline__ void add_q(const Ctx& x, double* Qt, const double (&acc)[4][2], unsigned long long w) {
+  const int row = mrow(x, w);
+  if (row == 0xff) return;
 #pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int ct = 0; ct < 4; ++ct) {
-      if (8 * mt + (x.lane >> 2) >= B) continue;
-      double2* q = reinterpret_cast<double2*>(Qt + (8 * mt + (x.lane >> 2)) * kRS + x.p * kL + 8 * ct +
-                                              2 * (x.lane & 3));
-      double2 v = *q;
-      v.x += acc[mt][ct][0];
-      v.y += acc[mt][ct][1];
-      *q = v;
-    }
-}
-
-// Q += acc (C fragments of 8-row tiles, rows < B): the fragments go to a shared staging
-// region [B][288] (stage_acc, then a barrier), then every thread updates Q with coalesced
-// 16-byte read-modify-writes (update_q) -- no accumulator is live while Q is loaded.
-template <int MT, int B>
-__device__ __forceinline__ void stage_acc(const Ctx& x, double* st, const double (&acc)[MT][4][2]) {
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int ct = 0; ct < 4; ++ct) {
-      const int row = 8 * mt + (x.lane >> 2);
-      if (row >= B) continue;
-      *reinterpret_cast<double2*>(st + swz(row, x.p * kL + 8 * ct + 2 * (x.lane & 3))) =
-          make_double2(acc[mt][ct][0], acc[mt][ct][1]);
-    }
-}
-#ifndef YDG_QSTAGE
-#define YDG_QSTAGE 0
-#endif
-template <int B>
-__device__ __forceinline__ void update_q(double* Qt, const double* st) {
-  constexpr int kPairs = B * kRS / 2;
-#pragma unroll 4
-  for (int c = threadIdx.x; c < kPairs; c += kP * kL) {
-    const int row = c / (kRS / 2), cc = 2 * (c % (kRS / 2));
-    double2* q = reinterpret_cast<double2*>(Qt + row * kRS + cc);
-    const double2 a = *reinterpret_cast<const double2*>(st + swz(row, cc));
+  for (int ct = 0; ct < 4; ++ct) {
+    double2* q = reinterpret_cast<double2*>(Qt + row * kRS + x.p * kL + 8 * ct + 2 * (x.lane & 3));
     double2 v = *q;
-    v.x += a.x;
-    v.y += a.y;
+    v.x += acc[ct][0];
+    v.y += acc[ct][1];
     *q = v;
   }
 }
 
-// Store the trace C fragments (rows < Bt) to global memory [tile][face][m][q][32].
-template <int MT, int Bt>
-__device__ __forceinline__ void store_trace_global(const Ctx& x, double* gtr, const double (&acc)[MT][4][2]) {
+// Trace C fragments of one m-tile -> staging block [lane][m][q] (stride TS per lane).
+template <int TS>
+__device__ __forceinline__ void stage_trace(const Ctx& x, double* stg, const double (&acc)[4][2], unsigned long long w) {
+  const int m = mrow(x, w);
+  if (m == 0xff) return;
 #pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int ct = 0; ct < 4; ++ct) {
-      const int row = 8 * mt + (x.lane >> 2);
-      const int col = x.p * kL + 8 * ct + 2 * (x.lane & 3);
-      if (row < Bt) *reinterpret_cast<double2*>(gtr + row * kRS + col) = make_double2(acc[mt][ct][0], acc[mt][ct][1]);
-    }
-}
-
-// Y = Z A^T per element (thread = element lane, quantity p), in place in the staging region
-// (all columns of Z are read before the barrier, then each thread writes its own column).
-template <int Bt>
-__device__ __forceinline__ void mix_inplace(const Ctx& x, double* Z, const double* flux, int64_t tile,
-                                            int F) {
-  double arow[kP];
-  const double* A = flux + ((tile * 4 + F) * kP + x.p) * kP * kL + x.lane;
-#pragma unroll
-  for (int q = 0; q < kP; ++q) arow[q] = A[q * kL];
-  double y[Bt];
-#pragma unroll
-  for (int m = 0; m < Bt; ++m) {
-    double s = 0.0;
-#pragma unroll
-    for (int q = 0; q < kP; ++q) s = fma(Z[swz(m, q * kL + x.lane)], arow[q], s);
-    y[m] = s;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int m = 0; m < Bt; ++m) Z[swz(m, x.p * kL + x.lane)] = y[m];
-}
-
-// Y = T A^T with T read from the tile's traces in global memory ([m][q][32] rows of face
-// F), written to the own column of a shared staging region; no barrier needed since the
-// lift that consumes Y reads only the warp's own columns.
-template <int Bt>
-__device__ __forceinline__ void mix_from_global(const Ctx& x, double* Y, const double* gT,
-                                                const double* flux, int64_t tile, int F) {
-  double arow[kP];
-  const double* A = flux + ((tile * 4 + F) * kP + x.p) * kP * kL + x.lane;
-#pragma unroll
-  for (int q = 0; q < kP; ++q) arow[q] = A[q * kL];
-#pragma unroll 3
-  for (int m = 0; m < Bt; ++m) {
-    const double* row = gT + m * kRS + x.lane;
-    double s = 0.0;
-#pragma unroll
-    for (int q = 0; q < kP; ++q) s = fma(row[q * kL], arow[q], s);
-    Y[swz(m, x.p * kL + x.lane)] = s;
+  for (int ct = 0; ct < 4; ++ct) {
+    const int e = 8 * ct + 2 * (x.lane & 3);
+    stg[e * TS + m * kP + x.p] = acc[ct][0];
+    stg[(e + 1) * TS + m * kP + x.p] = acc[ct][1];
   }
 }
 
@@ -249,14 +187,17 @@ template <int N>
 struct Layout {
   using G = DG<N>;
   static constexpr int XB = 9 * 3 * 4 * kXB;  // doubles
-  // local kernel: [I][S][xb]; the face staging region (TROWS rows) reuses S
-  // [I][S][xb]; Q^n of the tile is staged over I and S for the first CK step
-  static constexpr int LOCAL = (G::IROWS + G::SROWS > G::B ? G::IROWS + G::SROWS : G::B) * kRS + XB;
-  // Z, T, mbarrier (the Q-update staging [B][288] reuses Z and T)
-  static constexpr int NEIGH = (2 * G::TROWS + 2 * G::Bt > G::B ? 2 * G::TROWS + 2 * G::Bt : G::B) * kRS + 2;
+  static constexpr int FACE = kL * G::TS;      // doubles of one face of a tile
+  // local kernel: [I][S][xb]; Q^n of the tile is staged over I and S for the first CK
+  // step; the two trace staging blocks reuse S and xb
+  static constexpr int ROWS = (G::IROWS + G::SROWS > G::B ? G::IROWS + G::SROWS : G::B);
+  static constexpr int LOCAL = (ROWS * kRS + XB > G::IROWS * kRS + 2 * FACE ? ROWS * kRS + XB
+                                                                            : G::IROWS * kRS + 2 * FACE);
+  // flux kernel: own face block, two neighbour face blocks, Y rows, three mbarriers
+  static constexpr int FLUX = 3 * FACE + G::Bt * kRS + 3;
 };
 
-// ---- asynchronous copy helpers (TMA bulk copy + mbarrier, Ampere-style cp.async)
+// ---- asynchronous copy helpers (TMA bulk copies + mbarrier, Ampere-style cp.async)
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -285,15 +226,30 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_addr(bar))
       : "memory");
 }
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+template <int K>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(K) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
-
 __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void init_ctx(Ctx& x) {
+  x.lane = threadIdx.x & 31;
+  x.p = threadIdx.x >> 5;
+  x.sh4 = 8 * (x.lane & 3);
+  x.sh8 = 8 * (x.lane >> 2);
 }
 
 // CK + time integral, face traces R^iT I (stored for the flux kernel) and
@@ -301,18 +257,20 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
 template <int N>
 __global__ void __launch_bounds__(kP * kL, 1) dm_local(const __grid_constant__ StepParams<double> prm) {
   using G = DG<N>;
-  constexpr int B = G::B, Bt = G::Bt;
-  extern __shared__ __align__(16) double smem[];
+  using Lay = Layout<N>;
+  constexpr int B = G::B;
+  extern __shared__ __align__(128) double smem[];
   Ctx x;
-  x.lane = threadIdx.x & 31;
-  x.p = threadIdx.x >> 5;
+  init_ctx(x);
   x.I = smem;
   x.S = smem + G::IROWS * kRS;
-  x.xb = smem + (G::IROWS + G::SROWS > B ? G::IROWS + G::SROWS : B) * kRS + x.p * (3 * 4 * kXB);
+  x.xb = smem + Lay::ROWS * kRS + x.p * (3 * 4 * kXB);
   x.frags = frag_table<N>();
   x.dt = prm.dt;
   x.scal = prm.scal;
   x.N = N;
+  double* stg0 = x.S;              // trace staging blocks (S and xb are dead after CK)
+  double* stg1 = x.S + Lay::FACE;
   // 3-column pattern of star-matrix row p (setup.cpp star_cols), packed 5 bits per column
   {
     constexpr unsigned long long packed[9] = {6 | 7 << 5 | 8 << 10, 6 | 7 << 5 | 8 << 10, 6 | 7 << 5 | 8 << 10,
@@ -352,159 +310,144 @@ __global__ void __launch_bounds__(kP * kL, 1) dm_local(const __grid_constant__ S
     cp_async_wait_all();
     __syncthreads();
     G::ck(x);  // ends with a barrier: the time integral is complete
-    // traces T_F = R^FT I of the four faces -> global memory; they read Q^n (rows >=
-    // IROWS of I), so they precede the update of Q
-    double* gtr = prm.traces + tile * 4 * Bt * kRS;
+    // traces T_F = R^FT I of the four faces -> staging -> one TMA bulk store per face;
+    // they read Q^n (rows >= IROWS of I from global memory), so they precede the update
+    double* gtr = prm.traces + tile * 4 * Lay::FACE;
 #pragma unroll
     for (int F = 0; F < 4; ++F) {
-      double tacc[G::TROWS / 8][4][2];
-      zero_acc(tacc);
-      if (F == 0) G::template trace<0>(x, tacc);
-      else if (F == 1) G::template trace<1>(x, tacc);
-      else if (F == 2) G::template trace<2>(x, tacc);
-      else G::template trace<3>(x, tacc);
-      store_trace_global<G::TROWS / 8, Bt>(x, gtr + F * Bt * kRS, tacc);
+      double* stg = (F & 1) ? stg1 : stg0;
+      if (F >= 2) {
+        if (threadIdx.x == 0) bulk_wait_read<1>();  // the store of face F-2 has left stg
+        __syncthreads();
+      }
+      if (F == 0) G::template trace<0>(x, stg);
+      else if (F == 1) G::template trace<1>(x, stg);
+      else if (F == 2) G::template trace<2>(x, stg);
+      else G::template trace<3>(x, stg);
+      fence_proxy_async();
+      __syncthreads();
+      if (threadIdx.x == 0) bulk_s2g(gtr + F * Lay::FACE, stg, Lay::FACE * sizeof(double));
     }
+    if (threadIdx.x == 0) bulk_wait_read<0>();
+    __syncthreads();  // the staging blocks overlap the X buffers of the volume term
     {
       double acc[G::QMT][4][2];
       zero_acc(acc);
       G::volume(x, acc);
-#if YDG_QSTAGE
-      __syncthreads();  // I, S and the X buffers are dead: stage the update over them
-      stage_acc<G::QMT, B>(x, smem, acc);
+      G::add_volume(x, Qt, acc);
     }
-    __syncthreads();
-    update_q<B>(Qt, smem);
-#else
-      add_q<G::QMT, B>(x, Qt, acc);
-    }
-#endif
     __syncthreads();  // before the next tile overwrites the shared regions
   }
+  if (threadIdx.x == 0) bulk_wait_all();
 }
 
 // Flux kernel: local and neighbour flux with one lift per face:
 //   Q += sum_i R^i ( T_i A+_i^T + (f^h_i T^nb_(j_i)) A-_i^T ).
-// Two passes of two faces.  Per pass all loads are issued at once: one TMA bulk copy of the
-// tile's own traces of both faces (contiguous in the [tile][face][m][q][32] layout) and
-// per-thread cp.async gathers of the neighbour traces into the own column of the staging
-// region Z; then f^h rotates Z in place, thread (e,p) mixes T with A+ and Z with A-, writes
-// Y into Z after a barrier, and the warp lifts its own columns of Y with DMMAs.
+// Per (tile, face) item: one TMA bulk copy of the tile's own face block (buffer O) and one
+// per lane of the neighbour's face block (buffers N0/N1: the next face's copies are in
+// flight while this one computes); f^h rotates the neighbour column in place, thread
+// (e,p) mixes T with A+ and Z with A-, writing Y (rows [m][288]) and the warp lifts its
+// own columns of Y with DMMAs into Q.
 template <int N>
-__global__ void __launch_bounds__(kP * kL, 1) dm_neigh(const __grid_constant__ StepParams<double> prm) {
+__global__ void __launch_bounds__(kP * kL, 1) dm_flux(const __grid_constant__ StepParams<double> prm) {
   using G = DG<N>;
-  constexpr int B = G::B, Bt = G::Bt, TR = G::TROWS;
+  using Lay = Layout<N>;
+  constexpr int B = G::B, Bt = G::Bt, TS = G::TS, FACE = Lay::FACE;
   extern __shared__ __align__(128) double smem[];
-  double* Zs = smem;                     // [2][TR][288] swizzled (neighbour traces, then Y)
-  double* Ts = smem + 2 * TR * kRS;      // [2][Bt][288] own traces (TMA copy, unswizzled)
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(Ts + 2 * Bt * kRS);
+  double* O = smem;                    // own face block [lane][TS]
+  double* NB = smem + FACE;            // [2][lane][TS] neighbour face blocks
+  double* Y = smem + 3 * FACE;         // [Bt][288] mixed face values
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(Y + Bt * kRS);  // own, nb0, nb1
   Ctx x;
-  x.lane = threadIdx.x & 31;
-  x.p = threadIdx.x >> 5;
+  init_ctx(x);
   x.frags = frag_table<N>();
-  const int col = x.p * kL + x.lane;
-  for (int i = threadIdx.x; i < 2 * (TR - Bt) * kRS; i += blockDim.x) {
-    const int f = i / ((TR - Bt) * kRS), r = i % ((TR - Bt) * kRS);
-    Zs[f * TR * kRS + Bt * kRS + r] = 0.0;  // padding rows of the lift k-steps stay zero
+  if (blockIdx.x >= prm.ntiles) return;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
   }
-  if (threadIdx.x == 0) mbar_init(bar, 1);
   __syncthreads();
-  unsigned phase = 0;
-  constexpr unsigned kTBytes = 2 * Bt * kRS * sizeof(double);
+  auto issue_own = [&](int64_t tile, int F) {  // one thread
+    mbar_expect_tx(&bar[0], FACE * sizeof(double));
+    bulk_g2s(O, prm.traces + (tile * 4 + F) * FACE, FACE * sizeof(double), &bar[0]);
+  };
+  auto issue_nb = [&](int64_t tile, int F, int b) {  // warp 0
+    if (x.lane == 0) mbar_expect_tx(&bar[1 + b], FACE * sizeof(double));
+    __syncwarp();
+    const int64_t slot = (tile * 4 + F) * kL + x.lane;
+    const int64_t nbe = prm.nb[slot];
+    const int j = prm.jh[slot] & 3;
+    bulk_g2s(NB + b * FACE + x.lane * TS, prm.traces + ((nbe >> 5) * 4 + j) * FACE + (nbe & 31) * TS,
+             TS * sizeof(double), &bar[1 + b]);
+  };
+  if (threadIdx.x < kL) {
+    if (threadIdx.x == 0) issue_own(prm.tile0 + blockIdx.x, 0);
+    issue_nb(prm.tile0 + blockIdx.x, 0, 0);
+  }
+  unsigned ph_o = 0, ph_n0 = 0, ph_n1 = 0;
   for (int64_t it = blockIdx.x; it < prm.ntiles; it += gridDim.x) {
     const int64_t tile = prm.tile0 + it;
-    double* Qt = prm.Q + tile * B * kRS;
-    const double* gtr = prm.traces + tile * 4 * Bt * kRS;
-    if (threadIdx.x == 0 && it + gridDim.x < prm.ntiles) {
-      const int64_t nt = tile + gridDim.x;
-      prefetch_l2(prm.traces + nt * 4 * Bt * kRS, 4 * Bt * kRS * sizeof(double));
-      prefetch_l2(prm.aplus + nt * 4 * kP * kP * kL, 4 * kP * kP * kL * sizeof(double));
-      prefetch_l2(prm.aminus + nt * 4 * kP * kP * kL, 4 * kP * kP * kL * sizeof(double));
-      prefetch_l2(prm.Q + nt * B * kRS, B * kRS * sizeof(double));
-    }
+    const bool more = it + gridDim.x < prm.ntiles;
 #pragma unroll
-    for (int pass = 0; pass < 2; ++pass) {
-      // 1. all loads of the pass in flight at once
-      if (threadIdx.x == 0) {
-        mbar_expect_tx(bar, kTBytes);
-        bulk_g2s(Ts, gtr + 2 * pass * Bt * kRS, kTBytes, bar);
+    for (int F = 0; F < 4; ++F) {
+      const int b = F & 1;
+      __syncthreads();  // lift of the previous face done: Y and neighbour buffer b ^ 1 are free
+      if (threadIdx.x < kL) {
+        if (F < 3) issue_nb(tile, F + 1, b ^ 1);
+        else if (more) issue_nb(tile + gridDim.x, 0, b ^ 1);
       }
-      int hh[2];
-#pragma unroll
-      for (int f = 0; f < 2; ++f) {
-        const int F = 2 * pass + f;
-        const int64_t slot = (tile * 4 + F) * kL + x.lane;
-        const int64_t nbe = prm.nb[slot];
-        const int jh = prm.jh[slot];
-        hh[f] = jh >> 2;
-        const double* src = prm.traces + (((nbe >> 5) * 4 + (jh & 3)) * Bt) * kRS + x.p * kL + (nbe & 31);
-        double* Z = Zs + f * TR * kRS;
-#pragma unroll
-        for (int n = 0; n < Bt; ++n) cp_async8(Z + swz(n, col), src + n * kRS);
+      double* Z = NB + b * FACE + x.lane * TS;
+      const int h = prm.jh[(tile * 4 + F) * kL + x.lane] >> 2;
+      if (b == 0) {
+        mbar_wait(&bar[1], ph_n0);
+        ph_n0 ^= 1;
+      } else {
+        mbar_wait(&bar[2], ph_n1);
+        ph_n1 ^= 1;
       }
-      double ap[2][kP], am[2][kP];
+      {  // z = f^h t on the own column of the lane's neighbour block
+        double t[Bt];
 #pragma unroll
-      for (int f = 0; f < 2; ++f) {
-        const int64_t fo = ((tile * 4 + 2 * pass + f) * kP + x.p) * kP * kL + x.lane;
+        for (int n = 0; n < Bt; ++n) t[n] = Z[n * kP + x.p];
+        G::rot(h, t, Z + x.p);
+      }
+      double ap[kP], am[kP];
+      {
+        const int64_t fo = ((tile * 4 + F) * kP + x.p) * kP * kL + x.lane;
 #pragma unroll
         for (int q = 0; q < kP; ++q) {
-          ap[f][q] = prm.aplus[fo + q * kL];
-          am[f][q] = prm.aminus[fo + q * kL];
+          ap[q] = prm.aplus[fo + q * kL];
+          am[q] = prm.aminus[fo + q * kL];
         }
       }
-      cp_async_wait_all();
-      // 2. rotate the own column of Z in place: z = f^h t
-#pragma unroll
-      for (int f = 0; f < 2; ++f) {
-        double* Z = Zs + f * TR * kRS;
-        double tn[Bt];
-#pragma unroll
-        for (int n = 0; n < Bt; ++n) tn[n] = Z[swz(n, col)];
-        Gen<N>::template rot<double>(hh[f], tn, [&](int m, double z) { Z[swz(m, col)] = z; });
-      }
-      mbar_wait(bar, phase);
-      phase ^= 1;
-      __syncthreads();
-      // 3. Y = T A+^T + Z A-^T per element
-      double y[2][Bt];
-#pragma unroll
-      for (int f = 0; f < 2; ++f) {
-        const double* Z = Zs + f * TR * kRS;
-        const double* T = Ts + f * Bt * kRS + x.lane;
+      mbar_wait(&bar[0], ph_o);
+      ph_o ^= 1;
+      __syncthreads();  // rotated neighbour columns visible
+      {
+        const double* T = O + x.lane * TS;
 #pragma unroll
         for (int m = 0; m < Bt; ++m) {
-          double sacc = 0.0;
+          double s = 0.0;
 #pragma unroll
-          for (int q = 0; q < kP; ++q)
-            sacc = fma(T[m * kRS + q * kL], ap[f][q], fma(Z[swz(m, q * kL + x.lane)], am[f][q], sacc));
-          y[f][m] = sacc;
+          for (int q = 0; q < kP; ++q) s = fma(T[m * kP + q], ap[q], fma(Z[m * kP + q], am[q], s));
+          Y[swz(m, x.p * kL + x.lane)] = s;
         }
       }
-      __syncthreads();  // all columns of Z and T read
-#pragma unroll
-      for (int f = 0; f < 2; ++f)
-#pragma unroll
-        for (int m = 0; m < Bt; ++m) Zs[f * TR * kRS + swz(m, col)] = y[f][m];
-      __syncwarp();
-      // 4. lift with the DMMA tiles of R^i, update Q
-      double acc[G::QMT][4][2];
-      zero_acc(acc);
-      if (pass == 0) {
-        G::template lift<0>(x, Zs, acc);
-        G::template lift<1>(x, Zs + TR * kRS, acc);
-      } else {
-        G::template lift<2>(x, Zs, acc);
-        G::template lift<3>(x, Zs + TR * kRS, acc);
+      __syncthreads();  // every read of O done; Y complete
+      if (threadIdx.x == 0) {
+        if (F < 3) issue_own(tile, F + 1);
+        else if (more) issue_own(tile + gridDim.x, 0);
       }
-#if YDG_QSTAGE
-      __syncthreads();  // Y consumed by every warp: stage the update over Z and T
-      stage_acc<G::QMT, B>(x, smem, acc);
-      __syncthreads();
-      update_q<B>(Qt, smem);
-#else
-      add_q<G::QMT, B>(x, Qt, acc);
-#endif
-      __syncthreads();  // before the next pass overwrites Z and T
+      // lift and Q update per face: the accumulators live only here (168 registers per
+      // thread with 9 warps); the tile's Q stays in L2 across its four updates
+      double acc[G::LMT][4][2];
+      zero_acc(acc);
+      if (F == 0) G::template lift<0>(x, Y, acc);
+      else if (F == 1) G::template lift<1>(x, Y, acc);
+      else if (F == 2) G::template lift<2>(x, Y, acc);
+      else G::template lift<3>(x, Y, acc);
+      G::add_lift(x, prm.Q + tile * B * kRS, acc);
     }
   }
 }

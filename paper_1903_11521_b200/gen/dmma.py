@@ -7,221 +7,306 @@ Every product of a global matrix with a tile of 32 elements x 9 quantity columns
     trace     T_i     =  R^iT                       I
     lift      Q      +=  R^i                        Y_i
 
-is a GEMM with M = matrix rows, K = matrix columns and N = 288 data columns; it is cut into
-8x4 matrix tiles (the DMMA A operand) and only the tiles holding a nonzero are issued --
-the zero-block exploitation of the paper's equivalent sparsity patterns at
-tensor-core granularity.  Each warp owns the four 8-column data tiles of one quantity
-(warp = quantity column p, 32 elements), so every DMMA B operand is warp-private.
+is a GEMM with M = matrix rows, K = matrix columns and N = 288 data columns, issued as
+8x4 matrix tiles (the DMMA A operand).  The rows of a tile are not fixed blocks: an
+m-tile is any 8 output rows and a k-set any 4 input rows (gen/tiling.py chooses them to
+minimise the number of nonzero tiles -- the zero-block exploitation of the paper's
+equivalent sparsity patterns, with free block boundaries).  Input rows reach
+the B operand either through the warp-private star chunk X (CK, volume: the chunk is
+built from the 4 rows named at compile time) or by a per-lane gathered shared-memory load
+(trace, lift: lane row = byte (lane & 3) of a 32-bit immediate); accumulator rows are
+scattered on write-back (row = byte (lane >> 2) of a 64-bit immediate, 0xff = padding).
 
-The A fragments are stored lane-ordered (lane i holds A[i/4][i%4]) in a device table,
-one coalesced 256-byte load per tile.  Emits ``csrc/generated/ydg_dmma_N{n}.cuh``.
+Each warp owns the four 8-column data tiles of one quantity (warp = quantity column p,
+32 elements), so every B operand it feeds to a DMMA is warp-private.  A fragments are
+stored lane-ordered (lane i holds A[i/4][i%4]) in a device table, one coalesced 256-byte
+load per tile, issued one k-set ahead of use.
+
+Emits ``csrc/generated/ydg_dmma_N{n}.cuh``.
 """
 from __future__ import annotations
 
 import os
 from math import comb
 
-from . import tables
+from . import tables, tiling
 
 ORDERS = (1, 2, 3, 4, 5, 6)
+PAD = 0xFF
 
 
 def r8(x):
     return (x + 7) // 8 * 8
 
 
-def r4(x):
-    return (x + 3) // 4 * 4
-
-
 class Table:
     def __init__(self):
         self.frags = []  # list of 32-value lists
 
-    def add(self, M, m0, l0):
-        """Fragment of matrix M (callable (row, col) -> value) at tile origin; None if zero."""
-        vals = [M(m0 + i // 4, l0 + i % 4) for i in range(32)]
+    def add(self, M, rows, cols):
+        """Fragment of matrix M (callable (row, col) -> value) on the given output rows (8,
+        None = padding) and input columns (4, None = padding); None if all zero."""
+        vals = []
+        for i in range(32):
+            r, c = rows[i // 4], cols[i % 4]
+            vals.append(0.0 if r is None or c is None else float(M(r, c)))
         if not any(v != 0.0 for v in vals):
             return None
         self.frags.append(vals)
         return len(self.frags) - 1
 
 
-def emit_kstep(b, src, ks, tiles):
-    """X^c = D A*^cT for rows 4ks..4ks+3 (warp-private staging), then per c: B fragments and
-    the DMMAs of that c's nonzero tiles (one c's B fragments live at a time)."""
-    b(f"    xchunk<{src}, B>(x, {4 * ks});")
-    for c in range(3):
-        mine = [(mt, tid) for cc, mt, tid in tiles if cc == c]
-        if not mine:
-            continue
-        b(f"    {{ double bf[4]; xb_b(x, {c}, bf);")
-        for mt, tid in mine:
-            b(f"      {{ const double a = afrag(x, {tid}); dmma4(acc[{mt}], a, bf); }}")
-        b("    }")
-    b("    __syncwarp();")
+def pad_rows(g, n):
+    return list(g) + [None] * (n - len(g))
+
+
+def row_word64(rows):
+    w = 0
+    for i, r in enumerate(pad_rows(rows, 8)):
+        w |= (PAD if r is None else r) << (8 * i)
+    return f"0x{w:016x}ULL"
+
+
+def kset_word(rows):
+    """32-bit gather word; padding slots repeat the first row (their A column is zero)."""
+    rr = list(rows) + [rows[0]] * (4 - len(rows))
+    w = 0
+    for i, r in enumerate(rr):
+        w |= r << (8 * i)
+    return f"0x{w:08x}u"
+
+
+def kset_rows(rows):
+    return list(rows) + [rows[0]] * (4 - len(rows))
+
+
+class Emit:
+    def __init__(self):
+        self.lines = []
+        self.n = 0
+
+    def __call__(self, s):
+        self.lines.append(s)
+
+
+def emit_xprod(b, tab, name, mats, til, src, acc="acc"):
+    """CK / volume style product: per k-set the warp-private star chunk X^c of the 4 rows
+    (uniform across lanes), then per c the DMMAs of that c's nonzero tiles.  A fragments of
+    the next k-set are loaded before the current k-set's work."""
+    outs = til["out"]
+    ins = til["in"][0]
+    plan = []  # per k-set: list of (c, mt, tid)
+    for ks in ins:
+        cols = pad_rows(ks, 4)
+        tiles = []
+        for c, M in enumerate(mats):
+            for mt, og in enumerate(outs):
+                tid = tab.add(M, pad_rows(og, 8), cols)
+                if tid is not None:
+                    tiles.append((c, mt, tid))
+        plan.append(tiles)
+    b(f"    // {name}: {sum(len(t) for t in plan)} tiles, {len(ins)} k-sets, {len(outs)} m-tiles")
+    nv = 0
+    names = []
+    for i, tiles in enumerate(plan):
+        nm = [f"a{i}_{j}" for j in range(len(tiles))]
+        names.append(nm)
+    if plan and plan[0]:
+        b("    const double " + ", ".join(f"{n} = afrag(x, {t[2]})" for n, t in zip(names[0], plan[0])) + ";")
+    for i, (ks, tiles) in enumerate(zip(ins, plan)):
+        if i + 1 < len(plan) and plan[i + 1]:
+            b("    const double " + ", ".join(f"{n} = afrag(x, {t[2]})" for n, t in zip(names[i + 1], plan[i + 1])) + ";")
+        r = kset_rows(ks)
+        b(f"    xchunk<{src}, B>(x, {r[0]}, {r[1]}, {r[2]}, {r[3]});")
+        for c in range(len(mats)):
+            mine = [(mt, nm) for (cc, mt, tid), nm in zip(tiles, names[i]) if cc == c]
+            if not mine:
+                continue
+            b(f"    {{ double bf[4]; xb_b(x, {c}, bf);")
+            for mt, nm in mine:
+                b(f"      dmma4({acc}[{mt}], {nm}, bf);")
+            b("    }")
+        b("    __syncwarp();")
+        nv += len(tiles)
+    return nv
+
+
+def emit_gprod(b, tab, M, outs, ins, loader, acc="acc", pre=None):
+    """Trace / lift style product: B fragments gathered per lane from memory
+    (``loader(kset_index, word)`` returns the C expression filling ``bf``)."""
+    plan = []
+    for ks in ins:
+        cols = pad_rows(ks, 4)
+        tiles = []
+        for mt, og in enumerate(outs):
+            tid = tab.add(M, pad_rows(og, 8), cols)
+            if tid is not None:
+                tiles.append((mt, tid))
+        plan.append(tiles)
+    n = 0
+    live = [(i, ks, t) for i, (ks, t) in enumerate(zip(ins, plan)) if t]
+    names = {i: [f"g{i}_{j}" for j in range(len(t))] for i, _, t in live}
+    if live:
+        i0 = live[0][0]
+        b("      const double " + ", ".join(f"{nm} = afrag(x, {t[1]})" for nm, t in zip(names[i0], live[0][2])) + ";")
+    for k, (i, ks, tiles) in enumerate(live):
+        if k + 1 < len(live):
+            i1 = live[k + 1][0]
+            b("      const double " + ", ".join(f"{nm} = afrag(x, {t[1]})" for nm, t in zip(names[i1], live[k + 1][2])) + ";")
+        src = loader(i, kset_word(ks))
+        b(f"      {{ {src}")
+        for (mt, tid), nm in zip(tiles, names[i]):
+            b(f"        dmma4({acc}[{mt}], {nm}, bf);")
+        b("      }")
+        n += len(tiles)
+    return n
 
 
 def gen_order(N):
     t = tables.load(N)
-    K, R = t["K"], t["R"]
+    K, R, f = t["K"], t["R"], t["f"]
     B, Bt = t["B"], t["Bt"]
     Bv = comb(N + 2, 3)
+    til = tiling.tiling(N)
     tab = Table()
-    lines = []
-    e = lines.append
-
-    def mat(Mfun, nrows, ncols):
-        return lambda r, c: (Mfun(r, c) if r < nrows and c < ncols else 0.0)
-
-    e(f"// GENERATED by paper_1903_11521_b200/gen/dmma.py for N = {N} -- do not edit.")
-    e("#pragma once")
-    e("namespace ydg {")
-    e("namespace dm {")
-    e(f"template <> struct DG<{N}> {{")
-    e(f"  static constexpr int N = {N}, B = {B}, Bt = {Bt}, Bv = {Bv};")
-    e(f"  static constexpr int SROWS = {r8(comb(N + 2, 3)) if N > 0 else 8};  // rows of S (D^d, d >= 1)")
-    e(f"  static constexpr int IROWS = {r8(Bv)};  // rows of the time-integral region")
-    e(f"  static constexpr int TROWS = {r8(Bt)};  // rows of a face staging region")
-    e(f"  static constexpr int QMT = {r8(B) // 8};  // m-tiles of a B-row output")
+    IROWS = min(B, r8(Bv))
+    SROWS = max(8, r8(comb(N + 2, 3)))
+    TS = (9 * Bt + 1) // 2 * 2
+    QMT = len(til["vol"]["out"])
+    LMT = len(til["lift"]["out"])
+    TMT = max(len(til[f"tr{i}"]["out"]) for i in range(4))
     body = []
     b = body.append
+    counts = {}
     # ---------------- CK
     for d in range(N):
         bi, bo = comb(N - d + 3, 3), comb(N - d + 2, 3)
-        MT = r8(bo) // 8
-        KS = r4(bi) // 4
-        b(f"  // CK step d = {d}: rows in {bi}, rows out {bo} ({MT} m-tiles, {KS} k-steps)")
+        tl = til[f"ck{d}"]
+        MT = len(tl["out"])
+        mats = [(lambda r, col, c=c: -K[c][col][r]) for c in range(3)]  # Kt^c[r][col] = -K^c[col][r]
+        b(f"  // CK step d = {d}: rows in {bi}, rows out {bo}")
         b(f"  static __device__ __forceinline__ void ck{d}(Ctx& x) {{")
         b(f"    double acc[{MT}][4][2];")
-        b(f"    zero_acc(acc);")
-        for ks in range(KS):
-            tiles = []
-            for c in range(3):
-                Mc = mat(lambda r, col, c=c: -K[c][col][r], bo, bi)  # Kt^c[r][col] = -K^c[col][r]
-                for mt in range(MT):
-                    tid = tab.add(Mc, 8 * mt, 4 * ks)
-                    if tid is not None:
-                        tiles.append((c, mt, tid))
-            src = "SRC_Q" if d == 0 else "SRC_S"
-            emit_kstep(b, src, ks, tiles)
-        b(f"    __syncthreads();")
-        b(f"    ck_writeback<{MT}, {1 if d == 0 else 0}, B>(x, acc, {d});")
-        b(f"    __syncthreads();")
+        b("    zero_acc(acc);")
+        counts[f"ck{d}"] = emit_xprod(b, tab, f"ck{d}", mats, tl, "SRC_Q" if d == 0 else "SRC_S")
+        b("    __syncthreads();  // every read of D^d done")
+        for mt, og in enumerate(tl["out"]):
+            b(f"    ck_wb<{1 if d == 0 else 0}, B>(x, acc[{mt}], {d}, {row_word64(og)});")
+        if d == 0 and IROWS > bo:
+            b(f"    scale_irows<{bo}, {IROWS}>(x);  // rows of I fed by D^0 only: dt * Q")
+        b("    __syncthreads();")
         b("  }")
     b("  static __device__ __forceinline__ void ck(Ctx& x) {")
     for d in range(N):
         b(f"    ck{d}(x);")
     b("  }")
     # ---------------- volume
-    MT = r8(B) // 8
-    KS = r4(Bv) // 4
-    b(f"  // volume: Q += sum_c Khat^c (I A*^cT), {MT} m-tiles, {KS} k-steps")
-    b(f"  static __device__ __forceinline__ void volume(Ctx& x, double (&acc)[{MT}][4][2]) {{")
-    for ks in range(KS):
-        tiles = []
-        for c in range(3):
-            Mc = mat(lambda r, col, c=c: K[c][r][col], B, Bv)
-            for mt in range(MT):
-                tid = tab.add(Mc, 8 * mt, 4 * ks)
-                if tid is not None:
-                    tiles.append((c, mt, tid))
-        emit_kstep(b, "SRC_I", ks, tiles)
+    tl = til["vol"]
+    mats = [(lambda r, col, c=c: K[c][r][col]) for c in range(3)]
+    b(f"  // volume: Q += sum_c Khat^c (I A*^cT)")
+    b(f"  static __device__ __forceinline__ void volume(Ctx& x, double (&acc)[{QMT}][4][2]) {{")
+    counts["vol"] = emit_xprod(b, tab, "vol", mats, tl, "SRC_I")
+    b("  }")
+    b(f"  static __device__ __forceinline__ void add_volume(const Ctx& x, double* Qt, const double (&acc)[{QMT}][4][2]) {{")
+    for mt, og in enumerate(tl["out"]):
+        b(f"    add_q(x, Qt, acc[{mt}], {row_word64(og)});")
     b("  }")
     # ---------------- traces T_i = R^iT I
-    MTt = r8(Bt) // 8
-    KSt = r4(B) // 4
-    b(f"  // trace: T_F = R^FT I, {MTt} m-tiles, {KSt} k-steps (rows < IROWS from the I region,")
-    b(f"  // the rest is dt * Q from global memory)")
-    b(f"  template <int F> static __device__ __forceinline__ void trace(Ctx& x, double (&acc)[{MTt}][4][2]) {{")
-    ksq = [ks for ks in range(KSt) if 4 * ks >= r8(Bv)]  # k-steps fed from global dt * Q
-    b(f"    double bq[{max(1, len(ksq))}][4];  // global B fragments, loaded first (latency overlap)")
-    for n, ks in enumerate(ksq):
-        b(f"    gq_b<B>(x, {4 * ks}, bq[{n}]);")
+    b(f"  // trace: T_F = R^FT I (rows < IROWS of I from shared memory, dt * Q from global memory);")
+    b(f"  // the C fragments go to the staging block [lane][m][q] (stride TS)")
+    b(f"  template <int F> static __device__ __forceinline__ void trace(Ctx& x, double* stg) {{")
     for i in range(4):
+        tl = til[f"tr{i}"]
+        ins = tl["in"][0]
+        outs = tl["out"]
         b(f"    {'if' if i == 0 else 'else if'} constexpr (F == {i}) {{")
-        Mi = mat(lambda r, col, i=i: R[i][col][r], Bt, B)
-        for ks in range(KSt):
-            tiles = []
-            for mt in range(MTt):
-                tid = tab.add(Mi, 8 * mt, 4 * ks)
-                if tid is not None:
-                    tiles.append((mt, tid))
-            if not tiles:
-                continue
-            if ks in ksq:
-                src = f"bq[{ksq.index(ks)}]"
-                b("      {")
-            else:
-                src = "bf"
-                b(f"      {{ double bf[4]; ismem_b(x, {4 * ks}, bf);")
-            for mt, tid in tiles:
-                b(f"        {{ const double a = afrag(x, {tid}); dmma4(acc[{mt}], a, {src}); }}")
-            b("      }")
+        b(f"      double acc[{len(outs)}][4][2];")
+        b("      zero_acc(acc);")
+        gl = [k for k, ks in enumerate(ins) if ks[0] >= IROWS]
+        if gl:
+            b(f"      double bq[{len(gl)}][4];  // global B fragments first (latency overlap)")
+            for n_, k in enumerate(gl):
+                b(f"      gq_b<B>(x, {kset_word(ins[k])}, bq[{n_}]);")
+
+        def loader(k, w, gl=gl):
+            if k in gl:
+                return f"const double (&bf)[4] = bq[{gl.index(k)}];"
+            return f"double bf[4]; ismem_b(x, {w}, bf);"
+        Mi = lambda r, col, i=i: R[i][col][r]
+        counts[f"tr{i}"] = emit_gprod(b, tab, Mi, outs, ins, loader)
+        for mt, og in enumerate(outs):
+            b(f"      stage_trace<{TS}>(x, stg, acc[{mt}], {row_word64(og)});")
         b("    }")
     b("  }")
-    # ---------------- lift Q += R^i Y_i
-    MTl = r8(B) // 8
-    KSl = r4(Bt) // 4
-    b(f"  // lift: acc += R^F Y (Y own columns in shared memory), {MTl} m-tiles, {KSl} k-steps")
-    b(f"  template <int F> static __device__ __forceinline__ void lift(Ctx& x, const double* Y, double (&acc)[{MTl}][4][2]) {{")
+    # ---------------- lift Q += R^i Y_i (shared output tiling over the four faces)
+    tl = til["lift"]
+    b(f"  // lift: acc += R^F Y_F (Y own columns in shared memory, rows [m][288])")
+    b(f"  template <int F> static __device__ __forceinline__ void lift(Ctx& x, const double* Y, double (&acc)[{LMT}][4][2]) {{")
+    counts["lift"] = 0
     for i in range(4):
         b(f"    {'if' if i == 0 else 'else if'} constexpr (F == {i}) {{")
-        Mi = mat(lambda r, col, i=i: R[i][r][col], B, Bt)
-        for ks in range(KSl):
-            tiles = []
-            for mt in range(MTl):
-                tid = tab.add(Mi, 8 * mt, 4 * ks)
-                if tid is not None:
-                    tiles.append((mt, tid))
-            if not tiles:
-                continue
-            b(f"      {{ double bf[4]; smem_b(x, Y, {4 * ks}, bf);")
-            for mt, tid in tiles:
-                b(f"        {{ const double a = afrag(x, {tid}); dmma4(acc[{mt}], a, bf); }}")
-            b("      }")
+        Mi = lambda r, col, i=i: R[i][r][col]
+        counts["lift"] += emit_gprod(b, tab, Mi, tl["out"], tl["in"][i],
+                                     lambda k, w: f"double bf[4]; smem_b(x, Y, {w}, bf);")
         b("    }")
     b("  }")
-    e(f"  static constexpr int NFRAG = {len(tab.frags)};")
+    b(f"  static __device__ __forceinline__ void add_lift(const Ctx& x, double* Qt, const double (&acc)[{LMT}][4][2]) {{")
+    for mt, og in enumerate(tl["out"]):
+        b(f"    add_q(x, Qt, acc[{mt}], {row_word64(og)});")
+    b("  }")
+    # ---------------- neighbour orientation z = f^h t, uniform over lanes:
+    # f^1 = S (diagonal +-1) and f^2 = S f^0 S, so t' = (h != 0 ? S t : t), u = f^0 t',
+    # z = (h == 1 ? t' : (h == 2 ? S u : u))
+    S = [f[1][m][m] for m in range(Bt)]
+    for m in range(Bt):
+        for n in range(Bt):
+            assert (m == n) or f[1][m][n] == 0.0
+            assert abs(f[2][m][n] - S[m] * f[0][m][n] * S[n]) < 1e-14
+    b("  // z = f^h t (P:1342) for every lane's own h, without divergence (f^1 = S diagonal,")
+    b("  // f^2 = S f^0 S); z[m * kP] receives row m")
+    b(f"  static __device__ __forceinline__ void rot(int h, double (&t)[{Bt}], double* z) {{")
+    b("    const bool fl = h != 0, id = h == 1, s2 = h == 2;")
+    for n in range(Bt):
+        if S[n] < 0:
+            b(f"    t[{n}] = fl ? -t[{n}] : t[{n}];")
+    for m in range(Bt):
+        terms = [(n, f[0][m][n]) for n in range(Bt) if f[0][m][n] != 0.0]
+        expr = None
+        for n, v in terms:
+            expr = f"{float(v)!r} * t[{n}]" if expr is None else f"fma({float(v)!r}, t[{n}], {expr})"
+        b(f"    {{ const double u = {expr or '0.0'};")
+        if S[m] < 0:
+            b(f"      z[{m} * kP] = id ? t[{m}] : (s2 ? -u : u); }}")
+        else:
+            b(f"      z[{m} * kP] = id ? t[{m}] : u; }}")
+    b("  }")
+    lines = [f"// GENERATED by paper_1903_11521_b200/gen/dmma.py for N = {N} -- do not edit.",
+             "#pragma once", "namespace ydg {", "namespace dm {", f"template <> struct DG<{N}> {{",
+             f"  static constexpr int N = {N}, B = {B}, Bt = {Bt}, Bv = {Bv};",
+             f"  static constexpr int SROWS = {SROWS};  // rows of S (D^d, d >= 1)",
+             f"  static constexpr int IROWS = {IROWS};  // rows of the time-integral region",
+             f"  static constexpr int TS = {TS};  // doubles per element-face trace block [m][q]",
+             f"  static constexpr int QMT = {QMT}, LMT = {LMT}, TMT = {TMT};",
+             f"  static constexpr int NFRAG = {len(tab.frags)};",
+             "  // DMMA tiles per product (x 4 col tiles x 9 warps per 32-element tile): " +
+             ", ".join(f"{k} {v}" for k, v in counts.items())]
     lines += body
-    e("};")
-    # fragment table
-    e(f"__device__ const double frag_N{N}[{max(1, len(tab.frags)) * 32}] = {{")
+    lines.append("};")
+    lines.append(f"__device__ const double frag_N{N}[{max(1, len(tab.frags)) * 32}] = {{")
     flat = [v for fr in tab.frags for v in fr] or [0.0] * 32
     for s in range(0, len(flat), 8):
-        e("  " + ", ".join(repr(float(v)) if v != 0 else "0.0" for v in flat[s:s + 8]) + ",")
-    e("};")
-    e(f"template <> __device__ __forceinline__ const double* frag_table<{N}>() {{ return frag_N{N}; }}")
-    e("}  // namespace dm")
-    e("}  // namespace ydg")
-    return "\n".join(lines) + "\n", len(tab.frags)
+        lines.append("  " + ", ".join(repr(float(v)) if v != 0 else "0.0" for v in flat[s:s + 8]) + ",")
+    lines.append("};")
+    lines.append(f"template <> __device__ __forceinline__ const double* frag_table<{N}>() {{ return frag_N{N}; }}")
+    lines.append("}  // namespace dm")
+    lines.append("}  // namespace ydg")
+    return "\n".join(lines) + "\n", counts
 
 
 def dmma_counts(N):
-    """(tensor-core MACs executed per element, nonzero MACs) of the DMMA products."""
-    t = tables.load(N)
-    K, R = t["K"], t["R"]
-    B, Bt = t["B"], t["Bt"]
-    Bv = comb(N + 2, 3)
-
-    def tiles(Mfun, M, Kd, nr, nc):
-        n = 0
-        for m0 in range(0, r8(M), 8):
-            for l0 in range(0, r4(Kd), 4):
-                if any(Mfun(m0 + i // 4, l0 + i % 4) != 0 for i in range(32)
-                       if m0 + i // 4 < nr and l0 + i % 4 < nc):
-                    n += 1
-        return n
-    n = 0
-    for d in range(N):
-        bi, bo = comb(N - d + 3, 3), comb(N - d + 2, 3)
-        for c in range(3):
-            n += tiles(lambda r, col, c=c: -K[c][col][r], bo, bi, bo, bi)
-    for c in range(3):
-        n += tiles(lambda r, col, c=c: K[c][r][col], B, Bv, B, Bv)
-    for i in range(4):
-        n += tiles(lambda r, col, i=i: R[i][col][r], Bt, B, Bt, B)
-        n += tiles(lambda r, col, i=i: R[i][r][col], B, Bt, B, Bt)
+    """(tensor-core MACs executed per element) of the DMMA products."""
+    til = tiling.tiling(N)
+    n = sum(v["tiles"] for v in til.values())
     return n * 32 * 9
 
 
@@ -229,10 +314,10 @@ def main():
     here = os.path.dirname(os.path.abspath(__file__))
     outdir = os.path.join(here, "..", "csrc", "generated")
     for N in ORDERS:
-        text, nf = gen_order(N)
+        text, counts = gen_order(N)
         with open(os.path.join(outdir, f"ydg_dmma_N{N}.cuh"), "w") as fh:
             fh.write(text)
-        print(f"N={N}: {nf} fragments")
+        print(f"N={N}: {counts}")
 
 
 if __name__ == "__main__":
