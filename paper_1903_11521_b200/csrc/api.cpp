@@ -120,19 +120,26 @@ int check(ydg_solver* h) {
   return YDG_OK;
 }
 
+// Per-element coefficients in the tiled layouts of the kernels.  fp64 (tensor-core
+// kernels): star [tile][c][p][3][32] and the factored flux solvers [tile][face][12][32];
+// fp32 (sparse kernels): star and the flux-solver matrices A+-, [tile][face][p][q][32].
 template <typename T>
-void pack_tiles(int P, int64_t n0, int64_t n, int64_t slot0, const ElementCoeffs& c,
-                std::vector<T>& star, std::vector<T>& ap, std::vector<T>& am) {
-  // element t of the chunk -> local slot slot0 + t
-  (void)n0;
+void pack_tiles(int P, int64_t n, bool factored, const ElementCoeffs& c, std::vector<T>& star,
+                std::vector<T>& ap, std::vector<T>& am) {
   for (int64_t t = 0; t < n; ++t) {
-    const int64_t s = slot0 + t;
-    const int64_t tile = s / kLanes, lane = s % kLanes;
+    const int64_t tile = t / kLanes, lane = t % kLanes;
     for (int cc = 0; cc < 3; ++cc)
       for (int p = 0; p < P; ++p)
         for (int j = 0; j < 3; ++j)
           star[(((tile * 3 + cc) * P + p) * 3 + j) * kLanes + lane] =
               static_cast<T>(c.star[((t * 3 + cc) * P + p) * 3 + j]);
+    if (factored) {
+      for (int i = 0; i < 4; ++i)
+        for (int k = 0; k < kFaceCoeffs; ++k)
+          ap[((tile * 4 + i) * kFaceCoeffs + k) * kLanes + lane] =
+              static_cast<T>(c.face[(t * 4 + i) * kFaceCoeffs + k]);
+      continue;
+    }
     for (int i = 0; i < 4; ++i)
       for (int p = 0; p < P; ++p)
         for (int q = 0; q < P; ++q) {
@@ -146,16 +153,19 @@ void pack_tiles(int P, int64_t n0, int64_t n, int64_t slot0, const ElementCoeffs
 template <typename T>
 int upload_coeffs(ydg_solver* h, const double* xyz, const double* material, const double* anel) {
   const int P = h->P;
+  const bool factored = sizeof(T) == 8;  // fp64 flux kernel rebuilds A+- from 12 values/face
   const int64_t tiles = h->nslots / kLanes;
-  const size_t star_n = static_cast<size_t>(tiles) * 3 * P * 3 * kLanes;
-  const size_t flux_n = static_cast<size_t>(tiles) * 4 * P * P * kLanes;
+  const size_t star_t = static_cast<size_t>(3) * P * 3 * kLanes;  // per tile
+  const size_t flux_t = factored ? static_cast<size_t>(4) * kFaceCoeffs * kLanes : static_cast<size_t>(4) * P * P * kLanes;
   int rc;
-  if ((rc = dalloc(h, &h->star, star_n * sizeof(T)))) return rc;
-  if ((rc = dalloc(h, &h->aplus, flux_n * sizeof(T)))) return rc;
-  if ((rc = dalloc(h, &h->aminus, flux_n * sizeof(T)))) return rc;
-  CUDA_OR_FAIL(h, cudaMemset(h->star, 0, star_n * sizeof(T)));
-  CUDA_OR_FAIL(h, cudaMemset(h->aplus, 0, flux_n * sizeof(T)));
-  CUDA_OR_FAIL(h, cudaMemset(h->aminus, 0, flux_n * sizeof(T)));
+  if ((rc = dalloc(h, &h->star, tiles * star_t * sizeof(T)))) return rc;
+  if ((rc = dalloc(h, &h->aplus, tiles * flux_t * sizeof(T)))) return rc;
+  CUDA_OR_FAIL(h, cudaMemset(h->star, 0, tiles * star_t * sizeof(T)));
+  CUDA_OR_FAIL(h, cudaMemset(h->aplus, 0, tiles * flux_t * sizeof(T)));
+  if (!factored) {
+    if ((rc = dalloc(h, &h->aminus, tiles * flux_t * sizeof(T)))) return rc;
+    CUDA_OR_FAIL(h, cudaMemset(h->aminus, 0, tiles * flux_t * sizeof(T)));
+  }
   // owned elements in chunks of whole tiles
   const int64_t chunk_tiles = 2048;
   std::vector<T> st, ap, am;
@@ -167,33 +177,34 @@ int upload_coeffs(ydg_solver* h, const double* xyz, const double* material, cons
     std::string err;
     if (!element_coeffs(P, h->first + s0, n, xyz, material, anel, h->nbr, &c, &err))
       return fail(h, YDG_ERR_MESH, err);
-    st.assign(static_cast<size_t>(ct) * 3 * P * 3 * kLanes, T(0));
-    ap.assign(static_cast<size_t>(ct) * 4 * P * P * kLanes, T(0));
-    am.assign(ap.size(), T(0));
-    pack_tiles<T>(P, s0, n, 0, c, st, ap, am);
-    CUDA_OR_FAIL(h, cudaMemcpy(static_cast<T*>(h->star) + static_cast<size_t>(t0) * 3 * P * 3 * kLanes,
-                               st.data(), st.size() * sizeof(T), cudaMemcpyHostToDevice));
-    CUDA_OR_FAIL(h, cudaMemcpy(static_cast<T*>(h->aplus) + static_cast<size_t>(t0) * 4 * P * P * kLanes,
-                               ap.data(), ap.size() * sizeof(T), cudaMemcpyHostToDevice));
-    CUDA_OR_FAIL(h, cudaMemcpy(static_cast<T*>(h->aminus) + static_cast<size_t>(t0) * 4 * P * P * kLanes,
-                               am.data(), am.size() * sizeof(T), cudaMemcpyHostToDevice));
+    st.assign(static_cast<size_t>(ct) * star_t, T(0));
+    ap.assign(static_cast<size_t>(ct) * flux_t, T(0));
+    am.assign(factored ? 0 : ap.size(), T(0));
+    pack_tiles<T>(P, n, factored, c, st, ap, am);
+    CUDA_OR_FAIL(h, cudaMemcpy(static_cast<T*>(h->star) + static_cast<size_t>(t0) * star_t, st.data(),
+                               st.size() * sizeof(T), cudaMemcpyHostToDevice));
+    CUDA_OR_FAIL(h, cudaMemcpy(static_cast<T*>(h->aplus) + static_cast<size_t>(t0) * flux_t, ap.data(),
+                               ap.size() * sizeof(T), cudaMemcpyHostToDevice));
+    if (!factored)
+      CUDA_OR_FAIL(h, cudaMemcpy(static_cast<T*>(h->aminus) + static_cast<size_t>(t0) * flux_t, am.data(),
+                                 am.size() * sizeof(T), cudaMemcpyHostToDevice));
   }
   return YDG_OK;
 }
 
 // Algorithmic HBM bytes per element of each kernel (each array touched once).
-// fp64 (tensor-core kernels): local reads Q, star, writes Q and the 4 traces; the flux
-// kernel reads Q, own + neighbour traces, A+ and A-, writes Q.  fp32 (sparse kernels):
+// fp64 (tensor-core kernels): local reads Q, star, writes Q and the 4 trace blocks; the
+// flux kernel reads Q, own + neighbour trace blocks, the factored flux solvers, writes Q.  fp32 (sparse kernels):
 // the local kernel also reads A+ (local flux), the neighbour kernel reads A- only and the
 // neighbour traces.
 double alg_bytes_local(const ydg_solver* h) {
   const double P = h->P, B = h->B, Bt = h->Bt;
-  if (h->prec == 8) return (2 * B * P + 3 * P * 3 + 4 * Bt * P) * elem_bytes(h);
+  if (h->prec == 8) return (2 * B * P + 3 * P * 3 + 4 * trace_block(h)) * elem_bytes(h);
   return (2 * B * P + 3 * P * 3 + 4 * P * P + 4 * Bt * P) * elem_bytes(h);
 }
 double alg_bytes_neigh(const ydg_solver* h) {
   const double P = h->P, B = h->B, Bt = h->Bt;
-  if (h->prec == 8) return (2 * B * P + 2 * 4 * P * P + 2 * 4 * Bt * P) * elem_bytes(h) + 4 * (4 + 1);
+  if (h->prec == 8) return (2 * B * P + 4 * kFaceCoeffs + 2 * 4 * trace_block(h)) * elem_bytes(h) + 4 * (4 + 1);
   return (2 * B * P + 4 * P * P + 4 * Bt * P) * elem_bytes(h) + 4 * (4 + 1);
 }
 

@@ -13,6 +13,7 @@
 // TMA bulk store, the consumer gathers a neighbour's face with one TMA bulk copy.
 #pragma once
 #include "kernels.cuh"
+#include "setup.h"
 
 namespace ydg {
 namespace dm {
@@ -155,18 +156,33 @@ __device__ __forceinline__ void scale_irows(Ctx& x) {
   }
 }
 
-// Q += acc of one m-tile (rows from the word w): read-modify-write of the C fragments
-// in global memory (16-byte, two elements).
-__device__ __forceinline__ void add_q(const Ctx& x, double* Qt, const double (&acc)[4][2], unsigned long long w) {
-  const int row = mrow(x, w);
-  if (row == 0xff) return;
+// Q += acc over all m-tiles (rows from the words w[]), two m-tiles per batch: the batch's
+// Q loads are all issued before its stores (one L2/HBM latency per batch, bounded register
+// use), values are added into the accumulators, then stored (16-byte, two elements).
+template <int MT>
+__device__ __forceinline__ void add_q(const Ctx& x, double* Qt, double (&acc)[MT][4][2],
+                                      const unsigned long long (&w)[MT]) {
 #pragma unroll
-  for (int ct = 0; ct < 4; ++ct) {
-    double2* q = reinterpret_cast<double2*>(Qt + row * kRS + x.p * kL + 8 * ct + 2 * (x.lane & 3));
-    double2 v = *q;
-    v.x += acc[ct][0];
-    v.y += acc[ct][1];
-    *q = v;
+  for (int m0 = 0; m0 < MT; m0 += 2) {
+    double2 v[2][4];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int row = m0 + k < MT ? mrow(x, w[m0 + k < MT ? m0 + k : 0]) : 0xff;
+#pragma unroll
+      for (int ct = 0; ct < 4; ++ct)
+        v[k][ct] = row == 0xff ? make_double2(0.0, 0.0)
+                               : *reinterpret_cast<const double2*>(Qt + row * kRS + x.p * kL + 8 * ct + 2 * (x.lane & 3));
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (m0 + k >= MT) continue;
+      const int row = mrow(x, w[m0 + k]);
+      if (row == 0xff) continue;
+#pragma unroll
+      for (int ct = 0; ct < 4; ++ct)
+        *reinterpret_cast<double2*>(Qt + row * kRS + x.p * kL + 8 * ct + 2 * (x.lane & 3)) =
+            make_double2(acc[m0 + k][ct][0] + v[k][ct].x, acc[m0 + k][ct][1] + v[k][ct].y);
+    }
   }
 }
 
@@ -181,6 +197,56 @@ __device__ __forceinline__ void stage_trace(const Ctx& x, double* stg, const dou
     stg[e * TS + m * kP + x.p] = acc[ct][0];
     stg[(e + 1) * TS + m * kP + x.p] = acc[ct][1];
   }
+}
+
+// Flux of the Godunov state of one face-basis row (P:1341-1342 with reading R8):
+//   y = A+ t + A- z  for the own state t and the rotated neighbour state z (quantity order
+//   sxx syy szz sxy syz sxz u v w), rebuilt from the factored solver c (setup.h):
+//   tractions tau = sigma n; normal (p-wave) and tangential (s-wave) interface states
+//   v*_n = v_n- + Z+/S dv_n + dtau_n/S,  tau*_n = tau_n- + Z-/S dtau_n + Z-Z+/S dv_n (per wave
+//   type, S = Z- + Z+); flux  sigma = -lam v*_n I - mu (n v*^T + v* n^T),  v = -tau*/rho, all
+//   times -2|S_i|/det J.  Same linear map as T A_x(m-) G-+ T^-1 (setup.cpp), ~80 FMAs
+//   instead of 162.
+__device__ __forceinline__ void godunov_flux(const double* t, const double* z, const double (&c)[kFaceCoeffs],
+                                             double (&y)[kP]) {
+  const double nx = c[0], ny = c[1], nz = c[2];
+  const double t1x = fma(t[5], nz, fma(t[3], ny, t[0] * nx));
+  const double t1y = fma(t[4], nz, fma(t[1], ny, t[3] * nx));
+  const double t1z = fma(t[2], nz, fma(t[4], ny, t[5] * nx));
+  const double t2x = fma(z[5], nz, fma(z[3], ny, z[0] * nx));
+  const double t2y = fma(z[4], nz, fma(z[1], ny, z[3] * nx));
+  const double t2z = fma(z[2], nz, fma(z[4], ny, z[5] * nx));
+  const double dvx = z[6] - t[6], dvy = z[7] - t[7], dvz = z[8] - t[8];
+  const double dtx = t2x - t1x, dty = t2y - t1y, dtz = t2z - t1z;
+  const double vn1 = fma(t[8], nz, fma(t[7], ny, t[6] * nx));
+  const double dvn = fma(dvz, nz, fma(dvy, ny, dvx * nx));
+  const double tn1 = fma(t1z, nz, fma(t1y, ny, t1x * nx));
+  const double dtn = fma(dtz, nz, fma(dty, ny, dtx * nx));
+  // p wave: normal components
+  const double vns = fma(c[5], dtn, fma(1.0 - c[3], dvn, vn1));
+  const double tns = fma(c[4], dvn, fma(c[3], dtn, tn1));
+  // s wave: whole vectors, normal parts replaced below
+  const double bs = 1.0 - c[6];
+  const double vsx = fma(c[8], dtx, fma(bs, dvx, t[6]));
+  const double vsy = fma(c[8], dty, fma(bs, dvy, t[7]));
+  const double vsz = fma(c[8], dtz, fma(bs, dvz, t[8]));
+  const double tsx = fma(c[7], dvx, fma(c[6], dtx, t1x));
+  const double tsy = fma(c[7], dvy, fma(c[6], dty, t1y));
+  const double tsz = fma(c[7], dvz, fma(c[6], dtz, t1z));
+  const double cv = vns - fma(vsz, nz, fma(vsy, ny, vsx * nx));
+  const double ct = tns - fma(tsz, nz, fma(tsy, ny, tsx * nx));
+  const double vx = fma(cv, nx, vsx), vy = fma(cv, ny, vsy), vz = fma(cv, nz, vsz);
+  const double tx = fma(ct, nx, tsx), ty = fma(ct, ny, tsy), tz = fma(ct, nz, tsz);
+  const double L = c[9] * vns, M = c[10], M2 = 2.0 * c[10], R = c[11];
+  y[0] = -fma(M2 * nx, vx, L);
+  y[1] = -fma(M2 * ny, vy, L);
+  y[2] = -fma(M2 * nz, vz, L);
+  y[3] = -M * fma(nx, vy, ny * vx);
+  y[4] = -M * fma(ny, vz, nz * vy);
+  y[5] = -M * fma(nx, vz, nz * vx);
+  y[6] = -R * tx;
+  y[7] = -R * ty;
+  y[8] = -R * tz;
 }
 
 template <int N>
@@ -346,8 +412,8 @@ __global__ void __launch_bounds__(kP * kL, 1) dm_local(const __grid_constant__ S
 // Per (tile, face) item: one TMA bulk copy of the tile's own face block (buffer O) and one
 // per lane of the neighbour's face block (buffers N0/N1: the next face's copies are in
 // flight while this one computes); f^h rotates the neighbour column in place, thread
-// (e,p) mixes T with A+ and Z with A-, writing Y (rows [m][288]) and the warp lifts its
-// own columns of Y with DMMAs into Q.
+// (e, m) builds the Godunov flux of row m from T and Z (godunov_flux), writing Y (rows
+// [m][288]), and the warp lifts its own columns of Y with DMMAs into Q.
 template <int N>
 __global__ void __launch_bounds__(kP * kL, 1) dm_flux(const __grid_constant__ StepParams<double> prm) {
   using G = DG<N>;
@@ -396,6 +462,13 @@ __global__ void __launch_bounds__(kP * kL, 1) dm_flux(const __grid_constant__ St
       if (threadIdx.x < kL) {
         if (F < 3) issue_nb(tile, F + 1, b ^ 1);
         else if (more) issue_nb(tile + gridDim.x, 0, b ^ 1);
+      } else if (threadIdx.x == kL) {  // next item's flux coefficients (and next tile's Q) -> L2
+        const int64_t nt = F < 3 ? tile : tile + gridDim.x;
+        const int nF = F < 3 ? F + 1 : 0;
+        if (F < 3 || more) {
+          prefetch_l2(prm.aplus + (nt * 4 + nF) * kFaceCoeffs * kL, kFaceCoeffs * kL * sizeof(double));
+        }
+        if (F == 3 && more) prefetch_l2(prm.Q + nt * B * kRS, B * kRS * sizeof(double));
       }
       double* Z = NB + b * FACE + x.lane * TS;
       const int h = prm.jh[(tile * 4 + F) * kL + x.lane] >> 2;
@@ -412,26 +485,23 @@ __global__ void __launch_bounds__(kP * kL, 1) dm_flux(const __grid_constant__ St
         for (int n = 0; n < Bt; ++n) t[n] = Z[n * kP + x.p];
         G::rot(h, t, Z + x.p);
       }
-      double ap[kP], am[kP];
-      {
-        const int64_t fo = ((tile * 4 + F) * kP + x.p) * kP * kL + x.lane;
+      // flux solvers of this face, factored (setup.h kFaceCoeffs): the lane's element
+      double fc[kFaceCoeffs];
 #pragma unroll
-        for (int q = 0; q < kP; ++q) {
-          ap[q] = prm.aplus[fo + q * kL];
-          am[q] = prm.aminus[fo + q * kL];
-        }
-      }
+      for (int k = 0; k < kFaceCoeffs; ++k) fc[k] = prm.aplus[((tile * 4 + F) * kFaceCoeffs + k) * kL + x.lane];
       mbar_wait(&bar[0], ph_o);
       ph_o ^= 1;
       __syncthreads();  // rotated neighbour columns visible
       {
         const double* T = O + x.lane * TS;
 #pragma unroll
-        for (int m = 0; m < Bt; ++m) {
-          double s = 0.0;
+        for (int i = 0; i < (Bt + kP - 1) / kP; ++i) {  // rows m = p, p + 9, ... of element lane
+          const int m = x.p + kP * i;
+          if (m >= Bt) break;
+          double y[kP];
+          godunov_flux(T + m * kP, Z + m * kP, fc, y);
 #pragma unroll
-          for (int q = 0; q < kP; ++q) s = fma(T[m * kP + q], ap[q], fma(Z[m * kP + q], am[q], s));
-          Y[swz(m, x.p * kL + x.lane)] = s;
+          for (int q = 0; q < kP; ++q) Y[swz(m, q * kL + x.lane)] = y[q];
         }
       }
       __syncthreads();  // every read of O done; Y complete

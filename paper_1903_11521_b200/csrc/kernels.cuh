@@ -11,10 +11,12 @@ constexpr int kMaxN = 6;
 template <typename T>
 struct StepParams {
   T* Q;                  // [tile][k][p][32]  DOFs (updated in place)
-  T* traces;             // [elem][face][m][q] time-integrated face traces R^iT I (AoS)
+  T* traces;             // time-integrated face traces R^iT I: fp32 [tile][face][m][q][32],
+                         // fp64 [tile][face][lane][TS] (element-face blocks [m][q])
   const T* star;         // [tile][c][p][3][32]
-  const T* aplus;        // [tile][face][p][q][32]  (-2|S|/detJ folded in)
-  const T* aminus;       // [tile][face][p][q][32]
+  const T* aplus;        // fp32: [tile][face][p][q][32] (-2|S|/detJ folded in);
+                         // fp64: factored flux solvers [tile][face][kFaceCoeffs][32]
+  const T* aminus;       // fp32: [tile][face][p][q][32]; fp64: unused
   const int32_t* nb;     // [tile][face][32] neighbour element (local index incl. ghosts)
   const int8_t* jh;      // [tile][face][32] j | (h << 2)
   int64_t tile0;         // first tile handled by this launch

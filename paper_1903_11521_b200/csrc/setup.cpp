@@ -185,6 +185,7 @@ bool element_coeffs(int P, int64_t e0, int64_t n, const double* xyz, const doubl
   out->aplus.assign(static_cast<size_t>(n) * 4 * P * P, 0.0);
   out->aminus.assign(static_cast<size_t>(n) * 4 * P * P, 0.0);
   if (P == 27) out->src.assign(static_cast<size_t>(n) * P * P, 0.0);
+  if (P == 9) out->face.assign(static_cast<size_t>(n) * 4 * kFaceCoeffs, 0.0);
   const double* omega = P == 27 ? anelastic : nullptr;
   const double* Y = P == 27 ? anelastic + 3 : nullptr;
   bool ok = true;
@@ -266,6 +267,22 @@ bool element_coeffs(int P, int64_t e0, int64_t n, const double* xyz, const doubl
       const Mat mo = material_of(material + nbr.nb[e * 4 + i] * 3);
       const double Zpm = std::sqrt(m.rho * (m.lam + 2 * m.mu)), Zsm = std::sqrt(m.rho * m.mu);
       const double Zpp = std::sqrt(mo.rho * (mo.lam + 2 * mo.mu)), Zsp = std::sqrt(mo.rho * mo.mu);
+      if (P == 9) {
+        double* fc = &out->face[(t * 4 + i) * kFaceCoeffs];
+        fc[0] = nrm[0];
+        fc[1] = nrm[1];
+        fc[2] = nrm[2];
+        const double sp = Zpm + Zpp, ss = Zsm + Zsp;
+        fc[3] = Zpm / sp;
+        fc[4] = Zpm * Zpp / sp;
+        fc[5] = 1.0 / sp;
+        fc[6] = Zsm / ss;
+        fc[7] = Zsm * Zsp / ss;
+        fc[8] = 1.0 / ss;
+        fc[9] = scale * m.lam;
+        fc[10] = scale * m.mu;
+        fc[11] = scale / m.rho;
+      }
       // Ax(m-) = A[0]
       for (int side = 0; side < 2; ++side) {
         std::fill(G.begin(), G.end(), 0.0);

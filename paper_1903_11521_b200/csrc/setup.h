@@ -24,8 +24,15 @@ struct ElementCoeffs {
   //  star: [3][P][3] values of A*^c at the fixed 3-column pattern of row p (star_cols)
   //  aplus / aminus: [4][P][P] flux solvers with -2|S_i|/det J folded in (row-major p,q)
   //  src: [P][P] viscoelastic source E (P = 27 only)
-  std::vector<double> star, aplus, aminus, src;
+  //  face: [4][kFaceCoeffs] factored flux solver of face i (P = 9; see kFaceCoeffs)
+  std::vector<double> star, aplus, aminus, src, face;
 };
+
+// Factored form of the elastic flux solvers of one face (reading R8), all scaled by
+// s = -2|S_i|/det J:  n (3), then per wave type w in {p, s}: Z-/(Z-+Z+), Z-Z+/(Z-+Z+),
+// 1/(Z-+Z+), then s*lambda-, s*mu-, s/rho-.  A+ q- + A- q+ = the flux of the Godunov state
+// built from these (dm_flux).
+constexpr int kFaceCoeffs = 12;
 
 // Columns of the star-matrix pattern of row p (3 per row; unused slots repeat a column
 // with a zero coefficient).  Valid for P = 9 and P = 27.

@@ -207,9 +207,9 @@ def gen_order(N):
     b(f"  static __device__ __forceinline__ void volume(Ctx& x, double (&acc)[{QMT}][4][2]) {{")
     counts["vol"] = emit_xprod(b, tab, "vol", mats, tl, "SRC_I")
     b("  }")
-    b(f"  static __device__ __forceinline__ void add_volume(const Ctx& x, double* Qt, const double (&acc)[{QMT}][4][2]) {{")
-    for mt, og in enumerate(tl["out"]):
-        b(f"    add_q(x, Qt, acc[{mt}], {row_word64(og)});")
+    b(f"  static __device__ __forceinline__ void add_volume(const Ctx& x, double* Qt, double (&acc)[{QMT}][4][2]) {{")
+    b("    constexpr unsigned long long w[] = {" + ", ".join(row_word64(og) for og in tl["out"]) + "};")
+    b("    add_q(x, Qt, acc, w);")
     b("  }")
     # ---------------- traces T_i = R^iT I
     b(f"  // trace: T_F = R^FT I (rows < IROWS of I from shared memory, dt * Q from global memory);")
@@ -250,9 +250,9 @@ def gen_order(N):
                                      lambda k, w: f"double bf[4]; smem_b(x, Y, {w}, bf);")
         b("    }")
     b("  }")
-    b(f"  static __device__ __forceinline__ void add_lift(const Ctx& x, double* Qt, const double (&acc)[{LMT}][4][2]) {{")
-    for mt, og in enumerate(tl["out"]):
-        b(f"    add_q(x, Qt, acc[{mt}], {row_word64(og)});")
+    b(f"  static __device__ __forceinline__ void add_lift(const Ctx& x, double* Qt, double (&acc)[{LMT}][4][2]) {{")
+    b("    constexpr unsigned long long w[] = {" + ", ".join(row_word64(og) for og in tl["out"]) + "};")
+    b("    add_q(x, Qt, acc, w);")
     b("  }")
     # ---------------- neighbour orientation z = f^h t, uniform over lanes:
     # f^1 = S (diagonal +-1) and f^2 = S f^0 S, so t' = (h != 0 ? S t : t), u = f^0 t',
