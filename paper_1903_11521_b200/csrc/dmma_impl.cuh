@@ -186,6 +186,38 @@ __device__ __forceinline__ void add_q(const Ctx& x, double* Qt, double (&acc)[MT
   }
 }
 
+// Q rows of two m-tiles (words w0, w1; ~0 = absent) for the m-tile-group lift: load_q2
+// issues the loads, store_q2 writes Q + acc.
+__device__ __forceinline__ void load_q2(const Ctx& x, const double* Qt, unsigned long long w0, unsigned long long w1,
+                                        double2 (&q)[2][4]) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int row = mrow(x, k ? w1 : w0);
+#pragma unroll
+    for (int ct = 0; ct < 4; ++ct)
+      q[k][ct] = row == 0xff ? make_double2(0.0, 0.0)
+                             : *reinterpret_cast<const double2*>(Qt + row * kRS + x.p * kL + 8 * ct + 2 * (x.lane & 3));
+  }
+}
+__device__ __forceinline__ void copy_q2(const double2 (&a)[2][4], double2 (&b)[2][4]) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+#pragma unroll
+    for (int ct = 0; ct < 4; ++ct) b[k][ct] = a[k][ct];
+}
+__device__ __forceinline__ void store_q2(const Ctx& x, double* Qt, unsigned long long w0, unsigned long long w1,
+                                         const double (&acc)[2][4][2], const double2 (&q)[2][4]) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int row = mrow(x, k ? w1 : w0);
+    if (row == 0xff) continue;
+#pragma unroll
+    for (int ct = 0; ct < 4; ++ct)
+      *reinterpret_cast<double2*>(Qt + row * kRS + x.p * kL + 8 * ct + 2 * (x.lane & 3)) =
+          make_double2(q[k][ct].x + acc[k][ct][0], q[k][ct].y + acc[k][ct][1]);
+  }
+}
+
 // Trace C fragments of one m-tile -> staging block [lane][m][q] (stride TS per lane).
 template <int TS>
 __device__ __forceinline__ void stage_trace(const Ctx& x, double* stg, const double (&acc)[4][2], unsigned long long w) {
@@ -509,15 +541,14 @@ __global__ void __launch_bounds__(kP * kL, 1) dm_flux(const __grid_constant__ St
         if (F < 3) issue_own(tile, F + 1);
         else if (more) issue_own(tile + gridDim.x, 0);
       }
-      // lift and Q update per face: the accumulators live only here (168 registers per
-      // thread with 9 warps); the tile's Q stays in L2 across its four updates
-      double acc[G::LMT][4][2];
-      zero_acc(acc);
-      if (F == 0) G::template lift<0>(x, Y, acc);
-      else if (F == 1) G::template lift<1>(x, Y, acc);
-      else if (F == 2) G::template lift<2>(x, Y, acc);
-      else G::template lift<3>(x, Y, acc);
-      G::add_lift(x, prm.Q + tile * B * kRS, acc);
+      // lift and Q update per face, two m-tiles at a time (accumulators and Q rows live only
+      // there: 168 registers per thread with 9 warps); the tile's Q stays in L2 across its
+      // four updates
+      double* Qt = prm.Q + tile * B * kRS;
+      if (F == 0) G::template lift<0>(x, Y, Qt);
+      else if (F == 1) G::template lift<1>(x, Y, Qt);
+      else if (F == 2) G::template lift<2>(x, Y, Qt);
+      else G::template lift<3>(x, Y, Qt);
     }
   }
 }

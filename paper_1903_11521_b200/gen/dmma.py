@@ -238,21 +238,36 @@ def gen_order(N):
             b(f"      stage_trace<{TS}>(x, stg, acc[{mt}], {row_word64(og)});")
         b("    }")
     b("  }")
-    # ---------------- lift Q += R^i Y_i (shared output tiling over the four faces)
+    # ---------------- lift Q += R^i Y_i: m-tile-group major (two m-tiles at a time), the Q
+    # rows of the next group loaded while the current group's DMMAs run
     tl = til["lift"]
-    b(f"  // lift: acc += R^F Y_F (Y own columns in shared memory, rows [m][288])")
-    b(f"  template <int F> static __device__ __forceinline__ void lift(Ctx& x, const double* Y, double (&acc)[{LMT}][4][2]) {{")
+    outs = tl["out"]
+    groups = [list(range(g, min(g + 2, len(outs)))) for g in range(0, len(outs), 2)]
+    b(f"  // lift + Q update: Q += R^F Y_F (Y own columns in shared memory, rows [m][288])")
+    b(f"  template <int F> static __device__ __forceinline__ void lift(Ctx& x, const double* Y, double* Qt) {{")
     counts["lift"] = 0
     for i in range(4):
         b(f"    {'if' if i == 0 else 'else if'} constexpr (F == {i}) {{")
         Mi = lambda r, col, i=i: R[i][r][col]
-        counts["lift"] += emit_gprod(b, tab, Mi, tl["out"], tl["in"][i],
-                                     lambda k, w: f"double bf[4]; smem_b(x, Y, {w}, bf);")
+        ins = tl["in"][i]
+        b("      double2 qn[2][4];")
+        g0 = groups[0]
+        b(f"      load_q2(x, Qt, {row_word64(outs[g0[0]])}, {row_word64(outs[g0[1]]) if len(g0) > 1 else '~0ULL'}, qn);")
+        for gi, grp in enumerate(groups):
+            b("      {")
+            b("        double2 qc[2][4];")
+            b("        copy_q2(qn, qc);")
+            if gi + 1 < len(groups):
+                g1 = groups[gi + 1]
+                b(f"        load_q2(x, Qt, {row_word64(outs[g1[0]])}, {row_word64(outs[g1[1]]) if len(g1) > 1 else '~0ULL'}, qn);")
+            b("        double acc[2][4][2];")
+            b("        zero_acc(acc);")
+            sub = [outs[m] for m in grp]
+            counts["lift"] += emit_gprod(b, tab, Mi, sub, ins,
+                                         lambda k, w: f"double bf[4]; smem_b(x, Y, {w}, bf);")
+            b(f"        store_q2(x, Qt, {row_word64(outs[grp[0]])}, {row_word64(outs[grp[1]]) if len(grp) > 1 else '~0ULL'}, acc, qc);")
+            b("      }")
         b("    }")
-    b("  }")
-    b(f"  static __device__ __forceinline__ void add_lift(const Ctx& x, double* Qt, double (&acc)[{LMT}][4][2]) {{")
-    b("    constexpr unsigned long long w[] = {" + ", ".join(row_word64(og) for og in tl["out"]) + "};")
-    b("    add_q(x, Qt, acc, w);")
     b("  }")
     # ---------------- neighbour orientation z = f^h t, uniform over lanes:
     # f^1 = S (diagonal +-1) and f^2 = S f^0 S, so t' = (h != 0 ? S t : t), u = f^0 t',
