@@ -2,11 +2,13 @@
 //
 // Data of a 32-element tile live in shared memory as [row][col] with col = p*32 + e
 // (quantity-major), rows swizzled (col ^ 8*(row & 1)) so that the 4-row x 8-column DMMA
-// B-fragment loads take the minimum two wavefronts and per-thread column accesses stay
-// conflict-free.  Warp p owns the four 8-column tiles of quantity p: every B operand it
-// feeds to a DMMA is warp-private; only the per-element quantity mixing (star matrices
-// A*, flux solvers A+-) reads other warps' columns.  Global matrices are the DMMA A
-// operands: generated 8x4 tiles over freely grouped rows (gen/dmma.py, gen/tiling.py).
+// B-fragment loads take the minimum two wavefronts.  A CTA has 12 warps, three per SM
+// sub-partition (a multiple of 4 keeps the four tensor pipes equally loaded between
+// barriers): warp w owns the 8-column tiles (quantity 3g + k, elements 8ct..8ct+7),
+// k = 0..2, with g = w / 4, ct = w % 4 -- its "units".  Every B operand a warp feeds to a
+// DMMA is warp-private; only the per-element quantity mixing (star matrices A*, flux
+// solvers) reads other warps' columns.  Global matrices are the DMMA A operands:
+// generated 8x4 tiles over freely grouped rows (gen/dmma.py, gen/tiling.py).
 //
 // Face traces T_i = R^iT I live in HBM as [tile][face][lane][TS] with an element-face
 // block [m][q] of TS = even(9*Bt) doubles: the producer writes a face of a tile with one
@@ -21,33 +23,71 @@ namespace dm {
 constexpr int kP = 9;
 constexpr int kL = 32;
 constexpr int kRS = kP * kL;   // 288 columns per row
-constexpr int kXB = 40;        // padded row of the warp-private X buffer (2 wavefronts / B load)
+constexpr int kW = 12;         // warps per CTA
+constexpr int kT = kW * 32;    // threads per CTA
+constexpr int kU = 3;          // units (8-column tiles) per warp
+constexpr int kXW = 3 * kU * 4 * 8;  // warp-private X buffer: [c][k][row][8 elements]
+#ifndef YDG_XBUF
+#define YDG_XBUF 1
+#endif
+constexpr int kXBUF = YDG_XBUF;      // star-chunk buffers per warp (1: reuse after __syncwarp)
 
 enum Src { SRC_Q, SRC_S, SRC_I };
 
 __device__ __forceinline__ int swz(int row, int col) { return row * kRS + (col ^ ((row & 1) << 3)); }
 
 struct Ctx {
-  int lane, p;
+  int lane, w;
+  int col0;           // column of unit 0 of this warp's B fragments / C fragments: 3g*32 + 8ct
   int sh4, sh8;       // 8 * (lane & 3), 8 * (lane >> 2): byte of a k-set / m-tile row word
+  // star chunk role: lane -> (element xe = 8ct + (lane & 7), unit xk = lane >> 3; xk = 3 idle)
+  int xe, xk;
   double* S;          // [SROWS][288]  D^d, d >= 1
   double* I;          // [IROWS][288]  time integral rows < IROWS
-  double* xb;         // warp-private [3][4][kXB]
+  double* xb;         // warp-private [3][kU][4][8]
   const double* Qt;   // Q of this tile in global memory: [B][9][32]
   const double* frags;
-  double a[9];        // star matrices, row p: a[3c + j] = A*^c[p][q_j]
+  const double* fs;   // shared-memory A-fragment buffer (products staged there)
+  unsigned long long* fbar;  // its mbarrier
+  double a[9];        // star matrices, row p = 3g + xk: a[3c + j] = A*^c[p][q_j]
   int q0, q1, q2;     // star columns of row p
   double dt;
   const double* scal;  // kernel-parameter space: dt/(d+1) at [d], dt/(d+2) at [N + d]
   int N;
 };
 
+// Phase timing of the local kernel (build with YDG_NVFLAGS=-DYDG_PHASES): CTA 0, thread 0
+// prints clock64 deltas of a few tiles.
+#ifdef YDG_PHASES
+#define YDG_PHASE(k) \
+  do {               \
+    if (threadIdx.x == 0 && blockIdx.x == 0) ph_t[k] = clock64(); \
+  } while (0)
+__device__ long long ph_t[16];
+#else
+#define YDG_PHASE(k) \
+  do {               \
+  } while (0)
+#endif
+
 template <int N>
 struct DG;
 template <int N>
 __device__ const double* frag_table();
 
-__device__ __forceinline__ double afrag(const Ctx& x, int tid) { return __ldg(x.frags + tid * kL + x.lane); }
+// A fragments: read-only, reused by every warp and tile -> keep in L1 (evict_last); other
+// streaming loads use evict_first so they do not push the fragment table out.
+__device__ __forceinline__ double afrag(const Ctx& x, int tid) {
+  double v;
+  asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(x.frags + tid * kL + x.lane));
+  return v;
+}
+__device__ __forceinline__ double afrag_s(const Ctx& x, int i) { return x.fs[i * kL + x.lane]; }
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::evict_first.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
 
 __device__ __forceinline__ int krow(const Ctx& x, unsigned w) { return static_cast<int>((w >> x.sh4) & 0xffu); }
 __device__ __forceinline__ int mrow(const Ctx& x, unsigned long long w) {
@@ -59,18 +99,22 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
       : "+d"(c[0]), "+d"(c[1])
       : "d"(a), "d"(b));
 }
-__device__ __forceinline__ void dmma4(double (&acc)[4][2], double a, const double (&bf)[4]) {
+__device__ __forceinline__ void dmma3(double (&acc)[kU][2], double a, const double (&bf)[kU]) {
 #pragma unroll
-  for (int ct = 0; ct < 4; ++ct) dmma(acc[ct], a, bf[ct]);
+  for (int k = 0; k < kU; ++k) dmma(acc[k], a, bf[k]);
 }
 
 template <int MT>
-__device__ __forceinline__ void zero_acc(double (&acc)[MT][4][2]) {
+__device__ __forceinline__ void zero_acc(double (&acc)[MT][kU][2]) {
 #pragma unroll
   for (int m = 0; m < MT; ++m)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[m][c][0] = acc[m][c][1] = 0.0;
+    for (int c = 0; c < kU; ++c) acc[m][c][0] = acc[m][c][1] = 0.0;
 }
+// column of the B-fragment entry of unit k held by this lane (element 8ct + lane / 4)
+__device__ __forceinline__ int bcol(const Ctx& x, int k) { return x.col0 + k * kL + (x.lane >> 2); }
+// first of the two C-fragment columns of unit k held by this lane (elements 8ct + 2(lane & 3) + {0,1})
+__device__ __forceinline__ int ccol(const Ctx& x, int k) { return x.col0 + k * kL + 2 * (x.lane & 3); }
 
 template <Src SRC, int B>
 __device__ __forceinline__ double load_data(const Ctx& x, int row, int col) {
@@ -81,60 +125,81 @@ __device__ __forceinline__ double load_data(const Ctx& x, int row, int col) {
   else return x.I[swz(row, col)];
 }
 
-// X^c = D A*^cT for the 4 rows r0..r3 (compile-time, uniform over the warp) of the
-// thread's own column (element lane, quantity p), staged in the warp-private buffer
-// [c][r][kXB]; xb_b then reads one c's B fragments for the warp's four column tiles.
-// The caller ends the k-set with __syncwarp().
+// X^c = D A*^cT for the 4 rows r0..r3 (compile-time, uniform over the warp): lane
+// (xe, xk) computes its element's column of quantity 3g + xk into the warp-private buffer
+// buf ([c][k][r][8]); after a __syncwarp() xb_b reads one c's B fragments for the warp's
+// three units.
 template <Src SRC, int B>
-__device__ __forceinline__ void xchunk(Ctx& x, int r0, int r1, int r2, int r3) {
-  const int rr[4] = {r0, r1, r2, r3};
+__device__ __forceinline__ void xcalc(Ctx& x, int buf, int r0, int r1, int r2, int r3) {
+  if (kXBUF == 1) __syncwarp();  // every lane has read the previous chunk's B fragments
+  if (x.xk < kU) {
+    double* xb = x.xb + (buf % kXBUF) * kXW;
+    const int rr[4] = {r0, r1, r2, r3};
+    // all 12 loads first (no store in between), then 12 independent 3-term dot products:
+    // three dependent FP64 waves instead of a chain per row (the FP64 pipe is shared with
+    // the queued DMMAs, so every dependent FP64 step waits behind them)
+    double d[4][3];
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const double d0 = load_data<SRC, B>(x, rr[r], x.q0 * kL + x.lane);
-    const double d1 = load_data<SRC, B>(x, rr[r], x.q1 * kL + x.lane);
-    const double d2 = load_data<SRC, B>(x, rr[r], x.q2 * kL + x.lane);
+    for (int r = 0; r < 4; ++r) {
+      d[r][0] = load_data<SRC, B>(x, rr[r], x.q0 * kL + x.xe);
+      d[r][1] = load_data<SRC, B>(x, rr[r], x.q1 * kL + x.xe);
+      d[r][2] = load_data<SRC, B>(x, rr[r], x.q2 * kL + x.xe);
+    }
+    double v[4][3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
-      x.xb[(c * 4 + r) * kXB + x.lane] = fma(x.a[3 * c + 2], d2, fma(x.a[3 * c + 1], d1, x.a[3 * c] * d0));
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[r][c] = x.a[3 * c] * d[r][0];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[r][c] = fma(x.a[3 * c + 1], d[r][1], v[r][c]);
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[r][c] = fma(x.a[3 * c + 2], d[r][2], v[r][c]);
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) xb[((c * kU + x.xk) * 4 + r) * 8 + (x.lane & 7)] = v[r][c];
   }
-  __syncwarp();
 }
-__device__ __forceinline__ void xb_b(const Ctx& x, int c, double (&bf)[4]) {
+__device__ __forceinline__ void xb_b(const Ctx& x, int buf, int c, double (&bf)[kU]) {
+  const double* xb = x.xb + (buf % kXBUF) * kXW;
 #pragma unroll
-  for (int ct = 0; ct < 4; ++ct) bf[ct] = x.xb[(c * 4 + (x.lane & 3)) * kXB + 8 * ct + (x.lane >> 2)];
+  for (int k = 0; k < kU; ++k) bf[k] = xb[((c * kU + k) * 4 + (x.lane & 3)) * 8 + (x.lane >> 2)];
 }
 
 // Gathered B fragments of the own quantity column: lane row = byte (lane & 3) of w.
-__device__ __forceinline__ void ismem_b(const Ctx& x, unsigned w, double (&bf)[4]) {
+__device__ __forceinline__ void ismem_b(const Ctx& x, unsigned w, double (&bf)[kU]) {
   const int row = krow(x, w);
 #pragma unroll
-  for (int ct = 0; ct < 4; ++ct) bf[ct] = x.I[swz(row, x.p * kL + 8 * ct + (x.lane >> 2))];
+  for (int k = 0; k < kU; ++k) bf[k] = x.I[swz(row, bcol(x, k))];
 }
 // rows >= IROWS of the time integral are dt * Q (only D^0 contributes), from global memory
 template <int B>
-__device__ __forceinline__ void gq_b(const Ctx& x, unsigned w, double (&bf)[4]) {
+__device__ __forceinline__ void gq_b(const Ctx& x, unsigned w, double (&bf)[kU]) {
   const int row = krow(x, w);
 #pragma unroll
-  for (int ct = 0; ct < 4; ++ct) bf[ct] = x.dt * x.Qt[row * kRS + x.p * kL + 8 * ct + (x.lane >> 2)];
+  for (int k = 0; k < kU; ++k) bf[k] = x.dt * ld_stream(x.Qt + row * kRS + bcol(x, k));
 }
-__device__ __forceinline__ void smem_b(const Ctx& x, const double* Y, unsigned w, double (&bf)[4]) {
+__device__ __forceinline__ void smem_b(const Ctx& x, const double* Y, unsigned w, double (&bf)[kU]) {
   const int row = krow(x, w);
 #pragma unroll
-  for (int ct = 0; ct < 4; ++ct) bf[ct] = Y[swz(row, x.p * kL + 8 * ct + (x.lane >> 2))];
+  for (int k = 0; k < kU; ++k) bf[k] = Y[swz(row, bcol(x, k))];
 }
 
 // Write D^{d+1} = dt/(d+1) acc of one m-tile (rows from the word w) into S and accumulate
 // the time integral; at d = 0 the integral starts from dt * Q.
 template <int FIRST, int B>
-__device__ __forceinline__ void ck_wb(Ctx& x, const double (&acc)[4][2], int d, unsigned long long w) {
+__device__ __forceinline__ void ck_wb(Ctx& x, const double (&acc)[kU][2], int d, unsigned long long w) {
   const int row = mrow(x, w);
   if (row == 0xff) return;
   const double sc = x.scal[d], ic = x.scal[x.N + d];
 #pragma unroll
-  for (int ct = 0; ct < 4; ++ct) {
-    const int col = x.p * kL + 8 * ct + 2 * (x.lane & 3);
-    const int s = swz(row, col);
-    const double v0 = sc * acc[ct][0], v1 = sc * acc[ct][1];
+  for (int k = 0; k < kU; ++k) {
+    const int s = swz(row, ccol(x, k));
+    const double v0 = sc * acc[k][0], v1 = sc * acc[k][1];
     *reinterpret_cast<double2*>(x.S + s) = make_double2(v0, v1);
     double2 i2 = *reinterpret_cast<const double2*>(x.I + s);
     if (FIRST) {
@@ -146,12 +211,11 @@ __device__ __forceinline__ void ck_wb(Ctx& x, const double (&acc)[4][2], int d, 
     *reinterpret_cast<double2*>(x.I + s) = i2;
   }
 }
-// Rows [LO, HI) of the time-integral region receive no derivative: I = dt * Q (own column).
+// Rows [LO, HI) of the time-integral region receive no derivative: I = dt * Q.
 template <int LO, int HI>
 __device__ __forceinline__ void scale_irows(Ctx& x) {
-#pragma unroll
-  for (int r = LO; r < HI; ++r) {
-    double* v = x.I + swz(r, x.p * kL + x.lane);
+  for (int i = threadIdx.x; i < (HI - LO) * kRS; i += kT) {
+    double* v = x.I + (LO + i / kRS) * kRS + i % kRS;
     *v = x.dt * *v;
   }
 }
@@ -160,28 +224,28 @@ __device__ __forceinline__ void scale_irows(Ctx& x) {
 // Q loads are all issued before its stores (one L2/HBM latency per batch, bounded register
 // use), values are added into the accumulators, then stored (16-byte, two elements).
 template <int MT>
-__device__ __forceinline__ void add_q(const Ctx& x, double* Qt, double (&acc)[MT][4][2],
+__device__ __forceinline__ void add_q(const Ctx& x, double* Qt, double (&acc)[MT][kU][2],
                                       const unsigned long long (&w)[MT]) {
 #pragma unroll
   for (int m0 = 0; m0 < MT; m0 += 2) {
-    double2 v[2][4];
+    double2 v[2][kU];
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int row = m0 + k < MT ? mrow(x, w[m0 + k < MT ? m0 + k : 0]) : 0xff;
+    for (int k2 = 0; k2 < 2; ++k2) {
+      const int row = m0 + k2 < MT ? mrow(x, w[m0 + k2 < MT ? m0 + k2 : 0]) : 0xff;
 #pragma unroll
-      for (int ct = 0; ct < 4; ++ct)
-        v[k][ct] = row == 0xff ? make_double2(0.0, 0.0)
-                               : *reinterpret_cast<const double2*>(Qt + row * kRS + x.p * kL + 8 * ct + 2 * (x.lane & 3));
+      for (int k = 0; k < kU; ++k)
+        v[k2][k] = row == 0xff ? make_double2(0.0, 0.0)
+                               : *reinterpret_cast<const double2*>(Qt + row * kRS + ccol(x, k));
     }
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      if (m0 + k >= MT) continue;
-      const int row = mrow(x, w[m0 + k]);
+    for (int k2 = 0; k2 < 2; ++k2) {
+      if (m0 + k2 >= MT) continue;
+      const int row = mrow(x, w[m0 + k2]);
       if (row == 0xff) continue;
 #pragma unroll
-      for (int ct = 0; ct < 4; ++ct)
-        *reinterpret_cast<double2*>(Qt + row * kRS + x.p * kL + 8 * ct + 2 * (x.lane & 3)) =
-            make_double2(acc[m0 + k][ct][0] + v[k][ct].x, acc[m0 + k][ct][1] + v[k][ct].y);
+      for (int k = 0; k < kU; ++k)
+        *reinterpret_cast<double2*>(Qt + row * kRS + ccol(x, k)) =
+            make_double2(acc[m0 + k2][k][0] + v[k2][k].x, acc[m0 + k2][k][1] + v[k2][k].y);
     }
   }
 }
@@ -189,45 +253,44 @@ __device__ __forceinline__ void add_q(const Ctx& x, double* Qt, double (&acc)[MT
 // Q rows of two m-tiles (words w0, w1; ~0 = absent) for the m-tile-group lift: load_q2
 // issues the loads, store_q2 writes Q + acc.
 __device__ __forceinline__ void load_q2(const Ctx& x, const double* Qt, unsigned long long w0, unsigned long long w1,
-                                        double2 (&q)[2][4]) {
+                                        double2 (&q)[2][kU]) {
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int row = mrow(x, k ? w1 : w0);
+  for (int k2 = 0; k2 < 2; ++k2) {
+    const int row = mrow(x, k2 ? w1 : w0);
 #pragma unroll
-    for (int ct = 0; ct < 4; ++ct)
-      q[k][ct] = row == 0xff ? make_double2(0.0, 0.0)
-                             : *reinterpret_cast<const double2*>(Qt + row * kRS + x.p * kL + 8 * ct + 2 * (x.lane & 3));
+    for (int k = 0; k < kU; ++k)
+      q[k2][k] = row == 0xff ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(Qt + row * kRS + ccol(x, k));
   }
 }
-__device__ __forceinline__ void copy_q2(const double2 (&a)[2][4], double2 (&b)[2][4]) {
+__device__ __forceinline__ void copy_q2(const double2 (&a)[2][kU], double2 (&b)[2][kU]) {
 #pragma unroll
-  for (int k = 0; k < 2; ++k)
+  for (int k2 = 0; k2 < 2; ++k2)
 #pragma unroll
-    for (int ct = 0; ct < 4; ++ct) b[k][ct] = a[k][ct];
+    for (int k = 0; k < kU; ++k) b[k2][k] = a[k2][k];
 }
 __device__ __forceinline__ void store_q2(const Ctx& x, double* Qt, unsigned long long w0, unsigned long long w1,
-                                         const double (&acc)[2][4][2], const double2 (&q)[2][4]) {
+                                         const double (&acc)[2][kU][2], const double2 (&q)[2][kU]) {
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int row = mrow(x, k ? w1 : w0);
+  for (int k2 = 0; k2 < 2; ++k2) {
+    const int row = mrow(x, k2 ? w1 : w0);
     if (row == 0xff) continue;
 #pragma unroll
-    for (int ct = 0; ct < 4; ++ct)
-      *reinterpret_cast<double2*>(Qt + row * kRS + x.p * kL + 8 * ct + 2 * (x.lane & 3)) =
-          make_double2(q[k][ct].x + acc[k][ct][0], q[k][ct].y + acc[k][ct][1]);
+    for (int k = 0; k < kU; ++k)
+      *reinterpret_cast<double2*>(Qt + row * kRS + ccol(x, k)) =
+          make_double2(q[k2][k].x + acc[k2][k][0], q[k2][k].y + acc[k2][k][1]);
   }
 }
 
 // Trace C fragments of one m-tile -> staging block [lane][m][q] (stride TS per lane).
 template <int TS>
-__device__ __forceinline__ void stage_trace(const Ctx& x, double* stg, const double (&acc)[4][2], unsigned long long w) {
+__device__ __forceinline__ void stage_trace(const Ctx& x, double* stg, const double (&acc)[kU][2], unsigned long long w) {
   const int m = mrow(x, w);
   if (m == 0xff) return;
+  const int e = (x.col0 & 31) + 2 * (x.lane & 3), p0 = x.col0 >> 5;
 #pragma unroll
-  for (int ct = 0; ct < 4; ++ct) {
-    const int e = 8 * ct + 2 * (x.lane & 3);
-    stg[e * TS + m * kP + x.p] = acc[ct][0];
-    stg[(e + 1) * TS + m * kP + x.p] = acc[ct][1];
+  for (int k = 0; k < kU; ++k) {
+    stg[e * TS + m * kP + p0 + k] = acc[k][0];
+    stg[(e + 1) * TS + m * kP + p0 + k] = acc[k][1];
   }
 }
 
@@ -284,15 +347,19 @@ __device__ __forceinline__ void godunov_flux(const double* t, const double* z, c
 template <int N>
 struct Layout {
   using G = DG<N>;
-  static constexpr int XB = 9 * 3 * 4 * kXB;  // doubles
+  static constexpr int XB = kXBUF * kW * kXW;  // doubles (star-chunk buffers)
   static constexpr int FACE = kL * G::TS;      // doubles of one face of a tile
   // local kernel: [I][S][xb]; Q^n of the tile is staged over I and S for the first CK
   // step; the two trace staging blocks reuse S and xb
   static constexpr int ROWS = (G::IROWS + G::SROWS > G::B ? G::IROWS + G::SROWS : G::B);
-  static constexpr int LOCAL = (ROWS * kRS + XB > G::IROWS * kRS + 2 * FACE ? ROWS * kRS + XB
-                                                                            : G::IROWS * kRS + 2 * FACE);
-  // flux kernel: own face block, two neighbour face blocks, Y rows, three mbarriers
-  static constexpr int FLUX = 3 * FACE + G::Bt * kRS + 3;
+  // A-fragment buffer (CK step 0, then the volume term) after I, S, xb and the staging
+  static constexpr int FOFF = (ROWS * kRS + XB > G::IROWS * kRS + 2 * FACE ? ROWS * kRS + XB
+                                                                           : G::IROWS * kRS + 2 * FACE);
+  static constexpr int FSMAX = G::CK0_NF > G::VOL_NF ? G::CK0_NF : G::VOL_NF;
+  static constexpr int LOCAL = FOFF + FSMAX * kL + 2;  // + mbarrier
+  // flux kernel: own face block, two neighbour face blocks, Y rows, lift fragments, four
+  // mbarriers
+  static constexpr int FLUX = 3 * FACE + G::Bt * kRS + G::LIFT_NF * kL + 4;
 };
 
 // ---- asynchronous copy helpers (TMA bulk copies + mbarrier, Ampere-style cp.async)
@@ -345,15 +412,31 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
 
 __device__ __forceinline__ void init_ctx(Ctx& x) {
   x.lane = threadIdx.x & 31;
-  x.p = threadIdx.x >> 5;
+  x.w = threadIdx.x >> 5;
+  x.col0 = 3 * (x.w >> 2) * kL + 8 * (x.w & 3);
   x.sh4 = 8 * (x.lane & 3);
   x.sh8 = 8 * (x.lane >> 2);
+  x.xe = 8 * (x.w & 3) + (x.lane & 7);
+  x.xk = x.lane >> 3;
+}
+
+// Stage NF A fragments starting at table index F0 into the shared buffer (one thread).
+template <int N>
+__device__ __forceinline__ void stage_frags(const Ctx& x, int F0, int NF) {
+  mbar_expect_tx(x.fbar, NF * kL * sizeof(double));
+  bulk_g2s(const_cast<double*>(x.fs), frag_table<N>() + F0 * kL, NF * kL * sizeof(double), x.fbar);
+}
+// Called by DG<N>::ck after CK step 0 (which ends with a barrier): the fragment buffer
+// now receives the volume term's fragments.
+template <int N>
+__device__ __forceinline__ void after_ck0(Ctx& x) {
+  if (threadIdx.x == 0) stage_frags<N>(x, DG<N>::VOL_F0, DG<N>::VOL_NF);
 }
 
 // CK + time integral, face traces R^iT I (stored for the flux kernel) and
 // the volume term for 32-element tiles.
 template <int N>
-__global__ void __launch_bounds__(kP * kL, 1) dm_local(const __grid_constant__ StepParams<double> prm) {
+__global__ void __launch_bounds__(kT, 1) dm_local(const __grid_constant__ StepParams<double> prm) {
   using G = DG<N>;
   using Lay = Layout<N>;
   constexpr int B = G::B;
@@ -362,21 +445,30 @@ __global__ void __launch_bounds__(kP * kL, 1) dm_local(const __grid_constant__ S
   init_ctx(x);
   x.I = smem;
   x.S = smem + G::IROWS * kRS;
-  x.xb = smem + Lay::ROWS * kRS + x.p * (3 * 4 * kXB);
+  x.xb = smem + Lay::ROWS * kRS + x.w * kXBUF * kXW;
   x.frags = frag_table<N>();
+  x.fs = smem + Lay::FOFF;
+  x.fbar = reinterpret_cast<unsigned long long*>(smem + Lay::FOFF + Lay::FSMAX * kL);
+  if (threadIdx.x == 0) {
+    mbar_init(x.fbar, 1);
+    if (blockIdx.x < prm.ntiles) stage_frags<N>(x, G::CK0_F0, G::CK0_NF);
+  }
+  __syncthreads();
   x.dt = prm.dt;
   x.scal = prm.scal;
   x.N = N;
   double* stg0 = x.S;              // trace staging blocks (S and xb are dead after CK)
   double* stg1 = x.S + Lay::FACE;
-  // 3-column pattern of star-matrix row p (setup.cpp star_cols), packed 5 bits per column
+  // 3-column pattern of star-matrix row p = 3g + xk of the star-chunk role (setup.cpp
+  // star_cols), packed 5 bits per column
+  const int xp = 3 * (x.w >> 2) + (x.xk < kU ? x.xk : 0);
   {
     constexpr unsigned long long packed[9] = {6 | 7 << 5 | 8 << 10, 6 | 7 << 5 | 8 << 10, 6 | 7 << 5 | 8 << 10,
                                               6 | 7 << 5 | 7 << 10, 7 | 8 << 5 | 8 << 10, 6 | 8 << 5 | 8 << 10,
                                               0 | 3 << 5 | 5 << 10, 3 | 1 << 5 | 4 << 10, 5 | 4 << 5 | 2 << 10};
     unsigned long long w = 0;
 #pragma unroll
-    for (int i = 0; i < 9; ++i) w = (x.p == i) ? packed[i] : w;
+    for (int i = 0; i < 9; ++i) w = (xp == i) ? packed[i] : w;
     x.q0 = static_cast<int>(w & 31);
     x.q1 = static_cast<int>((w >> 5) & 31);
     x.q2 = static_cast<int>((w >> 10) & 31);
@@ -384,6 +476,7 @@ __global__ void __launch_bounds__(kP * kL, 1) dm_local(const __grid_constant__ S
   for (int64_t it = blockIdx.x; it < prm.ntiles; it += gridDim.x) {
     const int64_t tile = prm.tile0 + it;
     double* Qt = prm.Q + tile * B * kRS;
+    YDG_PHASE(0);
     if (threadIdx.x == 0 && it + gridDim.x < prm.ntiles) {  // next tile of this CTA -> L2
       const int64_t nt = tile + gridDim.x;
       prefetch_l2(prm.Q + nt * B * kRS, B * kRS * sizeof(double));
@@ -400,13 +493,15 @@ __global__ void __launch_bounds__(kP * kL, 1) dm_local(const __grid_constant__ S
                      : "memory");
       }
     }
-    const double* st = prm.star + (tile * 3 * kP) * 3 * kL + x.lane;
+    const double* st = prm.star + (tile * 3 * kP) * 3 * kL + x.xe;
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
-      for (int j = 0; j < 3; ++j) x.a[3 * c + j] = st[((c * kP + x.p) * 3 + j) * kL];
+      for (int j = 0; j < 3; ++j) x.a[3 * c + j] = ld_stream(st + ((c * kP + xp) * 3 + j) * kL);
     cp_async_wait_all();
+    mbar_wait(x.fbar, 0);  // CK step 0 fragments (first of the buffer's two loads per tile)
     __syncthreads();
+    YDG_PHASE(1);
     G::ck(x);  // ends with a barrier: the time integral is complete
     // traces T_F = R^FT I of the four faces -> staging -> one TMA bulk store per face;
     // they read Q^n (rows >= IROWS of I from global memory), so they precede the update
@@ -426,15 +521,29 @@ __global__ void __launch_bounds__(kP * kL, 1) dm_local(const __grid_constant__ S
       __syncthreads();
       if (threadIdx.x == 0) bulk_s2g(gtr + F * Lay::FACE, stg, Lay::FACE * sizeof(double));
     }
+    YDG_PHASE(8);
     if (threadIdx.x == 0) bulk_wait_read<0>();
     __syncthreads();  // the staging blocks overlap the X buffers of the volume term
+    YDG_PHASE(9);
     {
-      double acc[G::QMT][4][2];
+      double acc[G::QMT][kU][2];
       zero_acc(acc);
+      mbar_wait(x.fbar, 1);  // volume fragments (staged after CK step 0)
       G::volume(x, acc);
+      YDG_PHASE(10);
       G::add_volume(x, Qt, acc);
     }
     __syncthreads();  // before the next tile overwrites the shared regions
+    if (threadIdx.x == 0 && it + gridDim.x < prm.ntiles) stage_frags<N>(x, G::CK0_F0, G::CK0_NF);
+    YDG_PHASE(11);
+#ifdef YDG_PHASES
+    if (threadIdx.x == 0 && blockIdx.x == 0 && it >= 2 * gridDim.x && it < 6 * gridDim.x) {
+      printf("PH tile %lld: stage %lld ck %lld %lld %lld %lld %lld %lld traces %lld wait %lld vol %lld addq %lld total %lld\n",
+             (long long)it, ph_t[1] - ph_t[0], ph_t[2] - ph_t[1], ph_t[3] - ph_t[2], ph_t[4] - ph_t[3],
+             ph_t[5] - ph_t[4], ph_t[6] - ph_t[5], ph_t[7] - ph_t[6], ph_t[8] - ph_t[7], ph_t[9] - ph_t[8],
+             ph_t[10] - ph_t[9], ph_t[11] - ph_t[10], ph_t[11] - ph_t[0]);
+    }
+#endif
   }
   if (threadIdx.x == 0) bulk_wait_all();
 }
@@ -447,7 +556,7 @@ __global__ void __launch_bounds__(kP * kL, 1) dm_local(const __grid_constant__ S
 // (e, m) builds the Godunov flux of row m from T and Z (godunov_flux), writing Y (rows
 // [m][288]), and the warp lifts its own columns of Y with DMMAs into Q.
 template <int N>
-__global__ void __launch_bounds__(kP * kL, 1) dm_flux(const __grid_constant__ StepParams<double> prm) {
+__global__ void __launch_bounds__(kT, 1) dm_flux(const __grid_constant__ StepParams<double> prm) {
   using G = DG<N>;
   using Lay = Layout<N>;
   constexpr int B = G::B, Bt = G::Bt, TS = G::TS, FACE = Lay::FACE;
@@ -455,15 +564,20 @@ __global__ void __launch_bounds__(kP * kL, 1) dm_flux(const __grid_constant__ St
   double* O = smem;                    // own face block [lane][TS]
   double* NB = smem + FACE;            // [2][lane][TS] neighbour face blocks
   double* Y = smem + 3 * FACE;         // [Bt][288] mixed face values
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(Y + Bt * kRS);  // own, nb0, nb1
+  double* FS = Y + Bt * kRS;           // the lift's A fragments (whole kernel)
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(FS + G::LIFT_NF * kL);  // own, nb0, nb1, fs
   Ctx x;
   init_ctx(x);
   x.frags = frag_table<N>();
+  x.fs = FS;
+  x.fbar = &bar[3];
   if (blockIdx.x >= prm.ntiles) return;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     mbar_init(&bar[2], 1);
+    mbar_init(&bar[3], 1);
+    stage_frags<N>(x, G::LIFT_F0, G::LIFT_NF);
   }
   __syncthreads();
   auto issue_own = [&](int64_t tile, int F) {  // one thread
@@ -484,6 +598,7 @@ __global__ void __launch_bounds__(kP * kL, 1) dm_flux(const __grid_constant__ St
     issue_nb(prm.tile0 + blockIdx.x, 0, 0);
   }
   unsigned ph_o = 0, ph_n0 = 0, ph_n1 = 0;
+  mbar_wait(x.fbar, 0);
   for (int64_t it = blockIdx.x; it < prm.ntiles; it += gridDim.x) {
     const int64_t tile = prm.tile0 + it;
     const bool more = it + gridDim.x < prm.ntiles;
@@ -511,11 +626,11 @@ __global__ void __launch_bounds__(kP * kL, 1) dm_flux(const __grid_constant__ St
         mbar_wait(&bar[2], ph_n1);
         ph_n1 ^= 1;
       }
-      {  // z = f^h t on the own column of the lane's neighbour block
+      if (x.w < kP) {  // z = f^h t on column p = w of the lane's neighbour block
         double t[Bt];
 #pragma unroll
-        for (int n = 0; n < Bt; ++n) t[n] = Z[n * kP + x.p];
-        G::rot(h, t, Z + x.p);
+        for (int n = 0; n < Bt; ++n) t[n] = Z[n * kP + x.w];
+        G::rot(h, t, Z + x.w);
       }
       // flux solvers of this face, factored (setup.h kFaceCoeffs): the lane's element
       double fc[kFaceCoeffs];
@@ -527,8 +642,8 @@ __global__ void __launch_bounds__(kP * kL, 1) dm_flux(const __grid_constant__ St
       {
         const double* T = O + x.lane * TS;
 #pragma unroll
-        for (int i = 0; i < (Bt + kP - 1) / kP; ++i) {  // rows m = p, p + 9, ... of element lane
-          const int m = x.p + kP * i;
+        for (int i = 0; i < (Bt + kW - 1) / kW; ++i) {  // rows m = w, w + 12, ... of element lane
+          const int m = x.w + kW * i;
           if (m >= Bt) break;
           double y[kP];
           godunov_flux(T + m * kP, Z + m * kP, fc, y);

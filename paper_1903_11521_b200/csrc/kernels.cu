@@ -95,6 +95,8 @@ const void* pick_neigh(int N, int eb) {
   }
   return nullptr;
 }
+// fp64 tensor-core kernels: 12 warps (dmma_impl.cuh kW); fp32 sparse kernels: 9 warps
+int block_threads(int elem_bytes) { return elem_bytes == 8 ? 12 * kLanes : kP * kLanes; }
 int nB(int N) { return (N + 1) * (N + 2) * (N + 3) / 6; }
 int nBt(int N) { return (N + 1) * (N + 2) / 2; }
 
@@ -144,14 +146,14 @@ cudaError_t launch_local(int N, const StepParams<T>& p, int grid, cudaStream_t s
   const void* f = pick_local(N, sizeof(T));
   if (!f) return cudaErrorInvalidValue;
   void* args[] = {const_cast<StepParams<T>*>(&p)};
-  return cudaLaunchKernel(f, dim3(grid), dim3(kP * kLanes), args, local_smem_bytes(N, sizeof(T)), s);
+  return cudaLaunchKernel(f, dim3(grid), dim3(block_threads(sizeof(T))), args, local_smem_bytes(N, sizeof(T)), s);
 }
 template <typename T>
 cudaError_t launch_neigh(int N, const StepParams<T>& p, int grid, cudaStream_t s) {
   const void* f = pick_neigh(N, sizeof(T));
   if (!f) return cudaErrorInvalidValue;
   void* args[] = {const_cast<StepParams<T>*>(&p)};
-  return cudaLaunchKernel(f, dim3(grid), dim3(kP * kLanes), args, neigh_smem_bytes(N, sizeof(T)), s);
+  return cudaLaunchKernel(f, dim3(grid), dim3(block_threads(sizeof(T))), args, neigh_smem_bytes(N, sizeof(T)), s);
 }
 template <typename T>
 cudaError_t launch_to_tiled(int P, int B, const T* canon, T* tiled, int64_t first, int64_t count,

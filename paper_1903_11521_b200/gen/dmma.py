@@ -17,8 +17,8 @@ built from the 4 rows named at compile time) or by a per-lane gathered shared-me
 (trace, lift: lane row = byte (lane & 3) of a 32-bit immediate); accumulator rows are
 scattered on write-back (row = byte (lane >> 2) of a 64-bit immediate, 0xff = padding).
 
-Each warp owns the four 8-column data tiles of one quantity (warp = quantity column p,
-32 elements), so every B operand it feeds to a DMMA is warp-private.  A fragments are
+Each of the 12 warps owns three 8-column data tiles (quantities 3g..3g+2, elements
+8ct..8ct+7), so every B operand it feeds to a DMMA is warp-private.  A fragments are
 stored lane-ordered (lane i holds A[i/4][i%4]) in a device table, one coalesced 256-byte
 load per tile, issued one k-set ahead of use.
 
@@ -89,49 +89,57 @@ class Emit:
         self.lines.append(s)
 
 
-def emit_xprod(b, tab, name, mats, til, src, acc="acc"):
-    """CK / volume style product: per k-set the warp-private star chunk X^c of the 4 rows
-    (uniform across lanes), then per c the DMMAs of that c's nonzero tiles.  A fragments of
-    the next k-set are loaded before the current k-set's work."""
-    outs = til["out"]
-    ins = til["in"][0]
+def afrag_expr(tid, fbase):
+    """A-fragment load: from the shared-memory fragment buffer (fbase = first table index
+    staged there) or from the global table (L1-cached)."""
+    return f"afrag(x, {tid})" if fbase is None else f"afrag_s(x, {tid - fbase})"
+
+
+def plan_xprod(tab, mats, til):
     plan = []  # per k-set: list of (c, mt, tid)
-    for ks in ins:
+    for ks in til["in"][0]:
         cols = pad_rows(ks, 4)
         tiles = []
         for c, M in enumerate(mats):
-            for mt, og in enumerate(outs):
+            for mt, og in enumerate(til["out"]):
                 tid = tab.add(M, pad_rows(og, 8), cols)
                 if tid is not None:
                     tiles.append((c, mt, tid))
         plan.append(tiles)
-    b(f"    // {name}: {sum(len(t) for t in plan)} tiles, {len(ins)} k-sets, {len(outs)} m-tiles")
-    nv = 0
-    names = []
-    for i, tiles in enumerate(plan):
-        nm = [f"a{i}_{j}" for j in range(len(tiles))]
-        names.append(nm)
-    if plan and plan[0]:
-        b("    const double " + ", ".join(f"{n} = afrag(x, {t[2]})" for n, t in zip(names[0], plan[0])) + ";")
-    for i, (ks, tiles) in enumerate(zip(ins, plan)):
-        if i + 1 < len(plan) and plan[i + 1]:
-            b("    const double " + ", ".join(f"{n} = afrag(x, {t[2]})" for n, t in zip(names[i + 1], plan[i + 1])) + ";")
+    return plan
+
+
+def emit_xprod(b, plan, name, til, src, fbase=None, acc="acc"):
+    """CK / volume style product: per k-set the warp-private star chunk X^c of the 4 rows
+    (uniform across lanes), then per c the DMMAs of that c's nonzero tiles.  A fragments of
+    the next k-set are loaded before the current k-set's work."""
+    ins = til["in"][0]
+    b(f"    // {name}: {sum(len(t) for t in plan)} tiles, {len(ins)} k-sets, {len(til['out'])} m-tiles")
+    names = [[f"a{i}_{j}" for j in range(len(t))] for i, t in enumerate(plan)]
+
+    def afr(i):
+        if plan[i]:
+            b("    const double " + ", ".join(f"{nm} = {afrag_expr(t[2], fbase)}" for nm, t in zip(names[i], plan[i])) + ";")
+
+    afr(0)
+    for i, ks in enumerate(ins):
+        if i + 1 < len(ins):
+            afr(i + 1)
         r = kset_rows(ks)
-        b(f"    xchunk<{src}, B>(x, {r[0]}, {r[1]}, {r[2]}, {r[3]});")
-        for c in range(len(mats)):
-            mine = [(mt, nm) for (cc, mt, tid), nm in zip(tiles, names[i]) if cc == c]
+        b(f"    xcalc<{src}, B>(x, 0, {r[0]}, {r[1]}, {r[2]}, {r[3]});")
+        b("    __syncwarp();")
+        for c in range(3):
+            mine = [(mt, nm) for (cc, mt, tid), nm in zip(plan[i], names[i]) if cc == c]
             if not mine:
                 continue
-            b(f"    {{ double bf[4]; xb_b(x, {c}, bf);")
+            b(f"    {{ double bf[kU]; xb_b(x, 0, {c}, bf);")
             for mt, nm in mine:
-                b(f"      dmma4({acc}[{mt}], {nm}, bf);")
+                b(f"      dmma3({acc}[{mt}], {nm}, bf);")
             b("    }")
-        b("    __syncwarp();")
-        nv += len(tiles)
-    return nv
+    return sum(len(t) for t in plan)
 
 
-def emit_gprod(b, tab, M, outs, ins, loader, acc="acc", pre=None):
+def emit_gprod(b, tab, M, outs, ins, loader, acc="acc", fbase=None):
     """Trace / lift style product: B fragments gathered per lane from memory
     (``loader(kset_index, word)`` returns the C expression filling ``bf``)."""
     plan = []
@@ -148,15 +156,15 @@ def emit_gprod(b, tab, M, outs, ins, loader, acc="acc", pre=None):
     names = {i: [f"g{i}_{j}" for j in range(len(t))] for i, _, t in live}
     if live:
         i0 = live[0][0]
-        b("      const double " + ", ".join(f"{nm} = afrag(x, {t[1]})" for nm, t in zip(names[i0], live[0][2])) + ";")
+        b("      const double " + ", ".join(f"{nm} = {afrag_expr(t[1], fbase)}" for nm, t in zip(names[i0], live[0][2])) + ";")
     for k, (i, ks, tiles) in enumerate(live):
         if k + 1 < len(live):
             i1 = live[k + 1][0]
-            b("      const double " + ", ".join(f"{nm} = afrag(x, {t[1]})" for nm, t in zip(names[i1], live[k + 1][2])) + ";")
+            b("      const double " + ", ".join(f"{nm} = {afrag_expr(t[1], fbase)}" for nm, t in zip(names[i1], live[k + 1][2])) + ";")
         src = loader(i, kset_word(ks))
         b(f"      {{ {src}")
         for (mt, tid), nm in zip(tiles, names[i]):
-            b(f"        dmma4({acc}[{mt}], {nm}, bf);")
+            b(f"        dmma3({acc}[{mt}], {nm}, bf);")
         b("      }")
         n += len(tiles)
     return n
@@ -169,8 +177,8 @@ def gen_order(N):
     Bv = comb(N + 2, 3)
     til = tiling.tiling(N)
     tab = Table()
-    IROWS = min(B, r8(Bv))
-    SROWS = max(8, r8(comb(N + 2, 3)))
+    IROWS = Bv  # time-integral rows in shared memory (rows >= Bv are dt * Q)
+    SROWS = Bv  # rows of D^d, d >= 1
     TS = (9 * Bt + 1) // 2 * 2
     QMT = len(til["vol"]["out"])
     LMT = len(til["lift"]["out"])
@@ -178,6 +186,7 @@ def gen_order(N):
     body = []
     b = body.append
     counts = {}
+    regions = {}  # products whose A fragments are staged in shared memory: [first, end)
     # ---------------- CK
     for d in range(N):
         bi, bo = comb(N - d + 3, 3), comb(N - d + 2, 3)
@@ -186,9 +195,14 @@ def gen_order(N):
         mats = [(lambda r, col, c=c: -K[c][col][r]) for c in range(3)]  # Kt^c[r][col] = -K^c[col][r]
         b(f"  // CK step d = {d}: rows in {bi}, rows out {bo}")
         b(f"  static __device__ __forceinline__ void ck{d}(Ctx& x) {{")
-        b(f"    double acc[{MT}][4][2];")
+        b(f"    double acc[{MT}][kU][2];")
         b("    zero_acc(acc);")
-        counts[f"ck{d}"] = emit_xprod(b, tab, f"ck{d}", mats, tl, "SRC_Q" if d == 0 else "SRC_S")
+        f0 = len(tab.frags)
+        plan = plan_xprod(tab, mats, tl)
+        if d == 0:  # staged in the shared-memory fragment buffer
+            regions["CK0"] = (f0, len(tab.frags))
+        counts[f"ck{d}"] = emit_xprod(b, plan, f"ck{d}", tl, "SRC_Q" if d == 0 else "SRC_S",
+                                      fbase=f0 if d == 0 else None)
         b("    __syncthreads();  // every read of D^d done")
         for mt, og in enumerate(tl["out"]):
             b(f"    ck_wb<{1 if d == 0 else 0}, B>(x, acc[{mt}], {d}, {row_word64(og)});")
@@ -199,15 +213,21 @@ def gen_order(N):
     b("  static __device__ __forceinline__ void ck(Ctx& x) {")
     for d in range(N):
         b(f"    ck{d}(x);")
+        if d == 0:
+            b("    after_ck0<" + str(N) + ">(x);  // the fragment buffer is free: stage the volume's")
+        b(f"    YDG_PHASE({2 + d});")
     b("  }")
     # ---------------- volume
     tl = til["vol"]
     mats = [(lambda r, col, c=c: K[c][r][col]) for c in range(3)]
     b(f"  // volume: Q += sum_c Khat^c (I A*^cT)")
-    b(f"  static __device__ __forceinline__ void volume(Ctx& x, double (&acc)[{QMT}][4][2]) {{")
-    counts["vol"] = emit_xprod(b, tab, "vol", mats, tl, "SRC_I")
+    b(f"  static __device__ __forceinline__ void volume(Ctx& x, double (&acc)[{QMT}][kU][2]) {{")
+    f0 = len(tab.frags)
+    plan = plan_xprod(tab, mats, tl)
+    regions["VOL"] = (f0, len(tab.frags))
+    counts["vol"] = emit_xprod(b, plan, "vol", tl, "SRC_I", fbase=f0)
     b("  }")
-    b(f"  static __device__ __forceinline__ void add_volume(const Ctx& x, double* Qt, double (&acc)[{QMT}][4][2]) {{")
+    b(f"  static __device__ __forceinline__ void add_volume(const Ctx& x, double* Qt, double (&acc)[{QMT}][kU][2]) {{")
     b("    constexpr unsigned long long w[] = {" + ", ".join(row_word64(og) for og in tl["out"]) + "};")
     b("    add_q(x, Qt, acc, w);")
     b("  }")
@@ -220,18 +240,18 @@ def gen_order(N):
         ins = tl["in"][0]
         outs = tl["out"]
         b(f"    {'if' if i == 0 else 'else if'} constexpr (F == {i}) {{")
-        b(f"      double acc[{len(outs)}][4][2];")
+        b(f"      double acc[{len(outs)}][kU][2];")
         b("      zero_acc(acc);")
         gl = [k for k, ks in enumerate(ins) if ks[0] >= IROWS]
         if gl:
-            b(f"      double bq[{len(gl)}][4];  // global B fragments first (latency overlap)")
+            b(f"      double bq[{len(gl)}][kU];  // global B fragments first (latency overlap)")
             for n_, k in enumerate(gl):
                 b(f"      gq_b<B>(x, {kset_word(ins[k])}, bq[{n_}]);")
 
         def loader(k, w, gl=gl):
             if k in gl:
-                return f"const double (&bf)[4] = bq[{gl.index(k)}];"
-            return f"double bf[4]; ismem_b(x, {w}, bf);"
+                return f"const double (&bf)[kU] = bq[{gl.index(k)}];"
+            return f"double bf[kU]; ismem_b(x, {w}, bf);"
         Mi = lambda r, col, i=i: R[i][col][r]
         counts[f"tr{i}"] = emit_gprod(b, tab, Mi, outs, ins, loader)
         for mt, og in enumerate(outs):
@@ -246,29 +266,33 @@ def gen_order(N):
     b(f"  // lift + Q update: Q += R^F Y_F (Y own columns in shared memory, rows [m][288])")
     b(f"  template <int F> static __device__ __forceinline__ void lift(Ctx& x, const double* Y, double* Qt) {{")
     counts["lift"] = 0
+    lift0 = len(tab.frags)
+    # the lift fragments are numbered in emission order; the flux kernel holds them all in
+    # shared memory (index relative to lift0)
     for i in range(4):
         b(f"    {'if' if i == 0 else 'else if'} constexpr (F == {i}) {{")
         Mi = lambda r, col, i=i: R[i][r][col]
         ins = tl["in"][i]
-        b("      double2 qn[2][4];")
+        b("      double2 qn[2][kU];")
         g0 = groups[0]
         b(f"      load_q2(x, Qt, {row_word64(outs[g0[0]])}, {row_word64(outs[g0[1]]) if len(g0) > 1 else '~0ULL'}, qn);")
         for gi, grp in enumerate(groups):
             b("      {")
-            b("        double2 qc[2][4];")
+            b("        double2 qc[2][kU];")
             b("        copy_q2(qn, qc);")
             if gi + 1 < len(groups):
                 g1 = groups[gi + 1]
                 b(f"        load_q2(x, Qt, {row_word64(outs[g1[0]])}, {row_word64(outs[g1[1]]) if len(g1) > 1 else '~0ULL'}, qn);")
-            b("        double acc[2][4][2];")
+            b("        double acc[2][kU][2];")
             b("        zero_acc(acc);")
             sub = [outs[m] for m in grp]
             counts["lift"] += emit_gprod(b, tab, Mi, sub, ins,
-                                         lambda k, w: f"double bf[4]; smem_b(x, Y, {w}, bf);")
+                                         lambda k, w: f"double bf[kU]; smem_b(x, Y, {w}, bf);", fbase=lift0)
             b(f"        store_q2(x, Qt, {row_word64(outs[grp[0]])}, {row_word64(outs[grp[1]]) if len(grp) > 1 else '~0ULL'}, acc, qc);")
             b("      }")
         b("    }")
     b("  }")
+    regions["LIFT"] = (lift0, len(tab.frags))
     # ---------------- neighbour orientation z = f^h t, uniform over lanes:
     # f^1 = S (diagonal +-1) and f^2 = S f^0 S, so t' = (h != 0 ? S t : t), u = f^0 t',
     # z = (h == 1 ? t' : (h == 2 ? S u : u))
@@ -303,6 +327,10 @@ def gen_order(N):
              f"  static constexpr int TS = {TS};  // doubles per element-face trace block [m][q]",
              f"  static constexpr int QMT = {QMT}, LMT = {LMT}, TMT = {TMT};",
              f"  static constexpr int NFRAG = {len(tab.frags)};",
+             "  // A-fragment ranges staged in shared memory (first, count)",
+             f"  static constexpr int CK0_F0 = {regions['CK0'][0]}, CK0_NF = {regions['CK0'][1] - regions['CK0'][0]};",
+             f"  static constexpr int VOL_F0 = {regions['VOL'][0]}, VOL_NF = {regions['VOL'][1] - regions['VOL'][0]};",
+             f"  static constexpr int LIFT_F0 = {regions['LIFT'][0]}, LIFT_NF = {regions['LIFT'][1] - regions['LIFT'][0]};",
              "  // DMMA tiles per product (x 4 col tiles x 9 warps per 32-element tile): " +
              ", ".join(f"{k} {v}" for k, v in counts.items())]
     lines += body

@@ -44,7 +44,7 @@ def products(N):
     R = [np.array(r, dtype=float) != 0 for r in t["R"]]
     B, Bt = t["B"], t["Bt"]
     Bv = comb(N + 2, 3)
-    irows = min(B, (Bv + 7) // 8 * 8)  # rows of the time integral held in shared memory
+    irows = Bv  # rows of the time integral held in shared memory
     out = {}
     for d in range(N):
         bi, bo = comb(N - d + 3, 3), comb(N - d + 2, 3)
