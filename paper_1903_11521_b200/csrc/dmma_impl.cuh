@@ -223,9 +223,10 @@ __device__ __forceinline__ void scale_irows(Ctx& x) {
 // Q += acc over all m-tiles (rows from the words w[]), two m-tiles per batch: the batch's
 // Q loads are all issued before its stores (one L2/HBM latency per batch, bounded register
 // use), values are added into the accumulators, then stored (16-byte, two elements).
-template <int MT>
+// Qs: rows < IR of Q^n already in shared memory (plain [row][288] layout), else nullptr
+template <int MT, int IR = 0>
 __device__ __forceinline__ void add_q(const Ctx& x, double* Qt, double (&acc)[MT][kU][2],
-                                      const unsigned long long (&w)[MT]) {
+                                      const unsigned long long (&w)[MT], const double* Qs = nullptr) {
 #pragma unroll
   for (int m0 = 0; m0 < MT; m0 += 2) {
     double2 v[2][kU];
@@ -235,7 +236,8 @@ __device__ __forceinline__ void add_q(const Ctx& x, double* Qt, double (&acc)[MT
 #pragma unroll
       for (int k = 0; k < kU; ++k)
         v[k2][k] = row == 0xff ? make_double2(0.0, 0.0)
-                               : *reinterpret_cast<const double2*>(Qt + row * kRS + ccol(x, k));
+                   : (row < IR ? *reinterpret_cast<const double2*>(Qs + row * kRS + ccol(x, k))
+                               : *reinterpret_cast<const double2*>(Qt + row * kRS + ccol(x, k)));
     }
 #pragma unroll
     for (int k2 = 0; k2 < 2; ++k2) {
@@ -356,7 +358,7 @@ struct Layout {
   static constexpr int FOFF = (ROWS * kRS + XB > G::IROWS * kRS + 2 * FACE ? ROWS * kRS + XB
                                                                            : G::IROWS * kRS + 2 * FACE);
   static constexpr int FSMAX = G::CK0_NF > G::VOL_NF ? G::CK0_NF : G::VOL_NF;
-  static constexpr int LOCAL = FOFF + FSMAX * kL + 2;  // + mbarrier
+  static constexpr int LOCAL = FOFF + FSMAX * kL + 2;  // + two mbarriers
   // flux kernel: own face block, two neighbour face blocks, Y rows, lift fragments, four
   // mbarriers
   static constexpr int FLUX = 3 * FACE + G::Bt * kRS + G::LIFT_NF * kL + 4;
@@ -449,8 +451,11 @@ __global__ void __launch_bounds__(kT, 1) dm_local(const __grid_constant__ StepPa
   x.frags = frag_table<N>();
   x.fs = smem + Lay::FOFF;
   x.fbar = reinterpret_cast<unsigned long long*>(smem + Lay::FOFF + Lay::FSMAX * kL);
+  unsigned long long* qbar = x.fbar + 1;
+  unsigned qph = 0;
   if (threadIdx.x == 0) {
     mbar_init(x.fbar, 1);
+    mbar_init(qbar, 1);
     if (blockIdx.x < prm.ntiles) stage_frags<N>(x, G::CK0_F0, G::CK0_NF);
   }
   __syncthreads();
@@ -524,6 +529,10 @@ __global__ void __launch_bounds__(kT, 1) dm_local(const __grid_constant__ StepPa
     YDG_PHASE(8);
     if (threadIdx.x == 0) bulk_wait_read<0>();
     __syncthreads();  // the staging blocks overlap the X buffers of the volume term
+    if (threadIdx.x == 0) {  // rows < IROWS of Q^n -> S (free now) for the volume's update
+      mbar_expect_tx(qbar, G::IROWS * kRS * sizeof(double));
+      bulk_g2s(x.S, Qt, G::IROWS * kRS * sizeof(double), qbar);
+    }
     YDG_PHASE(9);
     {
       double acc[G::QMT][kU][2];
@@ -531,7 +540,9 @@ __global__ void __launch_bounds__(kT, 1) dm_local(const __grid_constant__ StepPa
       mbar_wait(x.fbar, 1);  // volume fragments (staged after CK step 0)
       G::volume(x, acc);
       YDG_PHASE(10);
-      G::add_volume(x, Qt, acc);
+      mbar_wait(qbar, qph);
+      qph ^= 1;
+      G::add_volume(x, Qt, acc, x.S);
     }
     __syncthreads();  // before the next tile overwrites the shared regions
     if (threadIdx.x == 0 && it + gridDim.x < prm.ntiles) stage_frags<N>(x, G::CK0_F0, G::CK0_NF);

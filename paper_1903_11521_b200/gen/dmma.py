@@ -227,9 +227,9 @@ def gen_order(N):
     regions["VOL"] = (f0, len(tab.frags))
     counts["vol"] = emit_xprod(b, plan, "vol", tl, "SRC_I", fbase=f0)
     b("  }")
-    b(f"  static __device__ __forceinline__ void add_volume(const Ctx& x, double* Qt, double (&acc)[{QMT}][kU][2]) {{")
+    b(f"  static __device__ __forceinline__ void add_volume(const Ctx& x, double* Qt, double (&acc)[{QMT}][kU][2], const double* Qs) {{")
     b("    constexpr unsigned long long w[] = {" + ", ".join(row_word64(og) for og in tl["out"]) + "};")
-    b("    add_q(x, Qt, acc, w);")
+    b("    add_q<" + str(QMT) + ", IROWS>(x, Qt, acc, w, Qs);")
     b("  }")
     # ---------------- traces T_i = R^iT I
     b(f"  // trace: T_F = R^FT I (rows < IROWS of I from shared memory, dt * Q from global memory);")
