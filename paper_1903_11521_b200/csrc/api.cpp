@@ -34,7 +34,8 @@ struct ydg_solver {
   // mesh
   bool have_mesh = false;
   int64_t ne = 0, first = 0, nlocal = 0;
-  int64_t nslots = 0;   // local element slots incl. ghosts (multiple of 32)
+  int64_t nslots = 0;   // local element slots incl. ghosts (multiple of lanes)
+  int lanes = 32;       // elements per tile: 16 (fp64 tensor-core kernels) or 32 (fp32)
   int64_t ntiles = 0;   // owned tiles
   Neighbours nbr;       // global tables (for ydg_get_neighbours)
   // device buffers
@@ -86,7 +87,7 @@ int fail(ydg_solver* h, int code, const std::string& msg) {
 int elem_bytes(const ydg_solver* h) { return h->prec; }
 
 // Values per element-face trace block of the fp64 tensor-core kernels (layout
-// [tile][face][lane][TS], block [m][q] padded to 16 bytes); 0 = the fp32 layout
+// [tile][face][lane][TS], 16 lanes, block [m][q] padded to 16 bytes); 0 = the fp32 layout
 // [tile][face][m][q][32].
 int trace_block(const ydg_solver* h) { return h->prec == 8 ? (h->Bt * h->P + 1) / 2 * 2 : 0; }
 
@@ -120,11 +121,12 @@ int check(ydg_solver* h) {
   return YDG_OK;
 }
 
-// Per-element coefficients in the tiled layouts of the kernels.  fp64 (tensor-core
-// kernels): star [tile][c][p][3][32] and the factored flux solvers [tile][face][12][32];
-// fp32 (sparse kernels): star and the flux-solver matrices A+-, [tile][face][p][q][32].
+// Per-element coefficients in the tiled layouts of the kernels (tiles of kLanes elements:
+// 16 for fp64, 32 for fp32).  fp64 (tensor-core kernels): star [tile][c][p][3][lane] and
+// the factored flux solvers [tile][face][12][lane]; fp32 (sparse kernels): star and the
+// flux-solver matrices A+-, [tile][face][p][q][lane].
 template <typename T>
-void pack_tiles(int P, int64_t n, bool factored, const ElementCoeffs& c, std::vector<T>& star,
+void pack_tiles(int P, int64_t n, bool factored, int kLanes, const ElementCoeffs& c, std::vector<T>& star,
                 std::vector<T>& ap, std::vector<T>& am) {
   for (int64_t t = 0; t < n; ++t) {
     const int64_t tile = t / kLanes, lane = t % kLanes;
@@ -154,6 +156,7 @@ template <typename T>
 int upload_coeffs(ydg_solver* h, const double* xyz, const double* material, const double* anel) {
   const int P = h->P;
   const bool factored = sizeof(T) == 8;  // fp64 flux kernel rebuilds A+- from 12 values/face
+  const int kLanes = h->lanes;
   const int64_t tiles = h->nslots / kLanes;
   const size_t star_t = static_cast<size_t>(3) * P * 3 * kLanes;  // per tile
   const size_t flux_t = factored ? static_cast<size_t>(4) * kFaceCoeffs * kLanes : static_cast<size_t>(4) * P * P * kLanes;
@@ -180,7 +183,7 @@ int upload_coeffs(ydg_solver* h, const double* xyz, const double* material, cons
     st.assign(static_cast<size_t>(ct) * star_t, T(0));
     ap.assign(static_cast<size_t>(ct) * flux_t, T(0));
     am.assign(factored ? 0 : ap.size(), T(0));
-    pack_tiles<T>(P, n, factored, c, st, ap, am);
+    pack_tiles<T>(P, n, factored, kLanes, c, st, ap, am);
     CUDA_OR_FAIL(h, cudaMemcpy(static_cast<T*>(h->star) + static_cast<size_t>(t0) * star_t, st.data(),
                                st.size() * sizeof(T), cudaMemcpyHostToDevice));
     CUDA_OR_FAIL(h, cudaMemcpy(static_cast<T*>(h->aplus) + static_cast<size_t>(t0) * flux_t, ap.data(),
@@ -564,6 +567,8 @@ int ydg_upload_mesh(ydg_solver* h, int64_t ne, const double* xyz, const int64_t*
     h->have_mesh = true;
     return YDG_OK;
   }
+  h->lanes = h->prec == 8 ? 16 : 32;
+  const int kLanes = h->lanes;
   h->ntiles = (h->nlocal + kLanes - 1) / kLanes;
   // local slots: owned [0, nlocal) padded to tiles, then ghosts
   std::vector<int64_t> ghost_of;  // global element id of each ghost slot
@@ -632,7 +637,7 @@ int ydg_upload_mesh(ydg_solver* h, int64_t ne, const double* xyz, const int64_t*
   rc = eb == 8 ? upload_coeffs<double>(h, xyz, material, anelastic) : upload_coeffs<float>(h, xyz, material, anelastic);
   if (rc) { free_mesh(h); return rc; }
   if (h->nranks > 1) {
-    rc = h->halo.bind(h->traces, h->Bt, h->P, trace_block(h), eb, owned_slots, &h->err);
+    rc = h->halo.bind(h->traces, h->Bt, h->P, trace_block(h), h->lanes, eb, owned_slots, &h->err);
     if (rc) { free_mesh(h); return fail(h, rc, h->err); }
   }
   // staging buffer for DOF transfers (bounded)
@@ -641,8 +646,8 @@ int ydg_upload_mesh(ydg_solver* h, int64_t ne, const double* xyz, const int64_t*
   // grids: resident CTAs per SM x SMs
   int sms = 0, occ_l = 0, occ_n = 0;
   CUDA_OR_FAIL(h, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->dev));
-  occ_l = 1;
-  occ_n = 1;
+  occ_l = eb == 8 ? 2 : 1;  // fp64: two 6-warp CTAs of 16-element tiles per SM
+  occ_n = eb == 8 ? 2 : 1;
   h->grid_local = sms * occ_l;
   h->grid_neigh = sms * occ_n;
   h->have_mesh = true;
@@ -683,14 +688,14 @@ static int xfer_dofs(ydg_solver* h, int64_t first, int64_t count, const void* sr
         CUDA_OR_FAIL(h, cudaMemcpyAsync(buf, static_cast<const char*>(src_host) + c0 * per * eb, n * per * eb,
                                         cudaMemcpyHostToDevice, s));
       }
-      cudaError_t e = eb == 8 ? launch_to_tiled<double>(h->P, h->B, static_cast<const double*>(buf), static_cast<double*>(h->Q), lfirst, n, s)
-                              : launch_to_tiled<float>(h->P, h->B, static_cast<const float*>(buf), static_cast<float*>(h->Q), lfirst, n, s);
+      cudaError_t e = eb == 8 ? launch_to_tiled<double>(h->P, h->B, h->lanes, static_cast<const double*>(buf), static_cast<double*>(h->Q), lfirst, n, s)
+                              : launch_to_tiled<float>(h->P, h->B, h->lanes, static_cast<const float*>(buf), static_cast<float*>(h->Q), lfirst, n, s);
       CUDA_OR_FAIL(h, e);
       if (!dev_side) CUDA_OR_FAIL(h, cudaStreamSynchronize(s));
     } else {
       if (dev_side) buf = static_cast<char*>(dst_dev) + c0 * per * eb;
-      cudaError_t e = eb == 8 ? launch_to_canonical<double>(h->P, h->B, static_cast<const double*>(h->Q), static_cast<double*>(buf), lfirst, n, s)
-                              : launch_to_canonical<float>(h->P, h->B, static_cast<const float*>(h->Q), static_cast<float*>(buf), lfirst, n, s);
+      cudaError_t e = eb == 8 ? launch_to_canonical<double>(h->P, h->B, h->lanes, static_cast<const double*>(h->Q), static_cast<double*>(buf), lfirst, n, s)
+                              : launch_to_canonical<float>(h->P, h->B, h->lanes, static_cast<const float*>(h->Q), static_cast<float*>(buf), lfirst, n, s);
       CUDA_OR_FAIL(h, e);
       if (!dev_side) {
         CUDA_OR_FAIL(h, cudaMemcpyAsync(static_cast<char*>(dst_host) + c0 * per * eb, buf, n * per * eb,

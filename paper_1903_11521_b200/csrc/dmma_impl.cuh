@@ -2,10 +2,11 @@
 //
 // Data of a 32-element tile live in shared memory as [row][col] with col = p*32 + e
 // (quantity-major), rows swizzled (col ^ 8*(row & 1)) so that the 4-row x 8-column DMMA
-// B-fragment loads take the minimum two wavefronts.  A CTA has 12 warps, three per SM
-// sub-partition (a multiple of 4 keeps the four tensor pipes equally loaded between
-// barriers): warp w owns the 8-column tiles (quantity 3g + k, elements 8ct..8ct+7),
-// k = 0..2, with g = w / 4, ct = w % 4 -- its "units".  Every B operand a warp feeds to a
+// B-fragment loads take the minimum two wavefronts.  A tile is 16 elements; a CTA has 6
+// warps and two CTAs share an SM, so each SM sub-partition runs three warps (equal load on
+// the four tensor pipes) and one CTA's barriers, memory phases and latency chains overlap
+// the other's DMMAs.  Warp w owns the 8-column tiles (quantity 3g + k, elements
+// 8ct..8ct+7), k = 0..2, with g = w / 2, ct = w % 2 -- its "units".  Every B operand a warp feeds to a
 // DMMA is warp-private; only the per-element quantity mixing (star matrices A*, flux
 // solvers) reads other warps' columns.  Global matrices are the DMMA A operands:
 // generated 8x4 tiles over freely grouped rows (gen/dmma.py, gen/tiling.py).
@@ -21,9 +22,9 @@ namespace ydg {
 namespace dm {
 
 constexpr int kP = 9;
-constexpr int kL = 32;
-constexpr int kRS = kP * kL;   // 288 columns per row
-constexpr int kW = 12;         // warps per CTA
+constexpr int kL = 16;         // elements per tile (HBM layouts of the fp64 path use the same)
+constexpr int kRS = kP * kL;   // 144 columns per row
+constexpr int kW = 6;          // warps per CTA (two CTAs per SM: 3 warps per sub-partition)
 constexpr int kT = kW * 32;    // threads per CTA
 constexpr int kU = 3;          // units (8-column tiles) per warp
 constexpr int kXW = 3 * kU * 4 * 8;  // warp-private X buffer: [c][k][row][8 elements]
@@ -79,10 +80,21 @@ __device__ const double* frag_table();
 // streaming loads use evict_first so they do not push the fragment table out.
 __device__ __forceinline__ double afrag(const Ctx& x, int tid) {
   double v;
-  asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(x.frags + tid * kL + x.lane));
+  asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(x.frags + tid * 32 + x.lane));
   return v;
 }
-__device__ __forceinline__ double afrag_s(const Ctx& x, int i) { return x.fs[i * kL + x.lane]; }
+__device__ __forceinline__ double afrag_s(const Ctx& x, int i) { return x.fs[i * 32 + x.lane]; }
+// Products whose fragments may be staged in shared memory: CK step 0 and the volume term
+// (local kernel), the lift (flux kernel).  With two CTAs per SM there is no room: off.
+#ifndef YDG_LOCAL_FS
+#define YDG_LOCAL_FS 0
+#endif
+#ifndef YDG_FLUX_FS
+#define YDG_FLUX_FS 0
+#endif
+constexpr bool kLocalFs = YDG_LOCAL_FS, kFluxFs = YDG_FLUX_FS;
+__device__ __forceinline__ double afrag_l(const Ctx& x, int g, int r) { return kLocalFs ? afrag_s(x, r) : afrag(x, g); }
+__device__ __forceinline__ double afrag_f(const Ctx& x, int g, int r) { return kFluxFs ? afrag_s(x, r) : afrag(x, g); }
 __device__ __forceinline__ double ld_stream(const double* p) {
   double v;
   asm("ld.global.nc.L1::evict_first.f64 %0, [%1];" : "=d"(v) : "l"(p));
@@ -288,7 +300,7 @@ template <int TS>
 __device__ __forceinline__ void stage_trace(const Ctx& x, double* stg, const double (&acc)[kU][2], unsigned long long w) {
   const int m = mrow(x, w);
   if (m == 0xff) return;
-  const int e = (x.col0 & 31) + 2 * (x.lane & 3), p0 = x.col0 >> 5;
+  const int e = (x.col0 % kL) + 2 * (x.lane & 3), p0 = x.col0 / kL;
 #pragma unroll
   for (int k = 0; k < kU; ++k) {
     stg[e * TS + m * kP + p0 + k] = acc[k][0];
@@ -357,11 +369,11 @@ struct Layout {
   // A-fragment buffer (CK step 0, then the volume term) after I, S, xb and the staging
   static constexpr int FOFF = (ROWS * kRS + XB > G::IROWS * kRS + 2 * FACE ? ROWS * kRS + XB
                                                                            : G::IROWS * kRS + 2 * FACE);
-  static constexpr int FSMAX = G::CK0_NF > G::VOL_NF ? G::CK0_NF : G::VOL_NF;
-  static constexpr int LOCAL = FOFF + FSMAX * kL + 2;  // + two mbarriers
+  static constexpr int FSMAX = kLocalFs ? (G::CK0_NF > G::VOL_NF ? G::CK0_NF : G::VOL_NF) : 0;
+  static constexpr int LOCAL = FOFF + FSMAX * 32 + 2;  // + two mbarriers
   // flux kernel: own face block, two neighbour face blocks, Y rows, lift fragments, four
   // mbarriers
-  static constexpr int FLUX = 3 * FACE + G::Bt * kRS + G::LIFT_NF * kL + 4;
+  static constexpr int FLUX = 3 * FACE + G::Bt * kRS + (kFluxFs ? G::LIFT_NF * 32 : 0) + 4;
 };
 
 // ---- asynchronous copy helpers (TMA bulk copies + mbarrier, Ampere-style cp.async)
@@ -415,30 +427,31 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
 __device__ __forceinline__ void init_ctx(Ctx& x) {
   x.lane = threadIdx.x & 31;
   x.w = threadIdx.x >> 5;
-  x.col0 = 3 * (x.w >> 2) * kL + 8 * (x.w & 3);
+  x.col0 = 3 * (x.w >> 1) * kL + 8 * (x.w & 1);
   x.sh4 = 8 * (x.lane & 3);
   x.sh8 = 8 * (x.lane >> 2);
-  x.xe = 8 * (x.w & 3) + (x.lane & 7);
+  x.xe = 8 * (x.w & 1) + (x.lane & 7);
   x.xk = x.lane >> 3;
 }
 
 // Stage NF A fragments starting at table index F0 into the shared buffer (one thread).
 template <int N>
 __device__ __forceinline__ void stage_frags(const Ctx& x, int F0, int NF) {
-  mbar_expect_tx(x.fbar, NF * kL * sizeof(double));
-  bulk_g2s(const_cast<double*>(x.fs), frag_table<N>() + F0 * kL, NF * kL * sizeof(double), x.fbar);
+  mbar_expect_tx(x.fbar, NF * 32 * sizeof(double));
+  bulk_g2s(const_cast<double*>(x.fs), frag_table<N>() + F0 * 32, NF * 32 * sizeof(double), x.fbar);
 }
 // Called by DG<N>::ck after CK step 0 (which ends with a barrier): the fragment buffer
 // now receives the volume term's fragments.
 template <int N>
 __device__ __forceinline__ void after_ck0(Ctx& x) {
-  if (threadIdx.x == 0) stage_frags<N>(x, DG<N>::VOL_F0, DG<N>::VOL_NF);
+  if constexpr (kLocalFs)
+    if (threadIdx.x == 0) stage_frags<N>(x, DG<N>::VOL_F0, DG<N>::VOL_NF);
 }
 
 // CK + time integral, face traces R^iT I (stored for the flux kernel) and
 // the volume term for 32-element tiles.
 template <int N>
-__global__ void __launch_bounds__(kT, 1) dm_local(const __grid_constant__ StepParams<double> prm) {
+__global__ void __launch_bounds__(kT, 2) dm_local(const __grid_constant__ StepParams<double> prm) {
   using G = DG<N>;
   using Lay = Layout<N>;
   constexpr int B = G::B;
@@ -450,13 +463,13 @@ __global__ void __launch_bounds__(kT, 1) dm_local(const __grid_constant__ StepPa
   x.xb = smem + Lay::ROWS * kRS + x.w * kXBUF * kXW;
   x.frags = frag_table<N>();
   x.fs = smem + Lay::FOFF;
-  x.fbar = reinterpret_cast<unsigned long long*>(smem + Lay::FOFF + Lay::FSMAX * kL);
+  x.fbar = reinterpret_cast<unsigned long long*>(smem + Lay::FOFF + Lay::FSMAX * 32);
   unsigned long long* qbar = x.fbar + 1;
   unsigned qph = 0;
   if (threadIdx.x == 0) {
     mbar_init(x.fbar, 1);
     mbar_init(qbar, 1);
-    if (blockIdx.x < prm.ntiles) stage_frags<N>(x, G::CK0_F0, G::CK0_NF);
+    if (kLocalFs && blockIdx.x < prm.ntiles) stage_frags<N>(x, G::CK0_F0, G::CK0_NF);
   }
   __syncthreads();
   x.dt = prm.dt;
@@ -466,7 +479,7 @@ __global__ void __launch_bounds__(kT, 1) dm_local(const __grid_constant__ StepPa
   double* stg1 = x.S + Lay::FACE;
   // 3-column pattern of star-matrix row p = 3g + xk of the star-chunk role (setup.cpp
   // star_cols), packed 5 bits per column
-  const int xp = 3 * (x.w >> 2) + (x.xk < kU ? x.xk : 0);
+  const int xp = 3 * (x.w >> 1) + (x.xk < kU ? x.xk : 0);
   {
     constexpr unsigned long long packed[9] = {6 | 7 << 5 | 8 << 10, 6 | 7 << 5 | 8 << 10, 6 | 7 << 5 | 8 << 10,
                                               6 | 7 << 5 | 7 << 10, 7 | 8 << 5 | 8 << 10, 6 | 8 << 5 | 8 << 10,
@@ -504,7 +517,7 @@ __global__ void __launch_bounds__(kT, 1) dm_local(const __grid_constant__ StepPa
 #pragma unroll
       for (int j = 0; j < 3; ++j) x.a[3 * c + j] = ld_stream(st + ((c * kP + xp) * 3 + j) * kL);
     cp_async_wait_all();
-    mbar_wait(x.fbar, 0);  // CK step 0 fragments (first of the buffer's two loads per tile)
+    if constexpr (kLocalFs) mbar_wait(x.fbar, 0);  // CK step 0 fragments (first of two loads per tile)
     __syncthreads();
     YDG_PHASE(1);
     G::ck(x);  // ends with a barrier: the time integral is complete
@@ -537,7 +550,7 @@ __global__ void __launch_bounds__(kT, 1) dm_local(const __grid_constant__ StepPa
     {
       double acc[G::QMT][kU][2];
       zero_acc(acc);
-      mbar_wait(x.fbar, 1);  // volume fragments (staged after CK step 0)
+      if constexpr (kLocalFs) mbar_wait(x.fbar, 1);  // volume fragments (staged after CK step 0)
       G::volume(x, acc);
       YDG_PHASE(10);
       mbar_wait(qbar, qph);
@@ -545,7 +558,7 @@ __global__ void __launch_bounds__(kT, 1) dm_local(const __grid_constant__ StepPa
       G::add_volume(x, Qt, acc, x.S);
     }
     __syncthreads();  // before the next tile overwrites the shared regions
-    if (threadIdx.x == 0 && it + gridDim.x < prm.ntiles) stage_frags<N>(x, G::CK0_F0, G::CK0_NF);
+    if (kLocalFs && threadIdx.x == 0 && it + gridDim.x < prm.ntiles) stage_frags<N>(x, G::CK0_F0, G::CK0_NF);
     YDG_PHASE(11);
 #ifdef YDG_PHASES
     if (threadIdx.x == 0 && blockIdx.x == 0 && it >= 2 * gridDim.x && it < 6 * gridDim.x) {
@@ -567,16 +580,17 @@ __global__ void __launch_bounds__(kT, 1) dm_local(const __grid_constant__ StepPa
 // (e, m) builds the Godunov flux of row m from T and Z (godunov_flux), writing Y (rows
 // [m][288]), and the warp lifts its own columns of Y with DMMAs into Q.
 template <int N>
-__global__ void __launch_bounds__(kT, 1) dm_flux(const __grid_constant__ StepParams<double> prm) {
+__global__ void __launch_bounds__(kT, 2) dm_flux(const __grid_constant__ StepParams<double> prm) {
   using G = DG<N>;
   using Lay = Layout<N>;
   constexpr int B = G::B, Bt = G::Bt, TS = G::TS, FACE = Lay::FACE;
   extern __shared__ __align__(128) double smem[];
   double* O = smem;                    // own face block [lane][TS]
   double* NB = smem + FACE;            // [2][lane][TS] neighbour face blocks
-  double* Y = smem + 3 * FACE;         // [Bt][288] mixed face values
-  double* FS = Y + Bt * kRS;           // the lift's A fragments (whole kernel)
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(FS + G::LIFT_NF * kL);  // own, nb0, nb1, fs
+  double* Y = smem + 3 * FACE;         // [Bt][144] mixed face values
+  double* FS = Y + Bt * kRS;           // the lift's A fragments (if kFluxFs)
+  unsigned long long* bar =
+      reinterpret_cast<unsigned long long*>(FS + (kFluxFs ? G::LIFT_NF * 32 : 0));  // own, nb0, nb1, fs
   Ctx x;
   init_ctx(x);
   x.frags = frag_table<N>();
@@ -588,28 +602,39 @@ __global__ void __launch_bounds__(kT, 1) dm_flux(const __grid_constant__ StepPar
     mbar_init(&bar[1], 1);
     mbar_init(&bar[2], 1);
     mbar_init(&bar[3], 1);
-    stage_frags<N>(x, G::LIFT_F0, G::LIFT_NF);
+    if (kFluxFs) stage_frags<N>(x, G::LIFT_F0, G::LIFT_NF);
   }
   __syncthreads();
-  auto issue_own = [&](int64_t tile, int F) {  // one thread
+  // thread 0 issues the TMA copies: the tile's own face block, one block per element for
+  // the neighbour faces
+  auto issue_own = [&](int64_t tile, int F) {
     mbar_expect_tx(&bar[0], FACE * sizeof(double));
     bulk_g2s(O, prm.traces + (tile * 4 + F) * FACE, FACE * sizeof(double), &bar[0]);
   };
-  auto issue_nb = [&](int64_t tile, int F, int b) {  // warp 0
-    if (x.lane == 0) mbar_expect_tx(&bar[1 + b], FACE * sizeof(double));
-    __syncwarp();
-    const int64_t slot = (tile * 4 + F) * kL + x.lane;
-    const int64_t nbe = prm.nb[slot];
-    const int j = prm.jh[slot] & 3;
-    bulk_g2s(NB + b * FACE + x.lane * TS, prm.traces + ((nbe >> 5) * 4 + j) * FACE + (nbe & 31) * TS,
-             TS * sizeof(double), &bar[1 + b]);
+  auto issue_nb = [&](int64_t tile, int F, int b) {
+    mbar_expect_tx(&bar[1 + b], FACE * sizeof(double));
+    int64_t nbe[kL];
+    int jj[kL];
+#pragma unroll
+    for (int e = 0; e < kL; ++e) {
+      const int64_t slot = (tile * 4 + F) * kL + e;
+      nbe[e] = prm.nb[slot];
+      jj[e] = prm.jh[slot] & 3;
+    }
+#pragma unroll
+    for (int e = 0; e < kL; ++e)
+      bulk_g2s(NB + b * FACE + e * TS, prm.traces + ((nbe[e] / kL) * 4 + jj[e]) * FACE + (nbe[e] % kL) * TS,
+               TS * sizeof(double), &bar[1 + b]);
   };
-  if (threadIdx.x < kL) {
-    if (threadIdx.x == 0) issue_own(prm.tile0 + blockIdx.x, 0);
+  if (threadIdx.x == 0) {
+    issue_own(prm.tile0 + blockIdx.x, 0);
     issue_nb(prm.tile0 + blockIdx.x, 0, 0);
   }
   unsigned ph_o = 0, ph_n0 = 0, ph_n1 = 0;
-  mbar_wait(x.fbar, 0);
+  if constexpr (kFluxFs) mbar_wait(x.fbar, 0);
+  // thread roles: rotation (element re, column rp) for threads < 144; Godunov rows
+  // m = gm + 12 i of element ge
+  const int re = threadIdx.x % kL, rp = threadIdx.x / kL;
   for (int64_t it = blockIdx.x; it < prm.ntiles; it += gridDim.x) {
     const int64_t tile = prm.tile0 + it;
     const bool more = it + gridDim.x < prm.ntiles;
@@ -617,19 +642,17 @@ __global__ void __launch_bounds__(kT, 1) dm_flux(const __grid_constant__ StepPar
     for (int F = 0; F < 4; ++F) {
       const int b = F & 1;
       __syncthreads();  // lift of the previous face done: Y and neighbour buffer b ^ 1 are free
-      if (threadIdx.x < kL) {
+      if (threadIdx.x == 0) {
         if (F < 3) issue_nb(tile, F + 1, b ^ 1);
         else if (more) issue_nb(tile + gridDim.x, 0, b ^ 1);
-      } else if (threadIdx.x == kL) {  // next item's flux coefficients (and next tile's Q) -> L2
+      } else if (threadIdx.x == 32) {  // next item's flux coefficients (and next tile's Q) -> L2
         const int64_t nt = F < 3 ? tile : tile + gridDim.x;
         const int nF = F < 3 ? F + 1 : 0;
-        if (F < 3 || more) {
-          prefetch_l2(prm.aplus + (nt * 4 + nF) * kFaceCoeffs * kL, kFaceCoeffs * kL * sizeof(double));
-        }
+        if (F < 3 || more) prefetch_l2(prm.aplus + (nt * 4 + nF) * kFaceCoeffs * kL, kFaceCoeffs * kL * sizeof(double));
         if (F == 3 && more) prefetch_l2(prm.Q + nt * B * kRS, B * kRS * sizeof(double));
       }
-      double* Z = NB + b * FACE + x.lane * TS;
-      const int h = prm.jh[(tile * 4 + F) * kL + x.lane] >> 2;
+      double* Zb = NB + b * FACE;
+      const int h = prm.jh[(tile * 4 + F) * kL + re] >> 2;
       if (b == 0) {
         mbar_wait(&bar[1], ph_n0);
         ph_n0 ^= 1;
@@ -637,29 +660,31 @@ __global__ void __launch_bounds__(kT, 1) dm_flux(const __grid_constant__ StepPar
         mbar_wait(&bar[2], ph_n1);
         ph_n1 ^= 1;
       }
-      if (x.w < kP) {  // z = f^h t on column p = w of the lane's neighbour block
+      if (threadIdx.x < kP * kL) {  // z = f^h t on column rp of element re's neighbour block
+        double* z = Zb + re * TS + rp;
         double t[Bt];
 #pragma unroll
-        for (int n = 0; n < Bt; ++n) t[n] = Z[n * kP + x.w];
-        G::rot(h, t, Z + x.w);
+        for (int n = 0; n < Bt; ++n) t[n] = z[n * kP];
+        G::rot(h, t, z);
       }
-      // flux solvers of this face, factored (setup.h kFaceCoeffs): the lane's element
+      // flux solvers of this face, factored (setup.h kFaceCoeffs): element ge's
       double fc[kFaceCoeffs];
 #pragma unroll
-      for (int k = 0; k < kFaceCoeffs; ++k) fc[k] = prm.aplus[((tile * 4 + F) * kFaceCoeffs + k) * kL + x.lane];
+      for (int k = 0; k < kFaceCoeffs; ++k) fc[k] = prm.aplus[((tile * 4 + F) * kFaceCoeffs + k) * kL + re];
       mbar_wait(&bar[0], ph_o);
       ph_o ^= 1;
       __syncthreads();  // rotated neighbour columns visible
       {
-        const double* T = O + x.lane * TS;
+        const double* T = O + re * TS;
+        const double* Z = Zb + re * TS;
 #pragma unroll
-        for (int i = 0; i < (Bt + kW - 1) / kW; ++i) {  // rows m = w, w + 12, ... of element lane
-          const int m = x.w + kW * i;
+        for (int i = 0; i < (Bt + kT / kL - 1) / (kT / kL); ++i) {  // rows m = rp, rp + 12, ...
+          const int m = rp + (kT / kL) * i;
           if (m >= Bt) break;
           double y[kP];
           godunov_flux(T + m * kP, Z + m * kP, fc, y);
 #pragma unroll
-          for (int q = 0; q < kP; ++q) Y[swz(m, q * kL + x.lane)] = y[q];
+          for (int q = 0; q < kP; ++q) Y[swz(m, q * kL + re)] = y[q];
         }
       }
       __syncthreads();  // every read of O done; Y complete
@@ -667,9 +692,8 @@ __global__ void __launch_bounds__(kT, 1) dm_flux(const __grid_constant__ StepPar
         if (F < 3) issue_own(tile, F + 1);
         else if (more) issue_own(tile + gridDim.x, 0);
       }
-      // lift and Q update per face, two m-tiles at a time (accumulators and Q rows live only
-      // there: 168 registers per thread with 9 warps); the tile's Q stays in L2 across its
-      // four updates
+      // lift and Q update per face, two m-tiles at a time; the tile's Q stays in L2
+      // across its four updates
       double* Qt = prm.Q + tile * B * kRS;
       if (F == 0) G::template lift<0>(x, Y, Qt);
       else if (F == 1) G::template lift<1>(x, Y, Qt);

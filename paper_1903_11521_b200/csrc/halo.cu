@@ -52,37 +52,37 @@ struct Nccl {
 Nccl g_nccl;
 
 // index of value v (= (face, m, q) flattened) of local element slot s in the trace layout:
-// TS == 0: [tile][face][m][q][32] (fp32 kernels); TS > 0: [tile][face][lane][TS] with an
-// element-face block [m][q] of TS values (fp64 tensor-core kernels)
-__device__ __forceinline__ int64_t tiled_index(int64_t s, int v, int Bt, int P, int TS) {
+// TS == 0: [tile][face][m][q][32] (fp32 kernels); TS > 0: [tile][face][lane][TS] with L
+// lanes per tile and an element-face block [m][q] of TS values (fp64 tensor-core kernels)
+__device__ __forceinline__ int64_t tiled_index(int64_t s, int v, int Bt, int P, int TS, int L) {
   const int F = v / (Bt * P), m = (v / P) % Bt, q = v % P;
-  if (TS > 0) return (((s >> 5) * 4 + F) * 32 + (s & 31)) * (int64_t)TS + m * P + q;
+  if (TS > 0) return (((s / L) * 4 + F) * L + (s % L)) * (int64_t)TS + m * P + q;
   return (((s >> 5) * 4 + F) * Bt + m) * (int64_t)(P * 32) + q * 32 + (s & 31);
 }
 
 template <typename W>
 __global__ void pack_kernel(const W* __restrict__ traces, const int64_t* __restrict__ slots,
-                            W* __restrict__ out, int64_t n, int Bt, int P, int TS) {
+                            W* __restrict__ out, int64_t n, int Bt, int P, int TS, int L) {
   const int vals = 4 * Bt * P;
   const int64_t total = n * vals;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = i / vals;
     const int v = static_cast<int>(i - s * vals);
-    out[i] = traces[tiled_index(slots[s], v, Bt, P, TS)];
+    out[i] = traces[tiled_index(slots[s], v, Bt, P, TS, L)];
   }
 }
 
 template <typename W>
 __global__ void unpack_kernel(const W* __restrict__ in, W* __restrict__ traces, int64_t first_slot,
-                              int64_t n, int Bt, int P, int TS) {
+                              int64_t n, int Bt, int P, int TS, int L) {
   const int vals = 4 * Bt * P;
   const int64_t total = n * vals;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t g = i / vals;
     const int v = static_cast<int>(i - g * vals);
-    traces[tiled_index(first_slot + g, v, Bt, P, TS)] = in[i];
+    traces[tiled_index(first_slot + g, v, Bt, P, TS, L)] = in[i];
   }
 }
 
@@ -178,10 +178,11 @@ int Halo::plan(const Neighbours& nbr, int64_t first, int64_t nlocal, int64_t own
   return 0;
 }
 
-int Halo::bind(void* traces, int Bt, int P, int TS, int elem_bytes, int64_t owned_slots, std::string* err) {
+int Halo::bind(void* traces, int Bt, int P, int TS, int L, int elem_bytes, int64_t owned_slots, std::string* err) {
   (void)traces;
   Bt_ = Bt;
   TS_ = TS;
+  L_ = L;
   P_ = P;
   vals_ = 4 * Bt * P;
   eb_ = elem_bytes;
@@ -205,11 +206,11 @@ int Halo::exchange(cudaStream_t s, void* traces, int elem_bytes, std::string* er
     if (elem_bytes == 8)
       pack_kernel<unsigned long long><<<148 * 4, 256, 0, cstream_>>>(
           static_cast<const unsigned long long*>(traces), d_send_slots_,
-          static_cast<unsigned long long*>(d_send_buf_), ns, Bt_, P_, TS_);
+          static_cast<unsigned long long*>(d_send_buf_), ns, Bt_, P_, TS_, L_);
     else
       pack_kernel<unsigned int><<<148 * 4, 256, 0, cstream_>>>(
           static_cast<const unsigned int*>(traces), d_send_slots_, static_cast<unsigned int*>(d_send_buf_),
-          ns, Bt_, P_, TS_);
+          ns, Bt_, P_, TS_, L_);
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
@@ -228,11 +229,11 @@ int Halo::exchange(cudaStream_t s, void* traces, int elem_bytes, std::string* er
     if (elem_bytes == 8)
       unpack_kernel<unsigned long long><<<148 * 4, 256, 0, cstream_>>>(
           static_cast<const unsigned long long*>(d_recv_buf_), static_cast<unsigned long long*>(traces),
-          owned_slots_, ng, Bt_, P_, TS_);
+          owned_slots_, ng, Bt_, P_, TS_, L_);
     else
       unpack_kernel<unsigned int><<<148 * 4, 256, 0, cstream_>>>(
           static_cast<const unsigned int*>(d_recv_buf_), static_cast<unsigned int*>(traces), owned_slots_,
-          ng, Bt_, P_, TS_);
+          ng, Bt_, P_, TS_, L_);
     e = cudaGetLastError();
     if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
   }

@@ -37,7 +37,7 @@ class Halo {
            std::vector<int64_t>* ghost_of, std::string* err);
   // traces use the layout [tile][face][m][q][32] (TS = 0) or [tile][face][lane][TS] with
   // element-face blocks [m][q] (TS > 0), Bt face functions, P quantities
-  int bind(void* traces, int Bt, int P, int TS, int elem_bytes, int64_t owned_slots, std::string* err);
+  int bind(void* traces, int Bt, int P, int TS, int L, int elem_bytes, int64_t owned_slots, std::string* err);
   // pack + send/recv on the comm stream after `s` reaches this point
   int exchange(cudaStream_t s, void* traces, int elem_bytes, std::string* err);
   // make `s` wait for the exchange
@@ -55,7 +55,7 @@ class Halo {
   int64_t* d_send_slots_ = nullptr;
   void* d_send_buf_ = nullptr;
   void* d_recv_buf_ = nullptr;
-  int vals_ = 0, eb_ = 0, Bt_ = 0, P_ = 0, TS_ = 0;
+  int vals_ = 0, eb_ = 0, Bt_ = 0, P_ = 0, TS_ = 0, L_ = 32;
   int64_t owned_slots_ = 0;
 };
 

@@ -45,9 +45,9 @@ namespace {
 constexpr int kP = 9;
 constexpr int kRS = kP * kLanes;
 
-// canonical [e][p][k] <-> tiled [tile][k][p][32]
+// canonical [e][p][k] <-> tiled [tile][k][p][L] (L = 16 for fp64, 32 for fp32)
 template <typename T>
-__global__ void to_tiled_kernel(int P, int B, const T* __restrict__ canon, T* __restrict__ tiled,
+__global__ void to_tiled_kernel(int P, int B, int L, const T* __restrict__ canon, T* __restrict__ tiled,
                                 int64_t first, int64_t count) {
   const int64_t n = count * P * B;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -56,11 +56,11 @@ __global__ void to_tiled_kernel(int P, int B, const T* __restrict__ canon, T* __
     const int r = static_cast<int>(i - el * P * B);
     const int p = r / B, k = r - p * B;
     const int64_t e = first + el;
-    tiled[((e / kLanes) * B + k) * P * kLanes + p * kLanes + (e % kLanes)] = canon[i];
+    tiled[((e / L) * B + k) * P * L + p * L + (e % L)] = canon[i];
   }
 }
 template <typename T>
-__global__ void to_canonical_kernel(int P, int B, const T* __restrict__ tiled, T* __restrict__ canon,
+__global__ void to_canonical_kernel(int P, int B, int L, const T* __restrict__ tiled, T* __restrict__ canon,
                                     int64_t first, int64_t count) {
   const int64_t n = count * P * B;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -69,7 +69,7 @@ __global__ void to_canonical_kernel(int P, int B, const T* __restrict__ tiled, T
     const int r = static_cast<int>(i - el * P * B);
     const int p = r / B, k = r - p * B;
     const int64_t e = first + el;
-    canon[i] = tiled[((e / kLanes) * B + k) * P * kLanes + p * kLanes + (e % kLanes)];
+    canon[i] = tiled[((e / L) * B + k) * P * L + p * L + (e % L)];
   }
 }
 
@@ -95,8 +95,8 @@ const void* pick_neigh(int N, int eb) {
   }
   return nullptr;
 }
-// fp64 tensor-core kernels: 12 warps (dmma_impl.cuh kW); fp32 sparse kernels: 9 warps
-int block_threads(int elem_bytes) { return elem_bytes == 8 ? 12 * kLanes : kP * kLanes; }
+// fp64 tensor-core kernels: 6 warps (dmma_impl.cuh kW); fp32 sparse kernels: 9 warps
+int block_threads(int elem_bytes) { return elem_bytes == 8 ? 6 * 32 : kP * kLanes; }
 int nB(int N) { return (N + 1) * (N + 2) * (N + 3) / 6; }
 int nBt(int N) { return (N + 1) * (N + 2) / 2; }
 
@@ -136,9 +136,12 @@ cudaError_t configure_kernels(int N, int eb) {
   if (!fl || !fn) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(fl, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(local_smem_bytes(N, eb)));
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(neigh_smem_bytes(N, eb)));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(neigh_smem_bytes(N, eb)));
+  // all of the unified L1 / shared memory as shared memory (two fp64 CTAs per SM)
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(fl, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  return e;
 }
 
 template <typename T>
@@ -156,17 +159,17 @@ cudaError_t launch_neigh(int N, const StepParams<T>& p, int grid, cudaStream_t s
   return cudaLaunchKernel(f, dim3(grid), dim3(block_threads(sizeof(T))), args, neigh_smem_bytes(N, sizeof(T)), s);
 }
 template <typename T>
-cudaError_t launch_to_tiled(int P, int B, const T* canon, T* tiled, int64_t first, int64_t count,
+cudaError_t launch_to_tiled(int P, int B, int L, const T* canon, T* tiled, int64_t first, int64_t count,
                             cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  to_tiled_kernel<T><<<148 * 8, 256, 0, s>>>(P, B, canon, tiled, first, count);
+  to_tiled_kernel<T><<<148 * 8, 256, 0, s>>>(P, B, L, canon, tiled, first, count);
   return cudaGetLastError();
 }
 template <typename T>
-cudaError_t launch_to_canonical(int P, int B, const T* tiled, T* canon, int64_t first,
+cudaError_t launch_to_canonical(int P, int B, int L, const T* tiled, T* canon, int64_t first,
                                 int64_t count, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  to_canonical_kernel<T><<<148 * 8, 256, 0, s>>>(P, B, tiled, canon, first, count);
+  to_canonical_kernel<T><<<148 * 8, 256, 0, s>>>(P, B, L, tiled, canon, first, count);
   return cudaGetLastError();
 }
 
@@ -174,9 +177,9 @@ template cudaError_t launch_local<double>(int, const StepParams<double>&, int, c
 template cudaError_t launch_local<float>(int, const StepParams<float>&, int, cudaStream_t);
 template cudaError_t launch_neigh<double>(int, const StepParams<double>&, int, cudaStream_t);
 template cudaError_t launch_neigh<float>(int, const StepParams<float>&, int, cudaStream_t);
-template cudaError_t launch_to_tiled<double>(int, int, const double*, double*, int64_t, int64_t, cudaStream_t);
-template cudaError_t launch_to_tiled<float>(int, int, const float*, float*, int64_t, int64_t, cudaStream_t);
-template cudaError_t launch_to_canonical<double>(int, int, const double*, double*, int64_t, int64_t, cudaStream_t);
-template cudaError_t launch_to_canonical<float>(int, int, const float*, float*, int64_t, int64_t, cudaStream_t);
+template cudaError_t launch_to_tiled<double>(int, int, int, const double*, double*, int64_t, int64_t, cudaStream_t);
+template cudaError_t launch_to_tiled<float>(int, int, int, const float*, float*, int64_t, int64_t, cudaStream_t);
+template cudaError_t launch_to_canonical<double>(int, int, int, const double*, double*, int64_t, int64_t, cudaStream_t);
+template cudaError_t launch_to_canonical<float>(int, int, int, const float*, float*, int64_t, int64_t, cudaStream_t);
 
 }  // namespace ydg

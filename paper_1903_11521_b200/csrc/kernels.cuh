@@ -5,12 +5,12 @@
 
 namespace ydg {
 
-constexpr int kLanes = 32;   // elements per tile (one warp = one tile, one quantity column)
+constexpr int kLanes = 32;   // elements per tile of the fp32 kernels (fp64 tensor-core kernels: 16)
 constexpr int kMaxN = 6;
 
 template <typename T>
 struct StepParams {
-  T* Q;                  // [tile][k][p][32]  DOFs (updated in place)
+  T* Q;                  // [tile][k][p][L]  DOFs (updated in place); L = 32 (fp32), 16 (fp64)
   T* traces;             // time-integrated face traces R^iT I: fp32 [tile][face][m][q][32],
                          // fp64 [tile][face][lane][TS] (element-face blocks [m][q])
   const T* star;         // [tile][c][p][3][32]
@@ -31,10 +31,10 @@ cudaError_t launch_local(int N, const StepParams<T>& p, int grid, cudaStream_t s
 template <typename T>
 cudaError_t launch_neigh(int N, const StepParams<T>& p, int grid, cudaStream_t s);
 template <typename T>
-cudaError_t launch_to_tiled(int P, int B, const T* canon, T* tiled, int64_t first, int64_t count,
+cudaError_t launch_to_tiled(int P, int B, int L, const T* canon, T* tiled, int64_t first, int64_t count,
                             cudaStream_t s);
 template <typename T>
-cudaError_t launch_to_canonical(int P, int B, const T* tiled, T* canon, int64_t first,
+cudaError_t launch_to_canonical(int P, int B, int L, const T* tiled, T* canon, int64_t first,
                                 int64_t count, cudaStream_t s);
 size_t local_smem_bytes(int N, int elem_bytes);
 size_t sparse_local_smem(int N, int elem_bytes);

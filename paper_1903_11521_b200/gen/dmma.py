@@ -89,10 +89,10 @@ class Emit:
         self.lines.append(s)
 
 
-def afrag_expr(tid, fbase):
-    """A-fragment load: from the shared-memory fragment buffer (fbase = first table index
-    staged there) or from the global table (L1-cached)."""
-    return f"afrag(x, {tid})" if fbase is None else f"afrag_s(x, {tid - fbase})"
+def afrag_expr(tid, fbase, kind="l"):
+    """A-fragment load: products that may be staged in shared memory (fbase = first table
+    index staged; kind l = local kernel, f = flux kernel) or the global table (L1-cached)."""
+    return f"afrag(x, {tid})" if fbase is None else f"afrag_{kind}(x, {tid}, {tid - fbase})"
 
 
 def plan_xprod(tab, mats, til):
@@ -156,11 +156,11 @@ def emit_gprod(b, tab, M, outs, ins, loader, acc="acc", fbase=None):
     names = {i: [f"g{i}_{j}" for j in range(len(t))] for i, _, t in live}
     if live:
         i0 = live[0][0]
-        b("      const double " + ", ".join(f"{nm} = {afrag_expr(t[1], fbase)}" for nm, t in zip(names[i0], live[0][2])) + ";")
+        b("      const double " + ", ".join(f"{nm} = {afrag_expr(t[1], fbase, 'f')}" for nm, t in zip(names[i0], live[0][2])) + ";")
     for k, (i, ks, tiles) in enumerate(live):
         if k + 1 < len(live):
             i1 = live[k + 1][0]
-            b("      const double " + ", ".join(f"{nm} = {afrag_expr(t[1], fbase)}" for nm, t in zip(names[i1], live[k + 1][2])) + ";")
+            b("      const double " + ", ".join(f"{nm} = {afrag_expr(t[1], fbase, 'f')}" for nm, t in zip(names[i1], live[k + 1][2])) + ";")
         src = loader(i, kset_word(ks))
         b(f"      {{ {src}")
         for (mt, tid), nm in zip(tiles, names[i]):
