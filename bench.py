@@ -44,10 +44,22 @@ BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
 METRIC = BASELINE["metric"]
 UNIT = "element-updates/s"
 
-# FP64 FMA peak derived from the unit counts and clock:
-# 148 SMs x 4 sub-partitions x 16 FP64 FMA lanes x 2 flop x 1.965 GHz
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2
-FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4
+# Roofline denominators.  MEASURED_PEAKS.json holds only bf16 and HBM, so the
+# FP64 / FP32 peaks are this pool's own measurements (tools/peaks.cu -> profiles/peaks_r01.json,
+# seconds-long sustained loops, the figure for a kernel timed inside a long step): FP64 DMMA
+# (the tensor pipe the fp64 kernels run on; DFMA shares it at the same rate) and FP32 FFMA.
+# Fallback: derived from the unit counts and the max clock, 148 SM x 64 FP64 FMA/clk x 2 x
+# 1.965 GHz = 37.2 TF/s and twice that for FP32.
+_PEAKS_FILE = os.path.join(ROOT, "profiles", "peaks_r01.json")
+try:
+    _PK = json.load(open(_PEAKS_FILE))
+    FP64_PEAK_TFLOPS = float(_PK["fp64_dmma_tflops_sustained"])
+    FP32_PEAK_TFLOPS = float(_PK["fp32_fma_tflops_sustained"])
+    PEAK_SOURCE = "of measured: profiles/peaks_r01.json (tools/peaks.cu, sustained)"
+except (OSError, KeyError, ValueError):
+    FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2
+    FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4
+    PEAK_SOURCE = "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"
 
 
 def parse():
@@ -206,7 +218,8 @@ def run_reference(args):
 
 
 def load_traffic(cfg_name):
-    """dram bytes per launch from the committed ncu capture (profiles/ncu_traffic.json)."""
+    """dram bytes (read + write) per launch of each kernel from the committed ncu --set full
+    capture (profiles/ncu_traffic.json: {workload: {kernel: bytes}})."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return {}
@@ -321,25 +334,33 @@ def run_ydg(args):
     peak = FP64_PEAK_TFLOPS if cfg.precision == 8 else FP32_PEAK_TFLOPS
     ach_local = fl_local * nloc / (avg_local / 1e3) / 1e12 if world == 1 else fl_local * nloc / (t_local / args.steps / 1e3) / 1e12
     ach_neigh = fl_neigh * nloc / (avg_neigh / 1e3) / 1e12
-    dominant = "ader_local" if t_local >= t_neigh else "ader_neigh"
+    # kernel names as ncu lists them: fp64 elastic = tensor-core kernels, fp32 = sparse FFMA
+    # kernels, viscoelastic / N=6 fp64 = generic kernels
+    if cfg.P == 27 or (cfg.precision == 8 and cfg.N == 6):
+        k_loc, k_nb, bound = "gen_local", "gen_neigh", "alu"
+    elif cfg.precision == 8:
+        k_loc, k_nb, bound = "dm_local", "dm_flux", "tensor"
+    else:
+        k_loc, k_nb, bound = "ader_local", "ader_neigh", "alu"
+    dominant = k_loc if t_local >= t_neigh else k_nb
     traffic = load_traffic(cfg.name)
-    dom_ach = ach_local if dominant == "ader_local" else ach_neigh
+    dom_ach = ach_local if dominant == k_loc else ach_neigh
     roofline = {
-        "bound": "alu", "achieved": round(dom_ach, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
+        "bound": bound, "achieved": round(dom_ach, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
         "frac": round(dom_ach / peak, 4), "traffic": traffic.get(dominant),
-        "kernel": dominant,
-        "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (tools/peaks.cu measured 36.85 TF/s)",
-        "algorithmic_flops_per_element": fl_local if dominant == "ader_local" else fl_neigh,
+        "kernel": dominant, "peak_source": PEAK_SOURCE,
+        "algorithmic_flops_per_element": fl_local if dominant == k_loc else fl_neigh,
+        "elements_per_launch": nloc,
     }
     kernels = {
-        "ader_local": {"ms_per_launch": round(avg_local, 4), "tflops": round(ach_local, 3),
-                       "frac_fp64_peak": round(ach_local / peak, 4),
-                       "alg_hbm_gbs": round(by_local * nloc / (avg_local / 1e3) / 1e9, 1),
-                       "nz_flops_per_element": fl_local, "alg_bytes_per_element": by_local},
-        "ader_neigh": {"ms_per_launch": round(avg_neigh, 4), "tflops": round(ach_neigh, 3),
-                       "frac_fp64_peak": round(ach_neigh / peak, 4),
-                       "alg_hbm_gbs": round(by_neigh * nloc / (avg_neigh / 1e3) / 1e9, 1),
-                       "nz_flops_per_element": fl_neigh, "alg_bytes_per_element": by_neigh},
+        k_loc: {"ms_per_launch": round(avg_local, 4), "tflops": round(ach_local, 3),
+                "frac_peak": round(ach_local / peak, 4),
+                "alg_hbm_gbs": round(by_local * nloc / (avg_local / 1e3) / 1e9, 1),
+                "nz_flops_per_element": fl_local, "alg_bytes_per_element": by_local},
+        k_nb: {"ms_per_launch": round(avg_neigh, 4), "tflops": round(ach_neigh, 3),
+               "frac_peak": round(ach_neigh / peak, 4),
+               "alg_hbm_gbs": round(by_neigh * nloc / (avg_neigh / 1e3) / 1e9, 1),
+               "nz_flops_per_element": fl_neigh, "alg_bytes_per_element": by_neigh},
     }
     step_roof = peak * 1e12 / nz  # element-updates/s if the whole step ran at the FP64 peak
     cpu = None

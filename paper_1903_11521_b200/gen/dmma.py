@@ -170,6 +170,74 @@ def emit_gprod(b, tab, M, outs, ins, loader, acc="acc", fbase=None):
     return n
 
 
+DFMA_CK_ROWS = 10  # CK steps with at most this many output rows run as sparse DFMA code
+
+
+def emit_ck_dfma(b, d, K, bi, bo, IROWS):
+    """Small CK step as constant-coefficient DFMAs, one thread per data column (element ce,
+    quantity cp): y_k = sum_c sum_l Ktilde^c[k][l] X^c[l], X^c = D A*^cT of the column, only
+    the nonzeros of Ktilde (exact nonzero count; no 8x4 tile padding)."""
+    nz = {}
+    n = 0
+    for c in range(3):
+        for k in range(bo):
+            for l in range(bi):
+                v = -K[c][l][k]
+                if v != 0.0:
+                    nz.setdefault(l, []).append((c, k, v))
+                    n += 1
+    src = "SRC_Q" if d == 0 else "SRC_S"
+    b(f"  // CK step d = {d}: rows in {bi}, rows out {bo}; sparse DFMA ({n} nonzeros)")
+    b(f"  static __device__ __forceinline__ void ck{d}(Ctx& x) {{")
+    b(f"    double y[{bo}];")
+    b(f"    for (int k = 0; k < {bo}; ++k) y[k] = 0.0;")
+    b("    if (x.cc < kRS) {")
+    b("      double ca[9];")
+    b("      int q0, q1, q2;")
+    b("      col_star(x, ca, q0, q1, q2);")
+    for l in sorted(nz):
+        b(f"      {{ double x0, x1, x2; col_x<{src}, B>(x, {l}, ca, q0, q1, q2, x0, x1, x2);")
+        for c, k, v in nz[l]:
+            b(f"        y[{k}] = fma({float(v)!r}, x{c}, y[{k}]);")
+        b("      }")
+    b("    }")
+    b("    __syncthreads();  // every read of D^d done")
+    b(f"    if (x.cc < kRS) col_wb<{1 if d == 0 else 0}, {bo}>(x, y, {d});")
+    if d == 0 and IROWS > bo:
+        b(f"    scale_irows<{bo}, {IROWS}>(x);  // rows of I fed by D^0 only: dt * Q")
+    b("    __syncthreads();")
+    b("  }")
+    return -n  # negative: nonzero FMAs (not tiles)
+
+
+def emit_trace01_dfma(b, R, B, Bt, IROWS, TS):
+    """Traces of the two sparsest faces (0, 1) as constant-coefficient DFMAs, one thread per
+    data column: T_F[m] = sum_k R^F[k][m] I[k] over the nonzeros, both faces from one pass
+    over the column; results go to the two staging blocks [lane][m][q]."""
+    n = 0
+    b("  // traces of faces 0 and 1 (sparse DFMA, one thread per data column)")
+    b("  static __device__ __forceinline__ void trace01(Ctx& x, double* stg0, double* stg1) {")
+    b("    if (x.cc >= kRS) return;")
+    b(f"    double t0[{Bt}], t1[{Bt}];")
+    b(f"    for (int m = 0; m < {Bt}; ++m) t0[m] = t1[m] = 0.0;")
+    for k in range(B):
+        terms = [(F, m, R[F][k][m]) for F in (0, 1) for m in range(Bt) if R[F][k][m] != 0.0]
+        if not terms:
+            continue
+        src = f"x.I[swz({k}, x.cc)]" if k < IROWS else f"x.dt * ld_stream(x.Qt + {k} * kRS + x.cc)"
+        b(f"    {{ const double ik = {src};")
+        for F, m, v in terms:
+            b(f"      t{F}[{m}] = fma({float(v)!r}, ik, t{F}[{m}]);")
+            n += 1
+        b("    }")
+    b(f"    for (int m = 0; m < {Bt}; ++m) {{")
+    b(f"      stg0[x.ce * {TS} + m * kP + x.cp] = t0[m];")
+    b(f"      stg1[x.ce * {TS} + m * kP + x.cp] = t1[m];")
+    b("    }")
+    b("  }")
+    return n
+
+
 def gen_order(N):
     t = tables.load(N)
     K, R, f = t["K"], t["R"], t["f"]
@@ -193,6 +261,9 @@ def gen_order(N):
         tl = til[f"ck{d}"]
         MT = len(tl["out"])
         mats = [(lambda r, col, c=c: -K[c][col][r]) for c in range(3)]  # Kt^c[r][col] = -K^c[col][r]
+        if bo <= DFMA_CK_ROWS:
+            counts[f"ck{d}"] = emit_ck_dfma(b, d, K, bi, bo, IROWS)
+            continue
         b(f"  // CK step d = {d}: rows in {bi}, rows out {bo}")
         b(f"  static __device__ __forceinline__ void ck{d}(Ctx& x) {{")
         b(f"    double acc[{MT}][kU][2];")
@@ -232,6 +303,7 @@ def gen_order(N):
     b("    add_q<" + str(QMT) + ", IROWS>(x, Qt, acc, w, Qs);")
     b("  }")
     # ---------------- traces T_i = R^iT I
+    counts["tr01_dfma"] = emit_trace01_dfma(b, R, B, Bt, IROWS, TS)
     b(f"  // trace: T_F = R^FT I (rows < IROWS of I from shared memory, dt * Q from global memory);")
     b(f"  // the C fragments go to the staging block [lane][m][q] (stride TS)")
     b(f"  template <int F> static __device__ __forceinline__ void trace(Ctx& x, double* stg) {{")
@@ -293,6 +365,7 @@ def gen_order(N):
         b("    }")
     b("  }")
     regions["LIFT"] = (lift0, len(tab.frags))
+    regions.setdefault("CK0", (0, 0))  # CK step 0 ran as sparse DFMA code
     # ---------------- neighbour orientation z = f^h t, uniform over lanes:
     # f^1 = S (diagonal +-1) and f^2 = S f^0 S, so t' = (h != 0 ? S t : t), u = f^0 t',
     # z = (h == 1 ? t' : (h == 2 ? S u : u))
@@ -341,6 +414,13 @@ def gen_order(N):
         lines.append("  " + ", ".join(repr(float(v)) if v != 0 else "0.0" for v in flat[s:s + 8]) + ",")
     lines.append("};")
     lines.append(f"template <> __device__ __forceinline__ const double* frag_table<{N}>() {{ return frag_N{N}; }}")
+    # dense neighbour-orientation matrices f^h, h = 0..2 (block-diagonal by face degree)
+    lines.append(f"__device__ const double fh_N{N}[{3 * Bt * Bt}] = {{")
+    flat = [float(f[h][m][n]) for h in range(3) for m in range(Bt) for n in range(Bt)]
+    for s0 in range(0, len(flat), 8):
+        lines.append("  " + ", ".join(repr(v) if v != 0 else "0.0" for v in flat[s0:s0 + 8]) + ",")
+    lines.append("};")
+    lines.append(f"template <> __device__ __forceinline__ const double* fh_table<{N}>() {{ return fh_N{N}; }}")
     lines.append("}  // namespace dm")
     lines.append("}  // namespace ydg")
     return "\n".join(lines) + "\n", counts
