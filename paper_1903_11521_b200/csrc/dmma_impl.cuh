@@ -417,7 +417,7 @@ struct Layout {
   static constexpr int LOCAL = FOFF + FSMAX * 32 + 2;  // + two mbarriers
   // flux kernel: own face block, two neighbour face blocks, Y rows, lift fragments, four
   // mbarriers
-  static constexpr int FLUX = 3 * FACE + G::Bt * kRS + 3 * G::Bt * G::Bt + (kFluxFs ? G::LIFT_NF * 32 : 0) + 4;
+  static constexpr int FLUX = 3 * FACE + G::Bt * kRS + kFaceCoeffs * kL + 16 + 3;  // + slots, j|h, mbarriers
 };
 
 // ---- asynchronous copy helpers (TMA bulk copies + mbarrier, Ampere-style cp.async)
@@ -635,58 +635,64 @@ __global__ void __launch_bounds__(kT, 2) dm_flux(const __grid_constant__ StepPar
   using G = DG<N>;
   using Lay = Layout<N>;
   constexpr int B = G::B, Bt = G::Bt, TS = G::TS, FACE = Lay::FACE;
+  constexpr int FCN = kFaceCoeffs * kL;  // factored flux solvers of one (tile, face)
   extern __shared__ __align__(128) double smem[];
   double* O = smem;                    // own face block [lane][TS]
   double* NB = smem + FACE;            // [2][lane][TS] neighbour face blocks
   double* Y = smem + 3 * FACE;         // [Bt][144] mixed face values
-  double* FH = Y + Bt * kRS;           // [3][Bt][Bt] neighbour orientation matrices f^h
-  double* FS = FH + 3 * Bt * Bt;       // the lift's A fragments (if kFluxFs)
-  unsigned long long* bar =
-      reinterpret_cast<unsigned long long*>(FS + (kFluxFs ? G::LIFT_NF * 32 : 0));  // own, nb0, nb1, fs
+  double* FC = Y + Bt * kRS;           // [12][16] flux coefficients of the current item
+  int32_t* NBX = reinterpret_cast<int32_t*>(FC + FCN);  // [16] neighbour slots of the next item
+  int8_t* JH = reinterpret_cast<int8_t*>(NBX + kL);     // [16] j | h << 2 of the current item
+  int8_t* JHX = JH + kL;                                // [16] j | h << 2 of the next item
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(JHX + kL);  // own, nb0, nb1
   Ctx x;
   init_ctx(x);
   x.frags = frag_table<N>();
-  x.fs = FS;
-  x.fbar = &bar[3];
   if (blockIdx.x >= prm.ntiles) return;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     mbar_init(&bar[2], 1);
-    mbar_init(&bar[3], 1);
-    if (kFluxFs) stage_frags<N>(x, G::LIFT_F0, G::LIFT_NF);
   }
-  for (int i = threadIdx.x; i < 3 * Bt * Bt; i += kT) FH[i] = fh_table<N>()[i];
   __syncthreads();
-  // thread 0 issues the TMA copies: the tile's own face block, one block per element for
-  // the neighbour faces
-  auto issue_own = [&](int64_t tile, int F) {
-    mbar_expect_tx(&bar[0], FACE * sizeof(double));
-    bulk_g2s(O, prm.traces + (tile * 4 + F) * FACE, FACE * sizeof(double), &bar[0]);
+  // Items k = (tile, face) in this CTA's order; item k's "own" copy (thread 0) brings the
+  // tile's face block, its flux coefficients and j|h, and the neighbour slots and j|h of
+  // item k+1, so no global load sits on the per-face critical path.
+  auto issue_own = [&](int64_t tile, int F, int64_t ntile, int nF, bool next) {
+    const int64_t item = tile * 4 + F, nitem = ntile * 4 + nF;
+    mbar_expect_tx(&bar[0], (FACE + FCN) * sizeof(double) + kL + (next ? kL * 5 : 0));  // + j|h, slots
+    bulk_g2s(O, prm.traces + item * FACE, FACE * sizeof(double), &bar[0]);
+    bulk_g2s(FC, prm.aplus + item * FCN, FCN * sizeof(double), &bar[0]);
+    bulk_g2s(JH, prm.jh + item * kL, kL, &bar[0]);
+    if (next) {
+      bulk_g2s(NBX, prm.nb + nitem * kL, kL * sizeof(int32_t), &bar[0]);
+      bulk_g2s(JHX, prm.jh + nitem * kL, kL, &bar[0]);
+    }
   };
-  auto issue_nb = [&](int64_t tile, int F, int b) {
+  auto issue_nb = [&](int b, const int32_t* nbs, const int8_t* jhs) {  // thread 0
     mbar_expect_tx(&bar[1 + b], FACE * sizeof(double));
-    int64_t nbe[kL];
-    int jj[kL];
 #pragma unroll
     for (int e = 0; e < kL; ++e) {
-      const int64_t slot = (tile * 4 + F) * kL + e;
-      nbe[e] = prm.nb[slot];
-      jj[e] = prm.jh[slot] & 3;
-    }
-#pragma unroll
-    for (int e = 0; e < kL; ++e)
-      bulk_g2s(NB + b * FACE + e * TS, prm.traces + ((nbe[e] / kL) * 4 + jj[e]) * FACE + (nbe[e] % kL) * TS,
+      const int64_t nbe = nbs[e];
+      bulk_g2s(NB + b * FACE + e * TS, prm.traces + ((nbe / kL) * 4 + (jhs[e] & 3)) * FACE + (nbe % kL) * TS,
                TS * sizeof(double), &bar[1 + b]);
+    }
   };
+  const int64_t t0 = prm.tile0 + blockIdx.x;
   if (threadIdx.x == 0) {
-    issue_own(prm.tile0 + blockIdx.x, 0);
-    issue_nb(prm.tile0 + blockIdx.x, 0, 0);
+    int32_t nbs[kL];
+    int8_t jhs[kL];
+#pragma unroll
+    for (int e = 0; e < kL; ++e) {
+      nbs[e] = prm.nb[t0 * 4 * kL + e];
+      jhs[e] = prm.jh[t0 * 4 * kL + e];
+    }
+    issue_nb(0, nbs, jhs);
+    issue_own(t0, 0, t0, 1, true);
   }
   unsigned ph_o = 0, ph_n0 = 0, ph_n1 = 0;
-  if constexpr (kFluxFs) mbar_wait(x.fbar, 0);
   // thread roles: rotation (element re, column rp) for threads < 144; Godunov rows
-  // m = gm + 12 i of element ge
+  // m = rp + 12 i of element re
   const int re = threadIdx.x % kL, rp = threadIdx.x / kL;
   for (int64_t it = blockIdx.x; it < prm.ntiles; it += gridDim.x) {
     const int64_t tile = prm.tile0 + it;
@@ -695,17 +701,16 @@ __global__ void __launch_bounds__(kT, 2) dm_flux(const __grid_constant__ StepPar
     for (int F = 0; F < 4; ++F) {
       const int b = F & 1;
       __syncthreads();  // lift of the previous face done: Y and neighbour buffer b ^ 1 are free
+      mbar_wait(&bar[0], ph_o);  // own block, coefficients, j|h of this item; slots of the next
+      ph_o ^= 1;
+      const bool has_next = F < 3 || more;
       if (threadIdx.x == 0) {
-        if (F < 3) issue_nb(tile, F + 1, b ^ 1);
-        else if (more) issue_nb(tile + gridDim.x, 0, b ^ 1);
-      } else if (threadIdx.x == 32) {  // next item's flux coefficients (and next tile's Q) -> L2
-        const int64_t nt = F < 3 ? tile : tile + gridDim.x;
-        const int nF = F < 3 ? F + 1 : 0;
-        if (F < 3 || more) prefetch_l2(prm.aplus + (nt * 4 + nF) * kFaceCoeffs * kL, kFaceCoeffs * kL * sizeof(double));
-        if (F == 3 && more) prefetch_l2(prm.Q + nt * B * kRS, B * kRS * sizeof(double));
+        if (has_next) issue_nb(b ^ 1, NBX, JHX);
+      } else if (threadIdx.x == 32 && F == 3 && more) {  // next tile's Q -> L2
+        prefetch_l2(prm.Q + (tile + gridDim.x) * B * kRS, B * kRS * sizeof(double));
       }
       double* Zb = NB + b * FACE;
-      const int h = prm.jh[(tile * 4 + F) * kL + re] >> 2;
+      const int h = JH[re] >> 2;
       if (b == 0) {
         mbar_wait(&bar[1], ph_n0);
         ph_n0 ^= 1;
@@ -713,48 +718,36 @@ __global__ void __launch_bounds__(kT, 2) dm_flux(const __grid_constant__ StepPar
         mbar_wait(&bar[2], ph_n1);
         ph_n1 ^= 1;
       }
-      // flux solvers of this face, factored (setup.h kFaceCoeffs): element re's
+      if (threadIdx.x < kP * kL) {  // z = f^h t on column rp of element re's neighbour block
+        double* z = Zb + re * TS + rp;
+        double t[Bt];
+#pragma unroll
+        for (int n = 0; n < Bt; ++n) t[n] = z[n * kP];
+        G::rot(h, t, z);
+      }
       double fc[kFaceCoeffs];
 #pragma unroll
-      for (int k = 0; k < kFaceCoeffs; ++k) fc[k] = prm.aplus[((tile * 4 + F) * kFaceCoeffs + k) * kL + re];
-      mbar_wait(&bar[0], ph_o);
-      ph_o ^= 1;
+      for (int k = 0; k < kFaceCoeffs; ++k) fc[k] = FC[k * kL + re];
+      __syncthreads();  // rotated neighbour columns visible
       {
-        // per (element re, row m): z = (f^h t)_m over the degree block of m (f^h is
-        // block-diagonal by face degree; rows of degree d are d(d+1)/2 .. (d+1)(d+2)/2-1),
-        // then the Godunov flux of row m from the own row T_m and z
         const double* T = O + re * TS;
-        const double* Zr = Zb + re * TS;
-        const double* fr0 = FH + h * Bt * Bt;
+        const double* Z = Zb + re * TS;
 #pragma unroll
         for (int i = 0; i < (Bt + kT / kL - 1) / (kT / kL); ++i) {  // rows m = rp, rp + 12, ...
           const int m = rp + (kT / kL) * i;
           if (m >= Bt) break;
-          int d = 0;
-          while ((d + 1) * (d + 2) / 2 <= m) ++d;
-          const int n0 = d * (d + 1) / 2;
-          const double* fr = fr0 + m * Bt + n0;
-          double z[kP];
-#pragma unroll
-          for (int q = 0; q < kP; ++q) z[q] = 0.0;
-#pragma unroll
-          for (int k = 0; k <= N; ++k) {
-            if (k > d) break;
-            const double c = fr[k];
-            const double* tn = Zr + (n0 + k) * kP;
-#pragma unroll
-            for (int q = 0; q < kP; ++q) z[q] = fma(c, tn[q], z[q]);
-          }
           double y[kP];
-          godunov_flux(T + m * kP, z, fc, y);
+          godunov_flux(T + m * kP, Z + m * kP, fc, y);
 #pragma unroll
           for (int q = 0; q < kP; ++q) Y[swz(m, q * kL + re)] = y[q];
         }
       }
-      __syncthreads();  // every read of O done; Y complete
-      if (threadIdx.x == 0) {
-        if (F < 3) issue_own(tile, F + 1);
-        else if (more) issue_own(tile + gridDim.x, 0);
+      __syncthreads();  // every read of O, FC, JH, NBX done; Y complete
+      if (threadIdx.x == 0 && has_next) {  // item k+1's own copy (and item k+2's slots)
+        const int64_t nt = F < 3 ? tile : tile + gridDim.x;
+        const int nF = F < 3 ? F + 1 : 0;
+        const bool nn = nF < 3 || nt + gridDim.x < prm.tile0 + prm.ntiles;
+        issue_own(nt, nF, nF < 3 ? nt : nt + gridDim.x, nF < 3 ? nF + 1 : 0, nn);
       }
       // lift and Q update per face, two m-tiles at a time; the tile's Q stays in L2
       // across its four updates
