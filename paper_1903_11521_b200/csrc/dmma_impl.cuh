@@ -417,7 +417,7 @@ struct Layout {
   static constexpr int LOCAL = FOFF + FSMAX * 32 + 2;  // + two mbarriers
   // flux kernel: own face block, two neighbour face blocks, Y rows, lift fragments, four
   // mbarriers
-  static constexpr int FLUX = 3 * FACE + G::Bt * kRS + kFaceCoeffs * kL + 16 + 3;  // + slots, j|h, mbarriers
+  static constexpr int FLUX = 2 * FACE + 2 * G::Bt * kRS + kFaceCoeffs * kL + 16 + 2;  // + slots, j|h, mbarriers
 };
 
 // ---- asynchronous copy helpers (TMA bulk copies + mbarrier, Ampere-style cp.async)
@@ -638,13 +638,13 @@ __global__ void __launch_bounds__(kT, 2) dm_flux(const __grid_constant__ StepPar
   constexpr int FCN = kFaceCoeffs * kL;  // factored flux solvers of one (tile, face)
   extern __shared__ __align__(128) double smem[];
   double* O = smem;                    // own face block [lane][TS]
-  double* NB = smem + FACE;            // [2][lane][TS] neighbour face blocks
-  double* Y = smem + 3 * FACE;         // [Bt][144] mixed face values
-  double* FC = Y + Bt * kRS;           // [12][16] flux coefficients of the current item
+  double* NB = smem + FACE;            // [lane][TS] neighbour face blocks
+  double* Y0 = smem + 2 * FACE;        // [2][Bt][144]: rotated neighbour rows, then the flux
+  double* FC = Y0 + 2 * Bt * kRS;      // [12][16] flux coefficients of the current item
   int32_t* NBX = reinterpret_cast<int32_t*>(FC + FCN);  // [16] neighbour slots of the next item
   int8_t* JH = reinterpret_cast<int8_t*>(NBX + kL);     // [16] j | h << 2 of the current item
   int8_t* JHX = JH + kL;                                // [16] j | h << 2 of the next item
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(JHX + kL);  // own, nb0, nb1
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(JHX + kL);  // own, nb
   Ctx x;
   init_ctx(x);
   x.frags = frag_table<N>();
@@ -652,7 +652,6 @@ __global__ void __launch_bounds__(kT, 2) dm_flux(const __grid_constant__ StepPar
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
-    mbar_init(&bar[2], 1);
   }
   __syncthreads();
   // Items k = (tile, face) in this CTA's order; item k's "own" copy (thread 0) brings the
@@ -669,13 +668,13 @@ __global__ void __launch_bounds__(kT, 2) dm_flux(const __grid_constant__ StepPar
       bulk_g2s(JHX, prm.jh + nitem * kL, kL, &bar[0]);
     }
   };
-  auto issue_nb = [&](int b, const int32_t* nbs, const int8_t* jhs) {  // thread 0
-    mbar_expect_tx(&bar[1 + b], FACE * sizeof(double));
+  auto issue_nb = [&](const int32_t* nbs, const int8_t* jhs) {  // thread 0
+    mbar_expect_tx(&bar[1], FACE * sizeof(double));
 #pragma unroll
     for (int e = 0; e < kL; ++e) {
       const int64_t nbe = nbs[e];
-      bulk_g2s(NB + b * FACE + e * TS, prm.traces + ((nbe / kL) * 4 + (jhs[e] & 3)) * FACE + (nbe % kL) * TS,
-               TS * sizeof(double), &bar[1 + b]);
+      bulk_g2s(NB + e * TS, prm.traces + ((nbe / kL) * 4 + (jhs[e] & 3)) * FACE + (nbe % kL) * TS,
+               TS * sizeof(double), &bar[1]);
     }
   };
   const int64_t t0 = prm.tile0 + blockIdx.x;
@@ -687,10 +686,10 @@ __global__ void __launch_bounds__(kT, 2) dm_flux(const __grid_constant__ StepPar
       nbs[e] = prm.nb[t0 * 4 * kL + e];
       jhs[e] = prm.jh[t0 * 4 * kL + e];
     }
-    issue_nb(0, nbs, jhs);
+    issue_nb(nbs, jhs);
     issue_own(t0, 0, t0, 1, true);
   }
-  unsigned ph_o = 0, ph_n0 = 0, ph_n1 = 0;
+  unsigned ph_o = 0, ph_n = 0;
   // thread roles: rotation (element re, column rp) for threads < 144; Godunov rows
   // m = rp + 12 i of element re
   const int re = threadIdx.x % kL, rp = threadIdx.x / kL;
@@ -699,50 +698,44 @@ __global__ void __launch_bounds__(kT, 2) dm_flux(const __grid_constant__ StepPar
     const bool more = it + gridDim.x < prm.ntiles;
 #pragma unroll
     for (int F = 0; F < 4; ++F) {
-      const int b = F & 1;
-      __syncthreads();  // lift of the previous face done: Y and neighbour buffer b ^ 1 are free
+      // Y buffer F & 1: last read by the lift of face F-2, which every warp finished before
+      // the barriers of face F-1
+      double* Y = Y0 + (F & 1) * Bt * kRS;
+      const bool has_next = F < 3 || more;
       mbar_wait(&bar[0], ph_o);  // own block, coefficients, j|h of this item; slots of the next
       ph_o ^= 1;
-      const bool has_next = F < 3 || more;
-      if (threadIdx.x == 0) {
-        if (has_next) issue_nb(b ^ 1, NBX, JHX);
-      } else if (threadIdx.x == 32 && F == 3 && more) {  // next tile's Q -> L2
-        prefetch_l2(prm.Q + (tile + gridDim.x) * B * kRS, B * kRS * sizeof(double));
-      }
-      double* Zb = NB + b * FACE;
-      const int h = JH[re] >> 2;
-      if (b == 0) {
-        mbar_wait(&bar[1], ph_n0);
-        ph_n0 ^= 1;
-      } else {
-        mbar_wait(&bar[2], ph_n1);
-        ph_n1 ^= 1;
-      }
-      if (threadIdx.x < kP * kL) {  // z = f^h t on column rp of element re's neighbour block
-        double* z = Zb + re * TS + rp;
+      mbar_wait(&bar[1], ph_n);  // neighbour blocks of this item
+      ph_n ^= 1;
+      if (threadIdx.x < kP * kL) {  // z = f^h t on column rp of element re's neighbour block -> Y
+        const int h = JH[re] >> 2;
+        const double* zc = NB + re * TS + rp;
         double t[Bt];
 #pragma unroll
-        for (int n = 0; n < Bt; ++n) t[n] = z[n * kP];
-        G::rot(h, t, z);
+        for (int n = 0; n < Bt; ++n) t[n] = zc[n * kP];
+        G::rot(h, t, Y, rp * kL + re);
       }
       double fc[kFaceCoeffs];
 #pragma unroll
       for (int k = 0; k < kFaceCoeffs; ++k) fc[k] = FC[k * kL + re];
-      __syncthreads();  // rotated neighbour columns visible
-      {
+      __syncthreads();  // rotated rows visible; every read of NB (and of NBX, JHX) done
+      if (threadIdx.x == 0 && has_next) issue_nb(NBX, JHX);
+      else if (threadIdx.x == 32 && F == 3 && more)  // next tile's Q -> L2
+        prefetch_l2(prm.Q + (tile + gridDim.x) * B * kRS, B * kRS * sizeof(double));
+      {  // Godunov flux of rows m = rp, rp + 12, ... of element re, in place in Y
         const double* T = O + re * TS;
-        const double* Z = Zb + re * TS;
 #pragma unroll
-        for (int i = 0; i < (Bt + kT / kL - 1) / (kT / kL); ++i) {  // rows m = rp, rp + 12, ...
+        for (int i = 0; i < (Bt + kT / kL - 1) / (kT / kL); ++i) {
           const int m = rp + (kT / kL) * i;
           if (m >= Bt) break;
-          double y[kP];
-          godunov_flux(T + m * kP, Z + m * kP, fc, y);
+          double z[kP], y[kP];
+#pragma unroll
+          for (int q = 0; q < kP; ++q) z[q] = Y[swz(m, q * kL + re)];
+          godunov_flux(T + m * kP, z, fc, y);
 #pragma unroll
           for (int q = 0; q < kP; ++q) Y[swz(m, q * kL + re)] = y[q];
         }
       }
-      __syncthreads();  // every read of O, FC, JH, NBX done; Y complete
+      __syncthreads();  // every read of O, FC, JH done; Y complete
       if (threadIdx.x == 0 && has_next) {  // item k+1's own copy (and item k+2's slots)
         const int64_t nt = F < 3 ? tile : tile + gridDim.x;
         const int nF = F < 3 ? F + 1 : 0;

@@ -375,8 +375,8 @@ def gen_order(N):
             assert (m == n) or f[1][m][n] == 0.0
             assert abs(f[2][m][n] - S[m] * f[0][m][n] * S[n]) < 1e-14
     b("  // z = f^h t (P:1342) for every lane's own h, without divergence (f^1 = S diagonal,")
-    b("  // f^2 = S f^0 S); z[m * kP] receives row m")
-    b(f"  static __device__ __forceinline__ void rot(int h, double (&t)[{Bt}], double* z) {{")
+    b("  // f^2 = S f^0 S); row m goes to Y[m][col] (swizzled rows of the flux staging)")
+    b(f"  static __device__ __forceinline__ void rot(int h, double (&t)[{Bt}], double* Y, int col) {{")
     b("    const bool fl = h != 0, id = h == 1, s2 = h == 2;")
     for n in range(Bt):
         if S[n] < 0:
@@ -388,9 +388,9 @@ def gen_order(N):
             expr = f"{float(v)!r} * t[{n}]" if expr is None else f"fma({float(v)!r}, t[{n}], {expr})"
         b(f"    {{ const double u = {expr or '0.0'};")
         if S[m] < 0:
-            b(f"      z[{m} * kP] = id ? t[{m}] : (s2 ? -u : u); }}")
+            b(f"      Y[swz({m}, col)] = id ? t[{m}] : (s2 ? -u : u); }}")
         else:
-            b(f"      z[{m} * kP] = id ? t[{m}] : u; }}")
+            b(f"      Y[swz({m}, col)] = id ? t[{m}] : u; }}")
     b("  }")
     lines = [f"// GENERATED by paper_1903_11521_b200/gen/dmma.py for N = {N} -- do not edit.",
              "#pragma once", "namespace ydg {", "namespace dm {", f"template <> struct DG<{N}> {{",
