@@ -241,21 +241,31 @@ __device__ __forceinline__ void scale_irows(Ctx& x) {
 // Q loads are all issued before its stores (one L2/HBM latency per batch, bounded register
 // use), values are added into the accumulators, then stored (16-byte, two elements).
 // Qs: rows < IR of Q^n already in shared memory (plain [row][288] layout), else nullptr
+template <int MT, int IR>
+__device__ __forceinline__ void q_batch(const Ctx& x, const double* Qt, const double* Qs,
+                                        const unsigned long long (&w)[MT], int m0, double2 (&v)[2][kU]) {
+#pragma unroll
+  for (int k2 = 0; k2 < 2; ++k2) {
+    const int row = m0 + k2 < MT ? mrow(x, w[m0 + k2 < MT ? m0 + k2 : 0]) : 0xff;
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      if (row == 0xff) v[k2][k] = make_double2(0.0, 0.0);
+      else if (row < IR) v[k2][k] = *reinterpret_cast<const double2*>(Qs + row * kRS + ccol(x, k));
+      else v[k2][k] = *reinterpret_cast<const double2*>(Qt + row * kRS + ccol(x, k));
+    }
+  }
+}
+// Q += acc over all m-tiles (rows from the words w[]; rows < IR of Q^n are read from the
+// shared copy Qs), two m-tiles per batch, software-pipelined: the next batch's Q loads are
+// issued before the current batch's stores (one memory latency in total, bounded registers).
 template <int MT, int IR = 0>
 __device__ __forceinline__ void add_q(const Ctx& x, double* Qt, double (&acc)[MT][kU][2],
                                       const unsigned long long (&w)[MT], const double* Qs = nullptr) {
+  double2 vc[2][kU], vn[2][kU];
+  q_batch<MT, IR>(x, Qt, Qs, w, 0, vc);
 #pragma unroll
   for (int m0 = 0; m0 < MT; m0 += 2) {
-    double2 v[2][kU];
-#pragma unroll
-    for (int k2 = 0; k2 < 2; ++k2) {
-      const int row = m0 + k2 < MT ? mrow(x, w[m0 + k2 < MT ? m0 + k2 : 0]) : 0xff;
-#pragma unroll
-      for (int k = 0; k < kU; ++k)
-        v[k2][k] = row == 0xff ? make_double2(0.0, 0.0)
-                   : (row < IR ? *reinterpret_cast<const double2*>(Qs + row * kRS + ccol(x, k))
-                               : *reinterpret_cast<const double2*>(Qt + row * kRS + ccol(x, k)));
-    }
+    if (m0 + 2 < MT) q_batch<MT, IR>(x, Qt, Qs, w, m0 + 2, vn);
 #pragma unroll
     for (int k2 = 0; k2 < 2; ++k2) {
       if (m0 + k2 >= MT) continue;
@@ -264,7 +274,13 @@ __device__ __forceinline__ void add_q(const Ctx& x, double* Qt, double (&acc)[MT
 #pragma unroll
       for (int k = 0; k < kU; ++k)
         *reinterpret_cast<double2*>(Qt + row * kRS + ccol(x, k)) =
-            make_double2(acc[m0 + k2][k][0] + v[k2][k].x, acc[m0 + k2][k][1] + v[k2][k].y);
+            make_double2(acc[m0 + k2][k][0] + vc[k2][k].x, acc[m0 + k2][k][1] + vc[k2][k].y);
+    }
+    if (m0 + 2 < MT) {
+#pragma unroll
+      for (int k2 = 0; k2 < 2; ++k2)
+#pragma unroll
+        for (int k = 0; k < kU; ++k) vc[k2][k] = vn[k2][k];
     }
   }
 }

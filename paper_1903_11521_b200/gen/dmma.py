@@ -220,11 +220,16 @@ def emit_trace01_dfma(b, R, B, Bt, IROWS, TS):
     b("    if (x.cc >= kRS) return;")
     b(f"    double t0[{Bt}], t1[{Bt}];")
     b(f"    for (int m = 0; m < {Bt}; ++m) t0[m] = t1[m] = 0.0;")
-    for k in range(B):
+    gk = [k for k in range(IROWS, B) if any(R[F][k][m] != 0.0 for F in (0, 1) for m in range(Bt))]
+    if gk:  # rows >= IROWS (dt * Q, global memory): all loads first, latency under the smem rows
+        b(f"    double qg[{len(gk)}];")
+        for i, k in enumerate(gk):
+            b(f"    qg[{i}] = ld_stream(x.Qt + {k} * kRS + x.cc);")
+    for k in list(range(IROWS)) + gk:
         terms = [(F, m, R[F][k][m]) for F in (0, 1) for m in range(Bt) if R[F][k][m] != 0.0]
         if not terms:
             continue
-        src = f"x.I[swz({k}, x.cc)]" if k < IROWS else f"x.dt * ld_stream(x.Qt + {k} * kRS + x.cc)"
+        src = f"x.I[swz({k}, x.cc)]" if k < IROWS else f"x.dt * qg[{gk.index(k)}]"
         b(f"    {{ const double ik = {src};")
         for F, m, v in terms:
             b(f"      t{F}[{m}] = fma({float(v)!r}, ik, t{F}[{m}]);")
