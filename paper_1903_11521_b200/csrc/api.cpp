@@ -35,7 +35,7 @@ struct ydg_solver {
   bool have_mesh = false;
   int64_t ne = 0, first = 0, nlocal = 0;
   int64_t nslots = 0;   // local element slots incl. ghosts (multiple of lanes)
-  int lanes = 32;       // elements per tile: 16 (fp64 tensor-core kernels) or 32 (fp32)
+  int lanes = 32;       // elements per tile: kDmLanes (fp64 tensor-core kernels) or 32 (fp32)
   int64_t ntiles = 0;   // owned tiles
   Neighbours nbr;       // global tables (for ydg_get_neighbours)
   // device buffers
@@ -567,13 +567,15 @@ int ydg_upload_mesh(ydg_solver* h, int64_t ne, const double* xyz, const int64_t*
     h->have_mesh = true;
     return YDG_OK;
   }
-  h->lanes = h->prec == 8 ? 16 : 32;
+  h->lanes = h->prec == 8 ? kDmLanes : 32;
   const int kLanes = h->lanes;
   h->ntiles = (h->nlocal + kLanes - 1) / kLanes;
   // local slots: owned [0, nlocal) padded to tiles, then ghosts
   std::vector<int64_t> ghost_of;  // global element id of each ghost slot
   std::vector<int32_t> nb_local(static_cast<size_t>(h->ntiles) * kLanes * 4, 0);
-  std::vector<int8_t> jh_local(nb_local.size(), 0);
+  // j | h << 2 per (tile, face): kLanes bytes, padded to 16 (TMA granularity) for fp64 tiles
+  const int jh_stride = kLanes < 16 ? 16 : kLanes;
+  std::vector<int8_t> jh_local(static_cast<size_t>(h->ntiles) * 4 * jh_stride, 0);
   int64_t owned_slots = h->ntiles * kLanes;
   std::vector<int64_t> boundary;  // owned tiles with ghosts
   if (h->nranks > 1) {
@@ -608,7 +610,7 @@ int ydg_upload_mesh(ydg_solver* h, int64_t ne, const double* xyz, const int64_t*
         }
         if (slot > INT32_MAX) return fail(h, YDG_ERR_UNSUPPORTED, "more than 2^31 local elements");
         nb_local[dst] = static_cast<int32_t>(slot);
-        jh_local[dst] = static_cast<int8_t>(h->nbr.j[g * 4 + i] | (h->nbr.h[g * 4 + i] << 2));
+        jh_local[(tile * 4 + i) * jh_stride + lane] = static_cast<int8_t>(h->nbr.j[g * 4 + i] | (h->nbr.h[g * 4 + i] << 2));
       }
     }
     // Tiles with ghost neighbours are launched before the interior so their traces can be
@@ -646,8 +648,8 @@ int ydg_upload_mesh(ydg_solver* h, int64_t ne, const double* xyz, const int64_t*
   // grids: resident CTAs per SM x SMs
   int sms = 0, occ_l = 0, occ_n = 0;
   CUDA_OR_FAIL(h, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->dev));
-  occ_l = eb == 8 ? 2 : 1;  // fp64: two 6-warp CTAs of 16-element tiles per SM
-  occ_n = eb == 8 ? 2 : 1;
+  occ_l = eb == 8 ? kDmCtasPerSm : 1;  // fp64: 12 warps per SM in kDmCtasPerSm CTAs
+  occ_n = eb == 8 ? kDmCtasPerSm : 1;
   h->grid_local = sms * occ_l;
   h->grid_neigh = sms * occ_n;
   h->have_mesh = true;

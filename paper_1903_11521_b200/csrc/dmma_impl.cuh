@@ -2,11 +2,11 @@
 //
 // Data of a 32-element tile live in shared memory as [row][col] with col = p*32 + e
 // (quantity-major), rows swizzled (col ^ 8*(row & 1)) so that the 4-row x 8-column DMMA
-// B-fragment loads take the minimum two wavefronts.  A tile is 16 elements; a CTA has 6
-// warps and two CTAs share an SM, so each SM sub-partition runs three warps (equal load on
-// the four tensor pipes) and one CTA's barriers, memory phases and latency chains overlap
-// the other's DMMAs.  Warp w owns the 8-column tiles (quantity 3g + k, elements
-// 8ct..8ct+7), k = 0..2, with g = w / 2, ct = w % 2 -- its "units".  Every B operand a warp feeds to a
+// B-fragment loads take the minimum two wavefronts.  A tile is kL = 8 (or 16) elements; a
+// CTA has 3 (6) warps and 4 (2) CTAs share an SM, so each SM sub-partition runs three warps
+// (equal load on the four tensor pipes) and one CTA's barriers, memory phases and latency
+// chains overlap the others' DMMAs.  Warp w owns the 8-column tiles (quantity 3g + k,
+// elements 8ct..8ct+7), k = 0..2, with g = w / kCT, ct = w % kCT -- its "units".  Every B operand a warp feeds to a
 // DMMA is warp-private; only the per-element quantity mixing (star matrices A*, flux
 // solvers) reads other warps' columns.  Global matrices are the DMMA A operands:
 // generated 8x4 tiles over freely grouped rows (gen/dmma.py, gen/tiling.py).
@@ -22,9 +22,11 @@ namespace ydg {
 namespace dm {
 
 constexpr int kP = 9;
-constexpr int kL = 16;         // elements per tile (HBM layouts of the fp64 path use the same)
-constexpr int kRS = kP * kL;   // 144 columns per row
-constexpr int kW = 6;          // warps per CTA (two CTAs per SM: 3 warps per sub-partition)
+constexpr int kL = kDmLanes;   // elements per tile (HBM layouts of the fp64 path use the same)
+constexpr int kRS = kP * kL;   // columns per row
+constexpr int kCT = kL / 8;    // 8-element column tiles per quantity
+constexpr int kJH = kL < 16 ? 16 : kL;  // bytes of j|h per (tile, face) (padded for TMA)
+constexpr int kW = kDmWarps;   // warps per CTA (kDmCtasPerSm CTAs per SM: 3 warps per sub-partition)
 constexpr int kT = kW * 32;    // threads per CTA
 constexpr int kU = 3;          // units (8-column tiles) per warp
 constexpr int kXW = 3 * kU * 4 * 8;  // warp-private X buffer: [c][k][row][8 elements]
@@ -35,7 +37,13 @@ constexpr int kXBUF = YDG_XBUF;      // star-chunk buffers per warp (1: reuse af
 
 enum Src { SRC_Q, SRC_S, SRC_I };
 
-__device__ __forceinline__ int swz(int row, int col) { return row * kRS + (col ^ ((row & 1) << 3)); }
+// Row swizzle inside aligned 8-column groups so that a 4-row x 8-column B-fragment load hits
+// 4 disjoint bank groups: rows of 144 doubles (16-element tiles) start on the same bank ->
+// XOR 8 on odd rows; rows of 72 doubles (8-element tiles) alternate by 8 banks already ->
+// XOR 4 on rows 2, 3 (mod 4).  Column pairs (2c, 2c+1) stay adjacent.
+__device__ __forceinline__ int swz(int row, int col) {
+  return row * kRS + (kL == 16 ? (col ^ ((row & 1) << 3)) : (col ^ ((row & 2) << 1)));
+}
 
 struct Ctx {
   int lane, w;
@@ -43,9 +51,9 @@ struct Ctx {
   int sh4, sh8;       // 8 * (lane & 3), 8 * (lane >> 2): byte of a k-set / m-tile row word
   // star chunk role: lane -> (element xe = 8ct + (lane & 7), unit xk = lane >> 3; xk = 3 idle)
   int xe, xk;
-  // column role (sparse DFMA steps): thread cc < 144 owns data column cc = cp*16 + ce
+  // column role (sparse DFMA steps): thread cc < 9 kL owns data column cc = cp*kL + ce
   int cc, ce, cp;
-  const double* star;  // star matrices of this tile, global [c][p][3][16]
+  const double* star;  // star matrices of this tile, global [c][p][3][kL]
   double* S;          // [SROWS][288]  D^d, d >= 1
   double* I;          // [IROWS][288]  time integral rows < IROWS
   double* xb;         // warp-private [3][kU][4][8]
@@ -487,10 +495,10 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
 __device__ __forceinline__ void init_ctx(Ctx& x) {
   x.lane = threadIdx.x & 31;
   x.w = threadIdx.x >> 5;
-  x.col0 = 3 * (x.w >> 1) * kL + 8 * (x.w & 1);
+  x.col0 = 3 * (x.w / kCT) * kL + 8 * (x.w % kCT);
   x.sh4 = 8 * (x.lane & 3);
   x.sh8 = 8 * (x.lane >> 2);
-  x.xe = 8 * (x.w & 1) + (x.lane & 7);
+  x.xe = 8 * (x.w % kCT) + (x.lane & 7);
   x.xk = x.lane >> 3;
   x.cc = threadIdx.x;
   x.ce = x.cc % kL;
@@ -514,7 +522,7 @@ __device__ __forceinline__ void after_ck0(Ctx& x) {
 // CK + time integral, face traces R^iT I (stored for the flux kernel) and
 // the volume term for 32-element tiles.
 template <int N>
-__global__ void __launch_bounds__(kT, 2) dm_local(const __grid_constant__ StepParams<double> prm) {
+__global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_local(const __grid_constant__ StepParams<double> prm) {
   using G = DG<N>;
   using Lay = Layout<N>;
   constexpr int B = G::B;
@@ -542,7 +550,7 @@ __global__ void __launch_bounds__(kT, 2) dm_local(const __grid_constant__ StepPa
   double* stg1 = x.S + Lay::FACE;
   // 3-column pattern of star-matrix row p = 3g + xk of the star-chunk role (setup.cpp
   // star_cols), packed 5 bits per column
-  const int xp = 3 * (x.w >> 1) + (x.xk < kU ? x.xk : 0);
+  const int xp = 3 * (x.w / kCT) + (x.xk < kU ? x.xk : 0);
   {
     constexpr unsigned long long packed[9] = {6 | 7 << 5 | 8 << 10, 6 | 7 << 5 | 8 << 10, 6 | 7 << 5 | 8 << 10,
                                               6 | 7 << 5 | 7 << 10, 7 | 8 << 5 | 8 << 10, 6 | 8 << 5 | 8 << 10,
@@ -647,7 +655,7 @@ __global__ void __launch_bounds__(kT, 2) dm_local(const __grid_constant__ StepPa
 // (e, m) builds the Godunov flux of row m from T and Z (godunov_flux), writing Y (rows
 // [m][288]), and the warp lifts its own columns of Y with DMMAs into Q.
 template <int N>
-__global__ void __launch_bounds__(kT, 2) dm_flux(const __grid_constant__ StepParams<double> prm) {
+__global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_flux(const __grid_constant__ StepParams<double> prm) {
   using G = DG<N>;
   using Lay = Layout<N>;
   constexpr int B = G::B, Bt = G::Bt, TS = G::TS, FACE = Lay::FACE;
@@ -656,11 +664,11 @@ __global__ void __launch_bounds__(kT, 2) dm_flux(const __grid_constant__ StepPar
   double* O = smem;                    // own face block [lane][TS]
   double* NB = smem + FACE;            // [lane][TS] neighbour face blocks
   double* Y0 = smem + 2 * FACE;        // [2][Bt][144]: rotated neighbour rows, then the flux
-  double* FC = Y0 + 2 * Bt * kRS;      // [12][16] flux coefficients of the current item
-  int32_t* NBX = reinterpret_cast<int32_t*>(FC + FCN);  // [16] neighbour slots of the next item
-  int8_t* JH = reinterpret_cast<int8_t*>(NBX + kL);     // [16] j | h << 2 of the current item
-  int8_t* JHX = JH + kL;                                // [16] j | h << 2 of the next item
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(JHX + kL);  // own, nb
+  double* FC = Y0 + 2 * Bt * kRS;      // [12][kL] flux coefficients of the current item
+  int32_t* NBX = reinterpret_cast<int32_t*>(FC + FCN);  // [kL] neighbour slots of the next item
+  int8_t* JH = reinterpret_cast<int8_t*>(NBX + kL);     // [kJH] j | h << 2 of the current item
+  int8_t* JHX = JH + kJH;                               // [kJH] j | h << 2 of the next item
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(JHX + kJH);  // own, nb
   Ctx x;
   init_ctx(x);
   x.frags = frag_table<N>();
@@ -675,13 +683,13 @@ __global__ void __launch_bounds__(kT, 2) dm_flux(const __grid_constant__ StepPar
   // item k+1, so no global load sits on the per-face critical path.
   auto issue_own = [&](int64_t tile, int F, int64_t ntile, int nF, bool next) {
     const int64_t item = tile * 4 + F, nitem = ntile * 4 + nF;
-    mbar_expect_tx(&bar[0], (FACE + FCN) * sizeof(double) + kL + (next ? kL * 5 : 0));  // + j|h, slots
+    mbar_expect_tx(&bar[0], (FACE + FCN) * sizeof(double) + kJH + (next ? kL * 4 + kJH : 0));  // + j|h, slots
     bulk_g2s(O, prm.traces + item * FACE, FACE * sizeof(double), &bar[0]);
     bulk_g2s(FC, prm.aplus + item * FCN, FCN * sizeof(double), &bar[0]);
-    bulk_g2s(JH, prm.jh + item * kL, kL, &bar[0]);
+    bulk_g2s(JH, prm.jh + item * kJH, kJH, &bar[0]);
     if (next) {
       bulk_g2s(NBX, prm.nb + nitem * kL, kL * sizeof(int32_t), &bar[0]);
-      bulk_g2s(JHX, prm.jh + nitem * kL, kL, &bar[0]);
+      bulk_g2s(JHX, prm.jh + nitem * kJH, kJH, &bar[0]);
     }
   };
   auto issue_nb = [&](const int32_t* nbs, const int8_t* jhs) {  // thread 0
@@ -700,7 +708,7 @@ __global__ void __launch_bounds__(kT, 2) dm_flux(const __grid_constant__ StepPar
 #pragma unroll
     for (int e = 0; e < kL; ++e) {
       nbs[e] = prm.nb[t0 * 4 * kL + e];
-      jhs[e] = prm.jh[t0 * 4 * kL + e];
+      jhs[e] = prm.jh[t0 * 4 * kJH + e];
     }
     issue_nb(nbs, jhs);
     issue_own(t0, 0, t0, 1, true);

@@ -95,8 +95,8 @@ const void* pick_neigh(int N, int eb) {
   }
   return nullptr;
 }
-// fp64 tensor-core kernels: 6 warps (dmma_impl.cuh kW); fp32 sparse kernels: 9 warps
-int block_threads(int elem_bytes) { return elem_bytes == 8 ? 6 * 32 : kP * kLanes; }
+// fp64 tensor-core kernels: kDmWarps warps (dmma_impl.cuh kW); fp32 sparse kernels: 9 warps
+int block_threads(int elem_bytes) { return elem_bytes == 8 ? kDmWarps * 32 : kP * kLanes; }
 int nB(int N) { return (N + 1) * (N + 2) * (N + 3) / 6; }
 int nBt(int N) { return (N + 1) * (N + 2) / 2; }
 

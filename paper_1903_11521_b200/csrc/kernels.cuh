@@ -5,7 +5,15 @@
 
 namespace ydg {
 
-constexpr int kLanes = 32;   // elements per tile of the fp32 kernels (fp64 tensor-core kernels: 16)
+constexpr int kLanes = 32;   // elements per tile of the fp32 kernels
+// fp64 tensor-core kernels: elements per tile (8 or 16), warps per CTA (3 per 8 elements),
+// CTAs per SM (12 warps per SM: three per sub-partition)
+#ifndef YDG_DM_LANES
+#define YDG_DM_LANES 16
+#endif
+constexpr int kDmLanes = YDG_DM_LANES;
+constexpr int kDmWarps = 3 * (kDmLanes / 8);
+constexpr int kDmCtasPerSm = 12 / kDmWarps;
 constexpr int kMaxN = 6;
 
 template <typename T>
@@ -18,7 +26,7 @@ struct StepParams {
                          // fp64: factored flux solvers [tile][face][kFaceCoeffs][32]
   const T* aminus;       // fp32: [tile][face][p][q][32]; fp64: unused
   const int32_t* nb;     // [tile][face][32] neighbour element (local index incl. ghosts)
-  const int8_t* jh;      // [tile][face][32] j | (h << 2)
+  const int8_t* jh;      // [tile][face][max(L, 16)] j | (h << 2)
   int64_t tile0;         // first tile handled by this launch
   int64_t ntiles;        // number of tiles handled
   T scal[2 * kMaxN];     // dt/(d+1), d < N ; dt/(d+2), d < N
