@@ -53,6 +53,9 @@ struct Ctx {
   int xe, xk;
   // column role (sparse DFMA steps): thread cc < 9 kL owns data column cc = cp*kL + ce
   int cc, ce, cp;
+  // tail role (warp-synchronous CK tail): element te = 3 w + lane / 9, quantity tp = lane % 9,
+  // column tc = tp*kL + te, or -1 if the lane has no element
+  int te, tp, tc;
   const double* star;  // star matrices of this tile, global [c][p][3][kL]
   double* S;          // [SROWS][288]  D^d, d >= 1
   double* I;          // [IROWS][288]  time integral rows < IROWS
@@ -388,38 +391,38 @@ __device__ __forceinline__ void godunov_flux(const double* t, const double* z, c
 }
 
 // Column role (sparse DFMA CK steps): star coefficients of quantity cp of element ce.
-__device__ __forceinline__ void col_star(const Ctx& x, double (&ca)[9], int& q0, int& q1, int& q2) {
+__device__ __forceinline__ void col_star(const Ctx& x, int ce, int cp, double (&ca)[9], int& q0, int& q1, int& q2) {
   constexpr unsigned long long packed[9] = {6 | 7 << 5 | 8 << 10, 6 | 7 << 5 | 8 << 10, 6 | 7 << 5 | 8 << 10,
                                             6 | 7 << 5 | 7 << 10, 7 | 8 << 5 | 8 << 10, 6 | 8 << 5 | 8 << 10,
                                             0 | 3 << 5 | 5 << 10, 3 | 1 << 5 | 4 << 10, 5 | 4 << 5 | 2 << 10};
   unsigned long long w = 0;
 #pragma unroll
-  for (int i = 0; i < 9; ++i) w = (x.cp == i) ? packed[i] : w;
+  for (int i = 0; i < 9; ++i) w = (cp == i) ? packed[i] : w;
   q0 = static_cast<int>(w & 31);
   q1 = static_cast<int>((w >> 5) & 31);
   q2 = static_cast<int>((w >> 10) & 31);
 #pragma unroll
   for (int c = 0; c < 3; ++c)
 #pragma unroll
-    for (int j = 0; j < 3; ++j) ca[3 * c + j] = ld_stream(x.star + ((c * kP + x.cp) * 3 + j) * kL + x.ce);
+    for (int j = 0; j < 3; ++j) ca[3 * c + j] = ld_stream(x.star + ((c * kP + cp) * 3 + j) * kL + ce);
 }
 template <Src SRC, int B>
-__device__ __forceinline__ void col_x(const Ctx& x, int l, const double (&ca)[9], int q0, int q1, int q2,
+__device__ __forceinline__ void col_x(const Ctx& x, int l, int ce, const double (&ca)[9], int q0, int q1, int q2,
                                       double& x0, double& x1, double& x2) {
-  const double d0 = load_data<SRC, B>(x, l, q0 * kL + x.ce);
-  const double d1 = load_data<SRC, B>(x, l, q1 * kL + x.ce);
-  const double d2 = load_data<SRC, B>(x, l, q2 * kL + x.ce);
+  const double d0 = load_data<SRC, B>(x, l, q0 * kL + ce);
+  const double d1 = load_data<SRC, B>(x, l, q1 * kL + ce);
+  const double d2 = load_data<SRC, B>(x, l, q2 * kL + ce);
   x0 = fma(ca[2], d2, fma(ca[1], d1, ca[0] * d0));
   x1 = fma(ca[5], d2, fma(ca[4], d1, ca[3] * d0));
   x2 = fma(ca[8], d2, fma(ca[7], d1, ca[6] * d0));
 }
 // Write-back of a sparse CK step: D^{d+1} = dt/(d+1) y into S, time integral (as ck_wb).
 template <int FIRST, int BO>
-__device__ __forceinline__ void col_wb(Ctx& x, const double (&y)[BO], int d) {
+__device__ __forceinline__ void col_wb(Ctx& x, int cc, const double (&y)[BO], int d) {
   const double sc = x.scal[d], ic = x.scal[x.N + d];
 #pragma unroll
   for (int k = 0; k < BO; ++k) {
-    const int s = swz(k, x.cc);
+    const int s = swz(k, cc);
     const double v = sc * y[k];
     x.S[s] = v;
     x.I[s] = FIRST ? fma(ic, v, x.dt * x.I[s]) : fma(ic, v, x.I[s]);
@@ -503,6 +506,9 @@ __device__ __forceinline__ void init_ctx(Ctx& x) {
   x.cc = threadIdx.x;
   x.ce = x.cc % kL;
   x.cp = x.cc / kL;
+  x.te = 3 * x.w + x.lane / kP;
+  x.tp = x.lane % kP;
+  x.tc = (x.lane < 3 * kP && x.te < kL) ? x.tp * kL + x.te : -1;
 }
 
 // Stage NF A fragments starting at table index F0 into the shared buffer (one thread).
@@ -596,19 +602,26 @@ __global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_local(const __grid_consta
     // traces T_F = R^FT I of the four faces -> staging -> one TMA bulk store per face;
     // they read Q^n (rows >= IROWS of I from global memory), so they precede the update
     double* gtr = prm.traces + tile * 4 * Lay::FACE;
-    G::trace01(x, stg0, stg1);  // faces 0 and 1: sparse DFMA
-    fence_proxy_async();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      bulk_s2g(gtr, stg0, Lay::FACE * sizeof(double));
-      bulk_s2g(gtr + Lay::FACE, stg1, Lay::FACE * sizeof(double));
+    constexpr int F0 = G::TR01_DFMA ? 2 : 0;
+    if constexpr (G::TR01_DFMA) {
+      G::trace01(x, stg0, stg1);  // faces 0 and 1: sparse DFMA
+      fence_proxy_async();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        bulk_s2g(gtr, stg0, Lay::FACE * sizeof(double));
+        bulk_s2g(gtr + Lay::FACE, stg1, Lay::FACE * sizeof(double));
+      }
     }
 #pragma unroll
-    for (int F = 2; F < 4; ++F) {  // faces 2 and 3: tensor cores
+    for (int F = F0; F < 4; ++F) {  // tensor-core faces
       double* stg = (F & 1) ? stg1 : stg0;
-      if (threadIdx.x == 0) bulk_wait_read<1>();  // the store of face F-2 has left stg
-      __syncthreads();
-      if (F == 2) G::template trace<2>(x, stg);
+      if (F >= 2) {
+        if (threadIdx.x == 0) bulk_wait_read<1>();  // the store of face F-2 has left stg
+        __syncthreads();
+      }
+      if (F == 0) G::template trace<0>(x, stg);
+      else if (F == 1) G::template trace<1>(x, stg);
+      else if (F == 2) G::template trace<2>(x, stg);
       else G::template trace<3>(x, stg);
       fence_proxy_async();
       __syncthreads();

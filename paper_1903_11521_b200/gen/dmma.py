@@ -170,7 +170,13 @@ def emit_gprod(b, tab, M, outs, ins, loader, acc="acc", fbase=None):
     return n
 
 
-DFMA_CK_ROWS = 10  # CK steps with at most this many output rows run as sparse DFMA code
+# CK steps with at most this many output rows run as sparse DFMA code (CTA-wide)
+DFMA_CK_ROWS = int(os.environ.get("YDG_GEN_CKROWS", "20"))
+# faces 0 and 1 traces as sparse DFMA code (else tensor cores)
+DFMA_TR01 = os.environ.get("YDG_GEN_TR01", "1") == "1"
+DFMA_TAIL_ROWS = 0   # CK steps d >= 1 from the first with at most this many output rows on:
+                     # one warp-synchronous sparse DFMA phase (0 = off: the element-grouped
+                     # lanes hit 9-way shared-memory bank conflicts, measured slower)
 
 
 def emit_ck_dfma(b, d, K, bi, bo, IROWS):
@@ -194,20 +200,60 @@ def emit_ck_dfma(b, d, K, bi, bo, IROWS):
     b("    if (x.cc < kRS) {")
     b("      double ca[9];")
     b("      int q0, q1, q2;")
-    b("      col_star(x, ca, q0, q1, q2);")
+    b("      col_star(x, x.ce, x.cp, ca, q0, q1, q2);")
     for l in sorted(nz):
-        b(f"      {{ double x0, x1, x2; col_x<{src}, B>(x, {l}, ca, q0, q1, q2, x0, x1, x2);")
+        b(f"      {{ double x0, x1, x2; col_x<{src}, B>(x, {l}, x.ce, ca, q0, q1, q2, x0, x1, x2);")
         for c, k, v in nz[l]:
             b(f"        y[{k}] = fma({float(v)!r}, x{c}, y[{k}]);")
         b("      }")
     b("    }")
     b("    __syncthreads();  // every read of D^d done")
-    b(f"    if (x.cc < kRS) col_wb<{1 if d == 0 else 0}, {bo}>(x, y, {d});")
+    b(f"    if (x.cc < kRS) col_wb<{1 if d == 0 else 0}, {bo}>(x, x.cc, y, {d});")
     if d == 0 and IROWS > bo:
         b(f"    scale_irows<{bo}, {IROWS}>(x);  // rows of I fed by D^0 only: dt * Q")
     b("    __syncthreads();")
     b("  }")
     return -n  # negative: nonzero FMAs (not tiles)
+
+
+def emit_ck_tail(b, d0, N, K):
+    """CK steps d0..N-1 (few output rows) as one warp-synchronous phase of constant-
+    coefficient DFMAs: thread (element te, quantity tp) -- the 9 quantities of an element
+    sit in one warp (3 elements per warp), so the cross-quantity star products need only
+    __syncwarp between steps, no CTA barrier.  Nonzeros of Ktilde only."""
+    n = 0
+    b(f"  // CK steps {d0}..{N - 1}: warp-synchronous sparse DFMA tail")
+    b("  static __device__ __forceinline__ void ck_tail(Ctx& x) {")
+    b("    double ca[9];")
+    b("    int q0 = 0, q1 = 0, q2 = 0;")
+    b("    if (x.tc >= 0) col_star(x, x.te, x.tp, ca, q0, q1, q2);")
+    for d in range(d0, N):
+        bi, bo = comb(N - d + 3, 3), comb(N - d + 2, 3)
+        nz = {}
+        for c in range(3):
+            for k in range(bo):
+                for l in range(bi):
+                    v = -K[c][l][k]
+                    if v != 0.0:
+                        nz.setdefault(l, []).append((c, k, v))
+                        n += 1
+        b(f"    {{  // step d = {d}: rows in {bi}, rows out {bo}")
+        b(f"      double y[{bo}];")
+        b(f"      for (int k = 0; k < {bo}; ++k) y[k] = 0.0;")
+        b("      if (x.tc >= 0) {")
+        for l in sorted(nz):
+            b(f"        {{ double x0, x1, x2; col_x<SRC_S, B>(x, {l}, x.te, ca, q0, q1, q2, x0, x1, x2);")
+            for c, k, v in nz[l]:
+                b(f"          y[{k}] = fma({float(v)!r}, x{c}, y[{k}]);")
+            b("        }")
+        b("      }")
+        b("      __syncwarp();  // every read of the element's D^d done")
+        b(f"      if (x.tc >= 0) col_wb<0, {bo}>(x, x.tc, y, {d});")
+        b("      __syncwarp();")
+        b("    }")
+    b("    __syncthreads();  // the time integral is complete")
+    b("  }")
+    return -n
 
 
 def emit_trace01_dfma(b, R, B, Bt, IROWS, TS):
@@ -259,6 +305,7 @@ def gen_order(N):
     body = []
     b = body.append
     counts = {}
+    tail0 = None
     regions = {}  # products whose A fragments are staged in shared memory: [first, end)
     # ---------------- CK
     for d in range(N):
@@ -266,6 +313,10 @@ def gen_order(N):
         tl = til[f"ck{d}"]
         MT = len(tl["out"])
         mats = [(lambda r, col, c=c: -K[c][col][r]) for c in range(3)]  # Kt^c[r][col] = -K^c[col][r]
+        if d >= 1 and bo <= DFMA_TAIL_ROWS:
+            tail0 = d
+            counts["ck_tail"] = emit_ck_tail(b, d, N, K)
+            break
         if bo <= DFMA_CK_ROWS:
             counts[f"ck{d}"] = emit_ck_dfma(b, d, K, bi, bo, IROWS)
             continue
@@ -287,11 +338,14 @@ def gen_order(N):
         b("    __syncthreads();")
         b("  }")
     b("  static __device__ __forceinline__ void ck(Ctx& x) {")
-    for d in range(N):
+    for d in range(tail0 if tail0 is not None else N):
         b(f"    ck{d}(x);")
         if d == 0:
             b("    after_ck0<" + str(N) + ">(x);  // the fragment buffer is free: stage the volume's")
         b(f"    YDG_PHASE({2 + d});")
+    if tail0 is not None:
+        b("    ck_tail(x);")
+        b(f"    YDG_PHASE({2 + tail0});")
     b("  }")
     # ---------------- volume
     tl = til["vol"]
@@ -308,7 +362,8 @@ def gen_order(N):
     b("    add_q<" + str(QMT) + ", IROWS>(x, Qt, acc, w, Qs);")
     b("  }")
     # ---------------- traces T_i = R^iT I
-    counts["tr01_dfma"] = emit_trace01_dfma(b, R, B, Bt, IROWS, TS)
+    counts["tr01_dfma"] = emit_trace01_dfma(b, R, B, Bt, IROWS, TS) if DFMA_TR01 else 0
+    b(f"  static constexpr bool TR01_DFMA = {'true' if DFMA_TR01 else 'false'};")
     b(f"  // trace: T_F = R^FT I (rows < IROWS of I from shared memory, dt * Q from global memory);")
     b(f"  // the C fragments go to the staging block [lane][m][q] (stride TS)")
     b(f"  template <int F> static __device__ __forceinline__ void trace(Ctx& x, double* stg) {{")

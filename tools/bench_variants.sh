@@ -8,7 +8,7 @@ for lib in paper_1903_11521_b200/libydg.so variants/*.so; do
   python3 -c "
 import json,sys
 d=json.loads(open('gpurun_out/v_$name.json').read().strip().splitlines()[-1])
-k=d['kernels']
-print('$name', round(d['ms_per_step'],2), 'local', k['ader_local']['ms_per_launch'], 'flux', k['ader_neigh']['ms_per_launch'])
+k=d['kernels']; ks=list(k)
+print('$name', round(d['ms_per_step'],2), ks[0], k[ks[0]]['ms_per_launch'], ks[1], k[ks[1]]['ms_per_launch'])
 " || tail -3 gpurun_out/v_$name.err
 done
