@@ -735,8 +735,7 @@ __global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_flux(const __grid_constan
     const bool more = it + gridDim.x < prm.ntiles;
 #pragma unroll
     for (int F = 0; F < 4; ++F) {
-      // Y buffer F & 1: last read by the lift of face F-2, which every warp finished before
-      // the barriers of face F-1
+      // Y buffer F & 1: last read by the paired lift of faces F-2, F-1 (followed by a barrier)
       double* Y = Y0 + (F & 1) * Bt * kRS;
       const bool has_next = F < 3 || more;
       mbar_wait(&bar[0], ph_o);  // own block, coefficients, j|h of this item; slots of the next
@@ -779,13 +778,15 @@ __global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_flux(const __grid_constan
         const bool nn = nF < 3 || nt + gridDim.x < prm.tile0 + prm.ntiles;
         issue_own(nt, nF, nF < 3 ? nt : nt + gridDim.x, nF < 3 ? nF + 1 : 0, nn);
       }
-      // lift and Q update per face, two m-tiles at a time; the tile's Q stays in L2
-      // across its four updates
-      double* Qt = prm.Q + tile * B * kRS;
-      if (F == 0) G::template lift<0>(x, Y, Qt);
-      else if (F == 1) G::template lift<1>(x, Y, Qt);
-      else if (F == 2) G::template lift<2>(x, Y, Qt);
-      else G::template lift<3>(x, Y, Qt);
+      // lift and Q update per pair of faces (both Y buffers), two m-tiles at a time; the
+      // tile's Q stays in L2 across its two updates.  The next pair's rotation rewrites the
+      // Y buffers: a barrier after the lift.
+      if (F & 1) {
+        double* Qt = prm.Q + tile * B * kRS;
+        if (F == 1) G::template lift2<0>(x, Y0, Y0 + Bt * kRS, Qt);
+        else G::template lift2<1>(x, Y0, Y0 + Bt * kRS, Qt);
+        __syncthreads();
+      }
     }
   }
 }

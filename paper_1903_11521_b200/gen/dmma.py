@@ -424,6 +424,34 @@ def gen_order(N):
             b("      }")
         b("    }")
     b("  }")
+    # paired lift: faces 2P and 2P+1 accumulate into the same registers, one Q update per pair
+    b(f"  // paired lift + Q update: Q += R^(2P) Ya + R^(2P+1) Yb")
+    b(f"  template <int P> static __device__ __forceinline__ void lift2(Ctx& x, const double* Ya, const double* Yb, double* Qt) {{")
+    for P in range(2):
+        b(f"    {'if' if P == 0 else 'else if'} constexpr (P == {P}) {{")
+        b("      double2 qn[2][kU];")
+        g0 = groups[0]
+        b(f"      load_q2(x, Qt, {row_word64(outs[g0[0]])}, {row_word64(outs[g0[1]]) if len(g0) > 1 else '~0ULL'}, qn);")
+        for gi, grp in enumerate(groups):
+            b("      {")
+            b("        double2 qc[2][kU];")
+            b("        copy_q2(qn, qc);")
+            if gi + 1 < len(groups):
+                g1 = groups[gi + 1]
+                b(f"        load_q2(x, Qt, {row_word64(outs[g1[0]])}, {row_word64(outs[g1[1]]) if len(g1) > 1 else '~0ULL'}, qn);")
+            b("        double acc[2][kU][2];")
+            b("        zero_acc(acc);")
+            sub = [outs[m] for m in grp]
+            for i, yv in ((2 * P, "Ya"), (2 * P + 1, "Yb")):
+                Mi = lambda r, col, i=i: R[i][r][col]
+                b("        {")
+                emit_gprod(b, tab, Mi, sub, tl["in"][i],
+                           lambda k, w, yv=yv: f"double bf[kU]; smem_b(x, {yv}, {w}, bf);", fbase=lift0)
+                b("        }")
+            b(f"        store_q2(x, Qt, {row_word64(outs[grp[0]])}, {row_word64(outs[grp[1]]) if len(grp) > 1 else '~0ULL'}, acc, qc);")
+            b("      }")
+        b("    }")
+    b("  }")
     regions["LIFT"] = (lift0, len(tab.frags))
     regions.setdefault("CK0", (0, 0))  # CK step 0 ran as sparse DFMA code
     # ---------------- neighbour orientation z = f^h t, uniform over lanes:
