@@ -24,6 +24,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
                   "-I", CSRC, "--expt-relaxed-constexpr"] + os.environ.get("YDG_NVFLAGS", "").split()
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-fopenmp", "-I", CSRC, "-I", os.path.join(CUDA, "include")]
+# -D defines of YDG_NVFLAGS apply to the host translation units as well (shared headers)
+CXXFLAGS += [f for f in os.environ.get("YDG_NVFLAGS", "").split() if f.startswith("-D")]
 
 
 def sources():

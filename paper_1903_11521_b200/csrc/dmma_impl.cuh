@@ -109,7 +109,15 @@ __device__ __forceinline__ double afrag_s(const Ctx& x, int i) { return x.fs[i *
 #define YDG_FLUX_FS 0
 #endif
 constexpr bool kLocalFs = YDG_LOCAL_FS, kFluxFs = YDG_FLUX_FS;
-__device__ __forceinline__ double afrag_l(const Ctx& x, int g, int r) { return kLocalFs ? afrag_s(x, r) : afrag(x, g); }
+// capacity of the local kernel's fragment buffer (fragments of 256 B; the rest of the
+// product reads the global table)
+#ifndef YDG_LOCAL_FS_CAP
+#define YDG_LOCAL_FS_CAP 56
+#endif
+constexpr int kLocalFsCap = YDG_LOCAL_FS_CAP;
+__device__ __forceinline__ double afrag_l(const Ctx& x, int g, int r) {
+  return (kLocalFs && r < kLocalFsCap) ? afrag_s(x, r) : afrag(x, g);
+}
 __device__ __forceinline__ double afrag_f(const Ctx& x, int g, int r) { return kFluxFs ? afrag_s(x, r) : afrag(x, g); }
 __device__ __forceinline__ double ld_stream(const double* p) {
   double v;
@@ -440,7 +448,8 @@ struct Layout {
   // A-fragment buffer (CK step 0, then the volume term) after I, S, xb and the staging
   static constexpr int FOFF = (ROWS * kRS + XB > G::IROWS * kRS + 2 * FACE ? ROWS * kRS + XB
                                                                            : G::IROWS * kRS + 2 * FACE);
-  static constexpr int FSMAX = kLocalFs ? (G::CK0_NF > G::VOL_NF ? G::CK0_NF : G::VOL_NF) : 0;
+  static constexpr int FSMAX0 = G::CK0_NF > G::VOL_NF ? G::CK0_NF : G::VOL_NF;
+  static constexpr int FSMAX = kLocalFs ? (FSMAX0 < kLocalFsCap ? FSMAX0 : kLocalFsCap) : 0;
   static constexpr int LOCAL = FOFF + FSMAX * 32 + 2;  // + two mbarriers
   // flux kernel: own face block, two neighbour face blocks, Y rows, lift fragments, four
   // mbarriers
@@ -522,7 +531,7 @@ __device__ __forceinline__ void stage_frags(const Ctx& x, int F0, int NF) {
 template <int N>
 __device__ __forceinline__ void after_ck0(Ctx& x) {
   if constexpr (kLocalFs)
-    if (threadIdx.x == 0) stage_frags<N>(x, DG<N>::VOL_F0, DG<N>::VOL_NF);
+    if (threadIdx.x == 0) stage_frags<N>(x, DG<N>::VOL_F0, DG<N>::VOL_NF < kLocalFsCap ? DG<N>::VOL_NF : kLocalFsCap);
 }
 
 // CK + time integral, face traces R^iT I (stored for the flux kernel) and
@@ -546,7 +555,7 @@ __global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_local(const __grid_consta
   if (threadIdx.x == 0) {
     mbar_init(x.fbar, 1);
     mbar_init(qbar, 1);
-    if (kLocalFs && blockIdx.x < prm.ntiles) stage_frags<N>(x, G::CK0_F0, G::CK0_NF);
+    if (kLocalFs && blockIdx.x < prm.ntiles) stage_frags<N>(x, G::CK0_F0, G::CK0_NF < kLocalFsCap ? G::CK0_NF : kLocalFsCap);
   }
   __syncthreads();
   x.dt = prm.dt;
@@ -646,7 +655,8 @@ __global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_local(const __grid_consta
       G::add_volume(x, Qt, acc, x.S);
     }
     __syncthreads();  // before the next tile overwrites the shared regions
-    if (kLocalFs && threadIdx.x == 0 && it + gridDim.x < prm.ntiles) stage_frags<N>(x, G::CK0_F0, G::CK0_NF);
+    if (kLocalFs && threadIdx.x == 0 && it + gridDim.x < prm.ntiles)
+      stage_frags<N>(x, G::CK0_F0, G::CK0_NF < kLocalFsCap ? G::CK0_NF : kLocalFsCap);
     YDG_PHASE(11);
 #ifdef YDG_PHASES
     if (threadIdx.x == 0 && blockIdx.x == 0 && it >= 2 * gridDim.x && it < 6 * gridDim.x) {
