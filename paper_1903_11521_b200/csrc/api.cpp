@@ -279,7 +279,8 @@ int do_step(ydg_solver* h, double dt, int nsteps, cudaStream_t s) {
     }
     prm.tile0 = 0;
     prm.ntiles = h->ntiles;
-    CUDA_OR_FAIL(h, timed(h, 1, s, [&] { return launch_neigh<T>(h->N, prm, static_cast<int>(std::min<int64_t>(h->grid_neigh, prm.ntiles)), s); }));
+    const int64_t units = prm.ntiles * (h->prec == 8 ? h->lanes / 8 : 1);  // fp64 flux CTAs take 8-element halves
+    CUDA_OR_FAIL(h, timed(h, 1, s, [&] { return launch_neigh<T>(h->N, prm, static_cast<int>(std::min<int64_t>(h->grid_neigh, units)), s); }));
   }
   return YDG_OK;
 }
@@ -649,7 +650,7 @@ int ydg_upload_mesh(ydg_solver* h, int64_t ne, const double* xyz, const int64_t*
   int sms = 0, occ_l = 0, occ_n = 0;
   CUDA_OR_FAIL(h, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->dev));
   occ_l = eb == 8 ? kDmCtasPerSm : 1;  // fp64: 12 warps per SM in kDmCtasPerSm CTAs
-  occ_n = eb == 8 ? kDmCtasPerSm : 1;
+  occ_n = eb == 8 ? 4 : 1;  // fp64 flux kernel: four 3-warp CTAs (8-element halves) per SM
   h->grid_local = sms * occ_l;
   h->grid_neigh = sms * occ_n;
   h->have_mesh = true;

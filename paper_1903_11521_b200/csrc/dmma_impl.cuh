@@ -49,6 +49,7 @@ struct Ctx {
   int lane, w;
   int col0;           // column of unit 0 of this warp's B fragments / C fragments: 3g*32 + 8ct
   int sh4, sh8;       // 8 * (lane & 3), 8 * (lane >> 2): byte of a k-set / m-tile row word
+  int qcol0;          // flux kernel: HBM column of unit 0 of this warp's C fragments
   // star chunk role: lane -> (element xe = 8ct + (lane & 7), unit xk = lane >> 3; xk = 3 idle)
   int xe, xk;
   // column role (sparse DFMA steps): thread cc < 9 kL owns data column cc = cp*kL + ce
@@ -335,6 +336,45 @@ __device__ __forceinline__ void store_q2(const Ctx& x, double* Qt, unsigned long
   }
 }
 
+// ---- flux-kernel layout: CTAs of kLF = 8 elements (half of a 16-element HBM tile), 3 warps,
+// four CTAs per SM.  Shared rows have 72 columns; warp w owns units (quantity 3w + k, the
+// CTA's 8 elements); Q columns in HBM are (3w + k) * kL + half * 8 + element.
+constexpr int kLF = 8;
+constexpr int kRSF = kP * kLF;
+constexpr int kWF = 3;
+constexpr int kTF = kWF * 32;
+constexpr int kHalves = kL / kLF;
+constexpr int kFluxCtas = 4;
+__device__ __forceinline__ int swzf(int row, int col) { return row * kRSF + (col ^ ((row & 2) << 1)); }
+__device__ __forceinline__ void smem_bf(const Ctx& x, const double* Y, unsigned w, double (&bf)[kU]) {
+  const int row = krow(x, w);
+#pragma unroll
+  for (int k = 0; k < kU; ++k) bf[k] = Y[swzf(row, x.col0 + k * kLF + (x.lane >> 2))];
+}
+__device__ __forceinline__ int qcolf(const Ctx& x, int k) { return x.qcol0 + k * kL + 2 * (x.lane & 3); }
+__device__ __forceinline__ void load_qf(const Ctx& x, const double* Qt, unsigned long long w0, unsigned long long w1,
+                                        double2 (&q)[2][kU]) {
+#pragma unroll
+  for (int k2 = 0; k2 < 2; ++k2) {
+    const int row = mrow(x, k2 ? w1 : w0);
+#pragma unroll
+    for (int k = 0; k < kU; ++k)
+      q[k2][k] = row == 0xff ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(Qt + row * kRS + qcolf(x, k));
+  }
+}
+__device__ __forceinline__ void store_qf(const Ctx& x, double* Qt, unsigned long long w0, unsigned long long w1,
+                                         const double (&acc)[2][kU][2], const double2 (&q)[2][kU]) {
+#pragma unroll
+  for (int k2 = 0; k2 < 2; ++k2) {
+    const int row = mrow(x, k2 ? w1 : w0);
+    if (row == 0xff) continue;
+#pragma unroll
+    for (int k = 0; k < kU; ++k)
+      *reinterpret_cast<double2*>(Qt + row * kRS + qcolf(x, k)) =
+          make_double2(q[k2][k].x + acc[k2][k][0], q[k2][k].y + acc[k2][k][1]);
+  }
+}
+
 // Trace C fragments of one m-tile -> staging block [lane][m][q] (stride TS per lane).
 template <int TS>
 __device__ __forceinline__ void stage_trace(const Ctx& x, double* stg, const double (&acc)[kU][2], unsigned long long w) {
@@ -451,9 +491,10 @@ struct Layout {
   static constexpr int FSMAX0 = G::CK0_NF > G::VOL_NF ? G::CK0_NF : G::VOL_NF;
   static constexpr int FSMAX = kLocalFs ? (FSMAX0 < kLocalFsCap ? FSMAX0 : kLocalFsCap) : 0;
   static constexpr int LOCAL = FOFF + FSMAX * 32 + 2;  // + two mbarriers
-  // flux kernel: own face block, two neighbour face blocks, Y rows, lift fragments, four
-  // mbarriers
-  static constexpr int FLUX = 2 * FACE + 2 * G::Bt * kRS + kFaceCoeffs * kL + 16 + 2;  // + slots, j|h, mbarriers
+  // flux kernel (8-element CTAs): own face block, neighbour blocks, two Y buffers,
+  // coefficients, slots, j|h, mbarriers
+  static constexpr int FACEF = kLF * G::TS;  // doubles of one face of a flux CTA
+  static constexpr int FLUX = 2 * FACEF + 2 * G::Bt * kRSF + kFaceCoeffs * kLF + 16 + 2;  // + slots, j|h, mbarriers
 };
 
 // ---- asynchronous copy helpers (TMA bulk copies + mbarrier, Ampere-style cp.async)
@@ -678,123 +719,139 @@ __global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_local(const __grid_consta
 // (e, m) builds the Godunov flux of row m from T and Z (godunov_flux), writing Y (rows
 // [m][288]), and the warp lifts its own columns of Y with DMMAs into Q.
 template <int N>
-__global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_flux(const __grid_constant__ StepParams<double> prm) {
+__global__ void __launch_bounds__(kTF, kFluxCtas) dm_flux(const __grid_constant__ StepParams<double> prm) {
   using G = DG<N>;
   using Lay = Layout<N>;
-  constexpr int B = G::B, Bt = G::Bt, TS = G::TS, FACE = Lay::FACE;
-  constexpr int FCN = kFaceCoeffs * kL;  // factored flux solvers of one (tile, face)
+  constexpr int B = G::B, Bt = G::Bt, TS = G::TS, FACE = Lay::FACE, FACEF = Lay::FACEF;
+  constexpr int FCN = kFaceCoeffs * kLF;  // factored flux solvers of one (tile, face, half)
   extern __shared__ __align__(128) double smem[];
-  double* O = smem;                    // own face block [lane][TS]
-  double* NB = smem + FACE;            // [lane][TS] neighbour face blocks
-  double* Y0 = smem + 2 * FACE;        // [2][Bt][144]: rotated neighbour rows, then the flux
-  double* FC = Y0 + 2 * Bt * kRS;      // [12][kL] flux coefficients of the current item
-  int32_t* NBX = reinterpret_cast<int32_t*>(FC + FCN);  // [kL] neighbour slots of the next item
-  int8_t* JH = reinterpret_cast<int8_t*>(NBX + kL);     // [kJH] j | h << 2 of the current item
-  int8_t* JHX = JH + kJH;                               // [kJH] j | h << 2 of the next item
+  double* O = smem;                    // own face block [lane][TS] of the CTA's 8 elements
+  double* NB = smem + FACEF;           // [lane][TS] neighbour face blocks
+  double* Y0 = smem + 2 * FACEF;       // [2][Bt][72]: rotated neighbour rows, then the flux
+  double* FC = Y0 + 2 * Bt * kRSF;     // [12][8] flux coefficients of the current item
+  int32_t* NBX = reinterpret_cast<int32_t*>(FC + FCN);  // [8] neighbour slots of the next item
+  int8_t* JH = reinterpret_cast<int8_t*>(NBX + kLF);    // [16] j | h << 2 of the current (tile, face)
+  int8_t* JHX = JH + kJH;                               // [16] of the next item's (tile, face)
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(JHX + kJH);  // own, nb
   Ctx x;
-  init_ctx(x);
+  x.lane = threadIdx.x & 31;
+  x.w = threadIdx.x >> 5;
+  x.col0 = 3 * x.w * kLF;
+  x.sh4 = 8 * (x.lane & 3);
+  x.sh8 = 8 * (x.lane >> 2);
   x.frags = frag_table<N>();
-  if (blockIdx.x >= prm.ntiles) return;
+  const int64_t nitems = prm.ntiles * kHalves;  // (tile, half) work units
+  if (blockIdx.x >= nitems) return;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
   }
   __syncthreads();
-  // Items k = (tile, face) in this CTA's order; item k's "own" copy (thread 0) brings the
-  // tile's face block, its flux coefficients and j|h, and the neighbour slots and j|h of
-  // item k+1, so no global load sits on the per-face critical path.
-  auto issue_own = [&](int64_t tile, int F, int64_t ntile, int nF, bool next) {
+  // Items k = (unit, face) in this CTA's order, unit = (tile, half); item k's "own" copy
+  // (thread 0) brings the unit's face block, its flux coefficients and j|h, and the
+  // neighbour slots and j|h of item k+1, so no global load sits on the per-face path.
+  auto issue_own = [&](int64_t u, int F, int64_t nu, int nF, bool next) {
+    const int64_t tile = prm.tile0 + u / kHalves, half = u % kHalves;
+    const int64_t ntile = prm.tile0 + nu / kHalves, nhalf = nu % kHalves;
     const int64_t item = tile * 4 + F, nitem = ntile * 4 + nF;
-    mbar_expect_tx(&bar[0], (FACE + FCN) * sizeof(double) + kJH + (next ? kL * 4 + kJH : 0));  // + j|h, slots
-    bulk_g2s(O, prm.traces + item * FACE, FACE * sizeof(double), &bar[0]);
-    bulk_g2s(FC, prm.aplus + item * FCN, FCN * sizeof(double), &bar[0]);
+    mbar_expect_tx(&bar[0], (FACEF + FCN) * sizeof(double) + kJH + (next ? kLF * 4 + kJH : 0));
+    bulk_g2s(O, prm.traces + item * FACE + half * FACEF, FACEF * sizeof(double), &bar[0]);
+#pragma unroll
+    for (int k = 0; k < kFaceCoeffs; ++k)
+      bulk_g2s(FC + k * kLF, prm.aplus + (item * kFaceCoeffs + k) * kL + half * kLF, kLF * sizeof(double), &bar[0]);
     bulk_g2s(JH, prm.jh + item * kJH, kJH, &bar[0]);
     if (next) {
-      bulk_g2s(NBX, prm.nb + nitem * kL, kL * sizeof(int32_t), &bar[0]);
+      bulk_g2s(NBX, prm.nb + nitem * kL + nhalf * kLF, kLF * sizeof(int32_t), &bar[0]);
       bulk_g2s(JHX, prm.jh + nitem * kJH, kJH, &bar[0]);
     }
   };
-  auto issue_nb = [&](const int32_t* nbs, const int8_t* jhs) {  // thread 0
-    mbar_expect_tx(&bar[1], FACE * sizeof(double));
+  auto issue_nb = [&](const int32_t* nbs, const int8_t* jhs) {  // thread 0; jhs = this half's 8
+    mbar_expect_tx(&bar[1], FACEF * sizeof(double));
 #pragma unroll
-    for (int e = 0; e < kL; ++e) {
+    for (int e = 0; e < kLF; ++e) {
       const int64_t nbe = nbs[e];
       bulk_g2s(NB + e * TS, prm.traces + ((nbe / kL) * 4 + (jhs[e] & 3)) * FACE + (nbe % kL) * TS,
                TS * sizeof(double), &bar[1]);
     }
   };
-  const int64_t t0 = prm.tile0 + blockIdx.x;
-  if (threadIdx.x == 0) {
-    int32_t nbs[kL];
-    int8_t jhs[kL];
+  {
+    const int64_t u0 = blockIdx.x;
+    if (threadIdx.x == 0) {
+      const int64_t tile = prm.tile0 + u0 / kHalves, half = u0 % kHalves;
+      int32_t nbs[kLF];
+      int8_t jhs[kLF];
 #pragma unroll
-    for (int e = 0; e < kL; ++e) {
-      nbs[e] = prm.nb[t0 * 4 * kL + e];
-      jhs[e] = prm.jh[t0 * 4 * kJH + e];
+      for (int e = 0; e < kLF; ++e) {
+        nbs[e] = prm.nb[tile * 4 * kL + half * kLF + e];
+        jhs[e] = prm.jh[tile * 4 * kJH + half * kLF + e];
+      }
+      issue_nb(nbs, jhs);
+      issue_own(u0, 0, u0, 1, true);
     }
-    issue_nb(nbs, jhs);
-    issue_own(t0, 0, t0, 1, true);
   }
   unsigned ph_o = 0, ph_n = 0;
-  // thread roles: rotation (element re, column rp) for threads < 144; Godunov rows
+  // thread roles: rotation (element re, column rp) for threads < 72; Godunov rows
   // m = rp + 12 i of element re
-  const int re = threadIdx.x % kL, rp = threadIdx.x / kL;
-  for (int64_t it = blockIdx.x; it < prm.ntiles; it += gridDim.x) {
-    const int64_t tile = prm.tile0 + it;
-    const bool more = it + gridDim.x < prm.ntiles;
+  const int re = threadIdx.x % kLF, rp = threadIdx.x / kLF;
+  for (int64_t u = blockIdx.x; u < nitems; u += gridDim.x) {
+    const int64_t tile = prm.tile0 + u / kHalves, half = u % kHalves;
+    x.qcol0 = 3 * x.w * kL + half * kLF;
+    const bool more = u + gridDim.x < nitems;
 #pragma unroll
     for (int F = 0; F < 4; ++F) {
       // Y buffer F & 1: last read by the paired lift of faces F-2, F-1 (followed by a barrier)
-      double* Y = Y0 + (F & 1) * Bt * kRS;
+      double* Y = Y0 + (F & 1) * Bt * kRSF;
       const bool has_next = F < 3 || more;
       mbar_wait(&bar[0], ph_o);  // own block, coefficients, j|h of this item; slots of the next
       ph_o ^= 1;
       mbar_wait(&bar[1], ph_n);  // neighbour blocks of this item
       ph_n ^= 1;
-      if (threadIdx.x < kP * kL) {  // z = f^h t on column rp of element re's neighbour block -> Y
-        const int h = JH[re] >> 2;
+      if (threadIdx.x < kP * kLF) {  // z = f^h t on column rp of element re's neighbour block -> Y
+        const int h = JH[half * kLF + re] >> 2;
         const double* zc = NB + re * TS + rp;
         double t[Bt];
 #pragma unroll
         for (int n = 0; n < Bt; ++n) t[n] = zc[n * kP];
-        G::rot(h, t, Y, rp * kL + re);
+        G::rotf(h, t, Y, rp * kLF + re);
       }
       double fc[kFaceCoeffs];
 #pragma unroll
-      for (int k = 0; k < kFaceCoeffs; ++k) fc[k] = FC[k * kL + re];
+      for (int k = 0; k < kFaceCoeffs; ++k) fc[k] = FC[k * kLF + re];
       __syncthreads();  // rotated rows visible; every read of NB (and of NBX, JHX) done
-      if (threadIdx.x == 0 && has_next) issue_nb(NBX, JHX);
-      else if (threadIdx.x == 32 && F == 3 && more)  // next tile's Q -> L2
-        prefetch_l2(prm.Q + (tile + gridDim.x) * B * kRS, B * kRS * sizeof(double));
+      if (threadIdx.x == 0 && has_next) {
+        const int nhalf = F < 3 ? half : (u + gridDim.x) % kHalves;
+        issue_nb(NBX, JHX + nhalf * kLF);
+      } else if (threadIdx.x == 32 && F == 3 && more) {  // next unit's Q -> L2
+        prefetch_l2(prm.Q + (prm.tile0 + (u + gridDim.x) / kHalves) * B * kRS, B * kRS * sizeof(double));
+      }
       {  // Godunov flux of rows m = rp, rp + 12, ... of element re, in place in Y
         const double* T = O + re * TS;
 #pragma unroll
-        for (int i = 0; i < (Bt + kT / kL - 1) / (kT / kL); ++i) {
-          const int m = rp + (kT / kL) * i;
+        for (int i = 0; i < (Bt + kTF / kLF - 1) / (kTF / kLF); ++i) {
+          const int m = rp + (kTF / kLF) * i;
           if (m >= Bt) break;
           double z[kP], y[kP];
 #pragma unroll
-          for (int q = 0; q < kP; ++q) z[q] = Y[swz(m, q * kL + re)];
+          for (int q = 0; q < kP; ++q) z[q] = Y[swzf(m, q * kLF + re)];
           godunov_flux(T + m * kP, z, fc, y);
 #pragma unroll
-          for (int q = 0; q < kP; ++q) Y[swz(m, q * kL + re)] = y[q];
+          for (int q = 0; q < kP; ++q) Y[swzf(m, q * kLF + re)] = y[q];
         }
       }
       __syncthreads();  // every read of O, FC, JH done; Y complete
       if (threadIdx.x == 0 && has_next) {  // item k+1's own copy (and item k+2's slots)
-        const int64_t nt = F < 3 ? tile : tile + gridDim.x;
+        const int64_t nu = F < 3 ? u : u + gridDim.x;
         const int nF = F < 3 ? F + 1 : 0;
-        const bool nn = nF < 3 || nt + gridDim.x < prm.tile0 + prm.ntiles;
-        issue_own(nt, nF, nF < 3 ? nt : nt + gridDim.x, nF < 3 ? nF + 1 : 0, nn);
+        const bool nn = nF < 3 || nu + gridDim.x < nitems;
+        issue_own(nu, nF, nF < 3 ? nu : nu + gridDim.x, nF < 3 ? nF + 1 : 0, nn);
       }
       // lift and Q update per pair of faces (both Y buffers), two m-tiles at a time; the
-      // tile's Q stays in L2 across its two updates.  The next pair's rotation rewrites the
+      // unit's Q stays in L2 across its two updates.  The next pair's rotation rewrites the
       // Y buffers: a barrier after the lift.
       if (F & 1) {
         double* Qt = prm.Q + tile * B * kRS;
-        if (F == 1) G::template lift2<0>(x, Y0, Y0 + Bt * kRS, Qt);
-        else G::template lift2<1>(x, Y0, Y0 + Bt * kRS, Qt);
+        if (F == 1) G::template lift2<0>(x, Y0, Y0 + Bt * kRSF, Qt);
+        else G::template lift2<1>(x, Y0, Y0 + Bt * kRSF, Qt);
         __syncthreads();
       }
     }

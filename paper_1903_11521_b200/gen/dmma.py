@@ -395,60 +395,33 @@ def gen_order(N):
     tl = til["lift"]
     outs = tl["out"]
     groups = [list(range(g, min(g + 2, len(outs)))) for g in range(0, len(outs), 2)]
-    b(f"  // lift + Q update: Q += R^F Y_F (Y own columns in shared memory, rows [m][288])")
-    b(f"  template <int F> static __device__ __forceinline__ void lift(Ctx& x, const double* Y, double* Qt) {{")
     counts["lift"] = 0
     lift0 = len(tab.frags)
-    # the lift fragments are numbered in emission order; the flux kernel holds them all in
-    # shared memory (index relative to lift0)
-    for i in range(4):
-        b(f"    {'if' if i == 0 else 'else if'} constexpr (F == {i}) {{")
-        Mi = lambda r, col, i=i: R[i][r][col]
-        ins = tl["in"][i]
-        b("      double2 qn[2][kU];")
-        g0 = groups[0]
-        b(f"      load_q2(x, Qt, {row_word64(outs[g0[0]])}, {row_word64(outs[g0[1]]) if len(g0) > 1 else '~0ULL'}, qn);")
-        for gi, grp in enumerate(groups):
-            b("      {")
-            b("        double2 qc[2][kU];")
-            b("        copy_q2(qn, qc);")
-            if gi + 1 < len(groups):
-                g1 = groups[gi + 1]
-                b(f"        load_q2(x, Qt, {row_word64(outs[g1[0]])}, {row_word64(outs[g1[1]]) if len(g1) > 1 else '~0ULL'}, qn);")
-            b("        double acc[2][kU][2];")
-            b("        zero_acc(acc);")
-            sub = [outs[m] for m in grp]
-            counts["lift"] += emit_gprod(b, tab, Mi, sub, ins,
-                                         lambda k, w: f"double bf[kU]; smem_b(x, Y, {w}, bf);", fbase=lift0)
-            b(f"        store_q2(x, Qt, {row_word64(outs[grp[0]])}, {row_word64(outs[grp[1]]) if len(grp) > 1 else '~0ULL'}, acc, qc);")
-            b("      }")
-        b("    }")
-    b("  }")
     # paired lift: faces 2P and 2P+1 accumulate into the same registers, one Q update per pair
-    b(f"  // paired lift + Q update: Q += R^(2P) Ya + R^(2P+1) Yb")
+    b(f"  // paired lift + Q update (flux kernel layout): Q += R^(2P) Ya + R^(2P+1) Yb")
     b(f"  template <int P> static __device__ __forceinline__ void lift2(Ctx& x, const double* Ya, const double* Yb, double* Qt) {{")
     for P in range(2):
         b(f"    {'if' if P == 0 else 'else if'} constexpr (P == {P}) {{")
         b("      double2 qn[2][kU];")
         g0 = groups[0]
-        b(f"      load_q2(x, Qt, {row_word64(outs[g0[0]])}, {row_word64(outs[g0[1]]) if len(g0) > 1 else '~0ULL'}, qn);")
+        b(f"      load_qf(x, Qt, {row_word64(outs[g0[0]])}, {row_word64(outs[g0[1]]) if len(g0) > 1 else '~0ULL'}, qn);")
         for gi, grp in enumerate(groups):
             b("      {")
             b("        double2 qc[2][kU];")
             b("        copy_q2(qn, qc);")
             if gi + 1 < len(groups):
                 g1 = groups[gi + 1]
-                b(f"        load_q2(x, Qt, {row_word64(outs[g1[0]])}, {row_word64(outs[g1[1]]) if len(g1) > 1 else '~0ULL'}, qn);")
+                b(f"        load_qf(x, Qt, {row_word64(outs[g1[0]])}, {row_word64(outs[g1[1]]) if len(g1) > 1 else '~0ULL'}, qn);")
             b("        double acc[2][kU][2];")
             b("        zero_acc(acc);")
             sub = [outs[m] for m in grp]
             for i, yv in ((2 * P, "Ya"), (2 * P + 1, "Yb")):
                 Mi = lambda r, col, i=i: R[i][r][col]
                 b("        {")
-                emit_gprod(b, tab, Mi, sub, tl["in"][i],
-                           lambda k, w, yv=yv: f"double bf[kU]; smem_b(x, {yv}, {w}, bf);", fbase=lift0)
+                counts["lift"] += emit_gprod(b, tab, Mi, sub, tl["in"][i],
+                                             lambda k, w, yv=yv: f"double bf[kU]; smem_bf(x, {yv}, {w}, bf);", fbase=lift0)
                 b("        }")
-            b(f"        store_q2(x, Qt, {row_word64(outs[grp[0]])}, {row_word64(outs[grp[1]]) if len(grp) > 1 else '~0ULL'}, acc, qc);")
+            b(f"        store_qf(x, Qt, {row_word64(outs[grp[0]])}, {row_word64(outs[grp[1]]) if len(grp) > 1 else '~0ULL'}, acc, qc);")
             b("      }")
         b("    }")
     b("  }")
@@ -464,7 +437,7 @@ def gen_order(N):
             assert abs(f[2][m][n] - S[m] * f[0][m][n] * S[n]) < 1e-14
     b("  // z = f^h t (P:1342) for every lane's own h, without divergence (f^1 = S diagonal,")
     b("  // f^2 = S f^0 S); row m goes to Y[m][col] (swizzled rows of the flux staging)")
-    b(f"  static __device__ __forceinline__ void rot(int h, double (&t)[{Bt}], double* Y, int col) {{")
+    b(f"  static __device__ __forceinline__ void rotf(int h, double (&t)[{Bt}], double* Y, int col) {{")
     b("    const bool fl = h != 0, id = h == 1, s2 = h == 2;")
     for n in range(Bt):
         if S[n] < 0:
@@ -476,9 +449,9 @@ def gen_order(N):
             expr = f"{float(v)!r} * t[{n}]" if expr is None else f"fma({float(v)!r}, t[{n}], {expr})"
         b(f"    {{ const double u = {expr or '0.0'};")
         if S[m] < 0:
-            b(f"      Y[swz({m}, col)] = id ? t[{m}] : (s2 ? -u : u); }}")
+            b(f"      Y[swzf({m}, col)] = id ? t[{m}] : (s2 ? -u : u); }}")
         else:
-            b(f"      Y[swz({m}, col)] = id ? t[{m}] : u; }}")
+            b(f"      Y[swzf({m}, col)] = id ? t[{m}] : u; }}")
     b("  }")
     lines = [f"// GENERATED by paper_1903_11521_b200/gen/dmma.py for N = {N} -- do not edit.",
              "#pragma once", "namespace ydg {", "namespace dm {", f"template <> struct DG<{N}> {{",
