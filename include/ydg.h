@@ -79,6 +79,10 @@ const char* ydg_last_error(void);
  *  Rank r owns global elements [r*ne/nranks, (r+1)*ne/nranks) (the generator orders
  *  elements z-major, so ranges are slabs).  NCCL is loaded at run time (libnccl.so.2). */
 int ydg_set_comm(ydg_solver* h, int rank, int nranks, const void* nccl_unique_id);
+/*  A unique id whose first 7 bytes are "YDGLOOP" selects the loopback transport instead of
+ *  NCCL: the ranks are handles of one process (one host thread each) on one GPU, the halo
+ *  goes device-to-device at host barriers -- for checking partition invariance on a single
+ *  GPU; same plan, pack and unpack as the NCCL path. */
 
 /* Upload the (global) mesh and material; builds geometry, star matrices, flux solvers and
  * the neighbour relation (Neigh, Face, Rot of P:1342) on the host in fp64.

@@ -812,7 +812,9 @@ int ydg_query(ydg_solver* h, int what, double* v) {
     case YDG_Q_N_ELEMENTS: *v = static_cast<double>(h->ne); break;
     case YDG_Q_FIRST_LOCAL: *v = static_cast<double>(h->first); break;
     case YDG_Q_N_LOCAL: *v = static_cast<double>(h->nlocal); break;
-    case YDG_Q_NZ_FLOPS: *v = nz_flops_elastic(h->N, h->prec == 8); break;
+    // canonical formulation of P:1312-1342 (local and neighbour flux with their own lifts,
+    // DESIGN.md R22); the fp64 kernels execute fewer (one lift per face) -- not counted
+    case YDG_Q_NZ_FLOPS: *v = nz_flops_elastic(h->N, false); break;
     case YDG_Q_ALG_BYTES: *v = alg_bytes_local(h) + alg_bytes_neigh(h); break;
     case YDG_Q_B: *v = h->B; break;
     case YDG_Q_BTILDE: *v = h->Bt; break;
@@ -820,8 +822,10 @@ int ydg_query(ydg_solver* h, int what, double* v) {
     case YDG_Q_LAUNCHES_PER_STEP: *v = h->nranks > 1 ? 5 : 2; break;
     case YDG_Q_LOCAL_BYTES: *v = alg_bytes_local(h); break;
     case YDG_Q_NEIGH_BYTES: *v = alg_bytes_neigh(h); break;
+    // fp64: the local kernel runs CK, time integral, volume, traces; both flux terms are in
+    // the flux kernel.  fp32: the local flux is in the local kernel.
     case YDG_Q_LOCAL_FLOPS: *v = nz_flops_local(h->N, h->prec == 8); break;
-    case YDG_Q_NEIGH_FLOPS: *v = nz_flops_elastic(h->N, h->prec == 8) - nz_flops_local(h->N, h->prec == 8); break;
+    case YDG_Q_NEIGH_FLOPS: *v = nz_flops_elastic(h->N, false) - nz_flops_local(h->N, h->prec == 8); break;
     default: return fail(h, YDG_ERR_ARG, "unknown query");
   }
   return YDG_OK;

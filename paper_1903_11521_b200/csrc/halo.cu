@@ -2,6 +2,11 @@
 // dependency (inside a torch process the already-loaded torch NCCL is reused).
 #include "halo.h"
 
+#include <condition_variable>
+#include <map>
+#include <memory>
+#include <mutex>
+
 #include <dlfcn.h>
 
 #include <algorithm>
@@ -150,9 +155,57 @@ bool plan_halo(const Neighbours& nbr, int64_t ne, int rank, int nranks, HaloPlan
   return true;
 }
 
+// ---- loopback transport (tests): several ranks as handles of one process on one GPU,
+// selected by a unique id starting with "YDGLOOP".  The exchange packs, meets the other
+// ranks at a host barrier, copies each peer's packed segment device-to-device and meets
+// again before anyone repacks -- the same plan, pack and unpack as the NCCL path, so a
+// partitioned run can be checked bit for bit against one rank on a single GPU.
+struct LoopGroup {
+  std::mutex mu;
+  std::condition_variable cv;
+  int nranks = 0, arrived = 0;
+  int64_t generation = 0;
+  std::vector<Halo*> members;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const int64_t gen = generation;
+    if (++arrived == nranks) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen; });
+    }
+  }
+};
+namespace {
+std::mutex g_loop_mu;
+std::map<std::string, std::shared_ptr<LoopGroup>> g_loops;
+}  // namespace
+
 int Halo::init(int rank, int nranks, const void* uid, std::string* err) {
   rank_ = rank;
   nranks_ = nranks;
+  if (std::memcmp(uid, "YDGLOOP", 7) == 0) {
+    const std::string key(static_cast<const char*>(uid), 128);
+    {
+      std::lock_guard<std::mutex> lk(g_loop_mu);
+      auto& g = g_loops[key];
+      if (!g) {
+        g = std::make_shared<LoopGroup>();
+        g->nranks = nranks;
+        g->members.assign(nranks, nullptr);
+      }
+      if (g->nranks != nranks || g->members[rank]) { *err = "loopback group mismatch"; return 4; }
+      g->members[rank] = this;
+      loop_ = g;
+    }
+    cudaError_t e = cudaStreamCreateWithFlags(&cstream_, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ready_, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&done_, cudaEventDisableTiming);
+    if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
+    return 0;
+  }
   if (!g_nccl.load(err)) return 4;
   NcclUid id;
   std::memcpy(&id, uid, sizeof(id));
@@ -215,6 +268,25 @@ int Halo::exchange(cudaStream_t s, void* traces, int elem_bytes, std::string* er
   }
   if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
   const size_t bytes_per = static_cast<size_t>(vals_) * eb_;
+  if (loop_) {
+    e = cudaStreamSynchronize(cstream_);  // own pack done
+    if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
+    loop_->barrier();                     // every rank's pack done
+    for (size_t k = 0; k < plan_.peers.size(); ++k) {
+      const Halo* ph = loop_->members[plan_.peers[k]];
+      const auto it = std::find(ph->plan_.peers.begin(), ph->plan_.peers.end(), rank_);
+      if (it == ph->plan_.peers.end()) { *err = "loopback peer without a segment"; return 4; }
+      const size_t idx = static_cast<size_t>(it - ph->plan_.peers.begin());
+      if (ph->plan_.send_cnt[idx] != plan_.recv_cnt[k]) { *err = "loopback segment size mismatch"; return 4; }
+      e = cudaMemcpyAsync(static_cast<char*>(d_recv_buf_) + plan_.recv_off[k] * bytes_per,
+                          static_cast<const char*>(ph->d_send_buf_) + ph->plan_.send_off[idx] * bytes_per,
+                          plan_.recv_cnt[k] * bytes_per, cudaMemcpyDeviceToDevice, cstream_);
+      if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
+    }
+    e = cudaStreamSynchronize(cstream_);
+    if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
+    loop_->barrier();  // every copy done before anyone repacks
+  } else {
   int r = g_nccl.gstart();
   for (size_t k = 0; r == 0 && k < plan_.peers.size(); ++k) {
     const char* sb = static_cast<const char*>(d_send_buf_) + plan_.send_off[k] * bytes_per;
@@ -225,6 +297,7 @@ int Halo::exchange(cudaStream_t s, void* traces, int elem_bytes, std::string* er
   }
   int r2 = g_nccl.gend();
   if (r || r2) { *err = std::string("NCCL: ") + g_nccl.errstr(r ? r : r2); return 4; }
+  }
   if (ng) {
     if (elem_bytes == 8)
       unpack_kernel<unsigned long long><<<148 * 4, 256, 0, cstream_>>>(
@@ -257,6 +330,16 @@ void Halo::destroy() {
   d_recv_buf_ = nullptr;
   if (comm_ && g_nccl.destroy) g_nccl.destroy(comm_);
   comm_ = nullptr;
+  if (loop_) {
+    std::lock_guard<std::mutex> lk(g_loop_mu);
+    loop_->members[rank_] = nullptr;
+    bool empty = true;
+    for (Halo* m : loop_->members) empty = empty && !m;
+    if (empty)
+      for (auto it = g_loops.begin(); it != g_loops.end(); ++it)
+        if (it->second == loop_) { g_loops.erase(it); break; }
+    loop_.reset();
+  }
   if (ready_) cudaEventDestroy(ready_);
   if (done_) cudaEventDestroy(done_);
   if (cstream_) cudaStreamDestroy(cstream_);

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -29,6 +30,8 @@ struct HaloPlan {
 // Peers own ranges [r*ne/nranks, (r+1)*ne/nranks).
 bool plan_halo(const Neighbours& nbr, int64_t ne, int rank, int nranks, HaloPlan* out,
                std::string* err);
+
+struct LoopGroup;
 
 class Halo {
  public:
@@ -57,6 +60,7 @@ class Halo {
   void* d_recv_buf_ = nullptr;
   int vals_ = 0, eb_ = 0, Bt_ = 0, P_ = 0, TS_ = 0, L_ = 32;
   int64_t owned_slots_ = 0;
+  std::shared_ptr<LoopGroup> loop_;  // loopback transport (unique id "YDGLOOP...")
 };
 
 }  // namespace ydg
