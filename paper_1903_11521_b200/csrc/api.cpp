@@ -357,6 +357,8 @@ int upload_csr(ydg_solver* h) {
     *m.ptr = static_cast<const int*>(dp);
     *m.col = static_cast<const int*>(dc);
     *m.val = static_cast<const double*>(dv);
+    if (m.ptr == &g.kt_ptr) g.kt_nnz = static_cast<int>(val.size());
+    if (m.ptr == &g.kh_ptr) g.kh_nnz = static_cast<int>(val.size());
   }
   return YDG_OK;
 }

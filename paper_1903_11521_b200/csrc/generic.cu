@@ -39,10 +39,10 @@ __device__ __forceinline__ int idx3(int k, int p, int e) { return (k * P + p) * 
 // acc[p] += sum over CSR row `row` of M: val * W[col][p][e], p < PO (W has PW quantities)
 template <int PO, int PW>
 __device__ __forceinline__ void csr_row(const Csr& M, int row, const double* W, int e, double (&acc)[PO]) {
-  const int t1 = __ldg(M.ptr + row + 1);
-  for (int t = __ldg(M.ptr + row); t < t1; ++t) {
-    const double v = __ldg(M.val + t);
-    const double* w = W + idx3<PW>(__ldg(M.col + t), 0, e);
+  const int t1 = M.ptr[row + 1];
+  for (int t = M.ptr[row]; t < t1; ++t) {
+    const double v = M.val[t];
+    const double* w = W + idx3<PW>(M.col[t], 0, e);
 #pragma unroll
     for (int p = 0; p < PO; ++p) acc[p] = fma(v, w[p * kTE], acc[p]);
   }
@@ -69,24 +69,49 @@ __device__ __forceinline__ void make_x(const double* D, const double* ST, double
   }
 }
 
-template <int P>
+// Shared-memory copy of a CSR matrix (values, then columns, then row pointers).
+__device__ __forceinline__ Csr stage_csr(const Csr& g, int rows, int nnz, double* dst) {
+  double* val = dst;
+  int* col = reinterpret_cast<int*>(val + nnz);
+  int* ptr = col + nnz;
+  for (int i = threadIdx.x; i < nnz; i += blockDim.x) {
+    val[i] = g.val[i];
+    col[i] = g.col[i];
+  }
+  for (int i = threadIdx.x; i <= rows; i += blockDim.x) ptr[i] = g.ptr[i];
+  return Csr{ptr, col, val};
+}
+__host__ __device__ __forceinline__ int csr_doubles(int rows, int nnz) { return nnz + (nnz + rows + 2) / 2 + 1; }
+
+// Persistent over groups of kTE elements; KSM: the CK and volume CSR matrices staged in
+// shared memory once per CTA (when they fit).
+template <int P, bool KSM>
 __global__ void __launch_bounds__(256) gen_local(const GenParams prm) {
   constexpr int kG = P / 9;  // groups of 9 quantity columns per (row, element): one thread each
   extern __shared__ double sm[];
   const int B = prm.B, Bt = prm.Bt;
   const int SZ = B * P * kTE;
-  double* D = sm;
+  const int XS = 3 * SZ > 4 * Bt * (9 + P) * kTE ? 3 * SZ : 4 * Bt * (9 + P) * kTE;
+  double* const base = sm;
+  double* ST = base + 3 * SZ + XS;     // [kTE][3][P][3] star coefficients
+  double* SRC = ST + kTE * 3 * P * 3;  // [kTE][P][9] source coefficients (P = 27)
+  Csr Kt{prm.kt_ptr, prm.kt_col, prm.kt_val}, Kh{prm.kh_ptr, prm.kh_col, prm.kh_val};
+  if (KSM) {
+    double* c0 = SRC + kTE * P * 9;
+    Kt = stage_csr(Kt, 3 * B, prm.kt_nnz, c0);
+    Kh = stage_csr(Kh, 3 * B, prm.kh_nnz, c0 + csr_doubles(3 * B, prm.kt_nnz));
+  }
+  const Csr Rt{prm.rt_ptr, prm.rt_col, prm.rt_val}, R{prm.r_ptr, prm.r_col, prm.r_val};
+  const int64_t nblk = (prm.n + kTE - 1) / kTE;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+  double* D = base;
   double* Dn = D + SZ;
   double* I = Dn + SZ;
   double* X = I + SZ;                  // [3][B][P][kTE]; later: traces / flux staging
-  const int XS = 3 * SZ > 4 * Bt * (9 + P) * kTE ? 3 * SZ : 4 * Bt * (9 + P) * kTE;
-  double* ST = X + XS;                 // [kTE][3][P][3] star coefficients
-  double* SRC = ST + kTE * 3 * P * 3;  // [kTE][P][9] source coefficients (P = 27)
-  const int64_t e0 = prm.e0 + static_cast<int64_t>(blockIdx.x) * kTE;
+  const int64_t e0 = prm.e0 + blk * kTE;
   const int64_t left = prm.e0 + prm.n - e0;
   const int ne = static_cast<int>(left < kTE ? left : kTE);
-  const Csr Kt{prm.kt_ptr, prm.kt_col, prm.kt_val}, Kh{prm.kh_ptr, prm.kh_col, prm.kh_val};
-  const Csr Rt{prm.rt_ptr, prm.rt_col, prm.rt_val}, R{prm.r_ptr, prm.r_col, prm.r_val};
+  __syncthreads();  // previous group done with the shared regions
   // load Q, I = dt Q, coefficients
   for (int i = threadIdx.x; i < SZ; i += blockDim.x) {
     const int e = i % kTE, kp = i / kTE, p = kp % P, k = kp / P;
@@ -206,6 +231,7 @@ __global__ void __launch_bounds__(256) gen_local(const GenParams prm) {
 #pragma unroll
       for (int q = 0; q < 9; ++q) prm.Q[((e0 + e) * P + 9 * g + q) * B + k] += s[q];
   }
+  }  // element groups
 }
 
 template <int P>
@@ -278,6 +304,11 @@ size_t gen_local_smem(int B, int Bt, int P) {
   const size_t coef = static_cast<size_t>(gen::kTE) * (3 * P * 3 + P * 9);
   return (3 * SZ + (3 * SZ > extra ? 3 * SZ : extra) + coef) * sizeof(double);
 }
+static size_t gen_local_smem_ksm(const GenParams& p) {
+  return gen_local_smem(p.B, p.Bt, p.P) +
+         (gen::csr_doubles(3 * p.B, p.kt_nnz) + gen::csr_doubles(3 * p.B, p.kh_nnz)) * sizeof(double);
+}
+static bool gen_ksm(const GenParams& p) { return gen_local_smem_ksm(p) <= 227 * 1024; }
 size_t gen_neigh_smem(int Bt, int P) {
   return (static_cast<size_t>(4) * Bt * 9 * gen::kTE + static_cast<size_t>(4) * Bt * P * gen::kTE) * sizeof(double);
 }
@@ -285,10 +316,13 @@ size_t gen_neigh_smem(int Bt, int P) {
 cudaError_t gen_configure(int B, int Bt, int P, const int (*ecols)[9], const int (*scols)[3]) {
   cudaError_t e = cudaMemcpyToSymbol(gen::c_ecols, ecols, sizeof(int) * 27 * 9);
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(gen::c_scols, scols, sizeof(int) * 27 * 3);
-  const void* fl = P == 27 ? reinterpret_cast<const void*>(&gen::gen_local<27>) : reinterpret_cast<const void*>(&gen::gen_local<9>);
+  const void* fls[4] = {reinterpret_cast<const void*>(&gen::gen_local<9, false>),
+                        reinterpret_cast<const void*>(&gen::gen_local<9, true>),
+                        reinterpret_cast<const void*>(&gen::gen_local<27, false>),
+                        reinterpret_cast<const void*>(&gen::gen_local<27, true>)};
   const void* fn = P == 27 ? reinterpret_cast<const void*>(&gen::gen_neigh<27>) : reinterpret_cast<const void*>(&gen::gen_neigh<9>);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(fl, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gen_local_smem(B, Bt, P)));
+  for (int i = (P == 27 ? 2 : 0); e == cudaSuccess && i < (P == 27 ? 4 : 2); ++i)
+    e = cudaFuncSetAttribute(fls[i], cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gen_neigh_smem(Bt, P)));
   return e;
@@ -299,8 +333,18 @@ cudaError_t gen_launch(const GenParams& p, bool local, cudaStream_t s) {
   if (blocks <= 0) return cudaSuccess;
   const unsigned nb = static_cast<unsigned>(blocks);
   if (local) {
-    if (p.P == 27) gen::gen_local<27><<<nb, 256, gen_local_smem(p.B, p.Bt, p.P), s>>>(p);
-    else gen::gen_local<9><<<nb, 256, gen_local_smem(p.B, p.Bt, p.P), s>>>(p);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const unsigned g = static_cast<unsigned>(blocks < sms ? blocks : sms);  // persistent
+    const bool ksm = gen_ksm(p);
+    const size_t smem = ksm ? gen_local_smem_ksm(p) : gen_local_smem(p.B, p.Bt, p.P);
+    if (p.P == 27) {
+      if (ksm) gen::gen_local<27, true><<<g, 256, smem, s>>>(p);
+      else gen::gen_local<27, false><<<g, 256, smem, s>>>(p);
+    } else {
+      if (ksm) gen::gen_local<9, true><<<g, 256, smem, s>>>(p);
+      else gen::gen_local<9, false><<<g, 256, smem, s>>>(p);
+    }
   } else {
     if (p.P == 27) gen::gen_neigh<27><<<nb, 256, gen_neigh_smem(p.Bt, p.P), s>>>(p);
     else gen::gen_neigh<9><<<nb, 256, gen_neigh_smem(p.Bt, p.P), s>>>(p);

@@ -17,6 +17,7 @@ struct GenParams {
   const int8_t* jh;     // [e][4]  j | h << 2
   const int *kt_ptr, *kt_col, *kh_ptr, *kh_col, *rt_ptr, *rt_col, *r_ptr, *r_col, *f_ptr, *f_col;
   const double *kt_val, *kh_val, *rt_val, *r_val, *f_val;
+  int kt_nnz, kh_nnz;   // nonzeros of the CK / volume CSR matrices (staged in shared memory)
   int N, B, Bt, P;
   int64_t e0, n;        // element range of this launch
   double dt;
