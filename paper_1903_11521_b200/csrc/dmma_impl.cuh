@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_local(const __grid_consta
     // traces T_F = R^FT I of the four faces -> staging -> one TMA bulk store per face;
     // they read Q^n (rows >= IROWS of I from global memory), so they precede the update
     double* gtr = prm.traces + tile * 4 * Lay::FACE;
-    constexpr int F0 = G::TR01_DFMA ? 2 : 0;
+    constexpr int F0 = G::TR23_DFMA ? 4 : (G::TR01_DFMA ? 2 : 0);
     if constexpr (G::TR01_DFMA) {
       G::trace01(x, stg0, stg1);  // faces 0 and 1: sparse DFMA
       fence_proxy_async();
@@ -660,6 +660,17 @@ __global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_local(const __grid_consta
       if (threadIdx.x == 0) {
         bulk_s2g(gtr, stg0, Lay::FACE * sizeof(double));
         bulk_s2g(gtr + Lay::FACE, stg1, Lay::FACE * sizeof(double));
+      }
+    }
+    if constexpr (G::TR23_DFMA) {
+      if (threadIdx.x == 0) bulk_wait_read<0>();  // faces 0, 1 have left the staging blocks
+      __syncthreads();
+      G::trace23(x, stg0, stg1);  // faces 2 and 3: sparse DFMA
+      fence_proxy_async();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        bulk_s2g(gtr + 2 * Lay::FACE, stg0, Lay::FACE * sizeof(double));
+        bulk_s2g(gtr + 3 * Lay::FACE, stg1, Lay::FACE * sizeof(double));
       }
     }
 #pragma unroll

@@ -172,8 +172,9 @@ def emit_gprod(b, tab, M, outs, ins, loader, acc="acc", fbase=None):
 
 # CK steps with at most this many output rows run as sparse DFMA code (CTA-wide)
 DFMA_CK_ROWS = int(os.environ.get("YDG_GEN_CKROWS", "20"))
-# faces 0 and 1 traces as sparse DFMA code (else tensor cores)
+# faces 0 and 1 traces as sparse DFMA code (else tensor cores); faces 2 and 3 as well
 DFMA_TR01 = os.environ.get("YDG_GEN_TR01", "1") == "1"
+DFMA_TR23 = os.environ.get("YDG_GEN_TR23", "0") == "1"
 DFMA_TAIL_ROWS = 0   # CK steps d >= 1 from the first with at most this many output rows on:
                      # one warp-synchronous sparse DFMA phase (0 = off: the element-grouped
                      # lanes hit 9-way shared-memory bank conflicts, measured slower)
@@ -256,29 +257,30 @@ def emit_ck_tail(b, d0, N, K):
     return -n
 
 
-def emit_trace01_dfma(b, R, B, Bt, IROWS, TS):
-    """Traces of the two sparsest faces (0, 1) as constant-coefficient DFMAs, one thread per
-    data column: T_F[m] = sum_k R^F[k][m] I[k] over the nonzeros, both faces from one pass
-    over the column; results go to the two staging blocks [lane][m][q]."""
+def emit_trace01_dfma(b, R, B, Bt, IROWS, TS, faces=(0, 1), fname="trace01"):
+    """Traces of two faces (the two sparsest, 0 and 1, by default) as constant-coefficient
+    DFMAs, one thread per data column: T_F[m] = sum_k R^F[k][m] I[k] over the nonzeros, both
+    faces from one pass over the column; results go to the two staging blocks [lane][m][q]."""
     n = 0
-    b("  // traces of faces 0 and 1 (sparse DFMA, one thread per data column)")
-    b("  static __device__ __forceinline__ void trace01(Ctx& x, double* stg0, double* stg1) {")
+    fa, fb = faces
+    b(f"  // traces of faces {fa} and {fb} (sparse DFMA, one thread per data column)")
+    b(f"  static __device__ __forceinline__ void {fname}(Ctx& x, double* stg0, double* stg1) {{")
     b("    if (x.cc >= kRS) return;")
     b(f"    double t0[{Bt}], t1[{Bt}];")
     b(f"    for (int m = 0; m < {Bt}; ++m) t0[m] = t1[m] = 0.0;")
-    gk = [k for k in range(IROWS, B) if any(R[F][k][m] != 0.0 for F in (0, 1) for m in range(Bt))]
+    gk = [k for k in range(IROWS, B) if any(R[F][k][m] != 0.0 for F in faces for m in range(Bt))]
     if gk:  # rows >= IROWS (dt * Q, global memory): all loads first, latency under the smem rows
         b(f"    double qg[{len(gk)}];")
         for i, k in enumerate(gk):
             b(f"    qg[{i}] = ld_stream(x.Qt + {k} * kRS + x.cc);")
     for k in list(range(IROWS)) + gk:
-        terms = [(F, m, R[F][k][m]) for F in (0, 1) for m in range(Bt) if R[F][k][m] != 0.0]
+        terms = [(j, m, R[F][k][m]) for j, F in enumerate(faces) for m in range(Bt) if R[F][k][m] != 0.0]
         if not terms:
             continue
         src = f"x.I[swz({k}, x.cc)]" if k < IROWS else f"x.dt * qg[{gk.index(k)}]"
         b(f"    {{ const double ik = {src};")
-        for F, m, v in terms:
-            b(f"      t{F}[{m}] = fma({float(v)!r}, ik, t{F}[{m}]);")
+        for j, m, v in terms:
+            b(f"      t{j}[{m}] = fma({float(v)!r}, ik, t{j}[{m}]);")
             n += 1
         b("    }")
     b(f"    for (int m = 0; m < {Bt}; ++m) {{")
@@ -363,7 +365,9 @@ def gen_order(N):
     b("  }")
     # ---------------- traces T_i = R^iT I
     counts["tr01_dfma"] = emit_trace01_dfma(b, R, B, Bt, IROWS, TS) if DFMA_TR01 else 0
+    counts["tr23_dfma"] = emit_trace01_dfma(b, R, B, Bt, IROWS, TS, (2, 3), "trace23") if DFMA_TR01 and DFMA_TR23 else 0
     b(f"  static constexpr bool TR01_DFMA = {'true' if DFMA_TR01 else 'false'};")
+    b(f"  static constexpr bool TR23_DFMA = {'true' if DFMA_TR01 and DFMA_TR23 else 'false'};")
     b(f"  // trace: T_F = R^FT I (rows < IROWS of I from shared memory, dt * Q from global memory);")
     b(f"  // the C fragments go to the staging block [lane][m][q] (stride TS)")
     b(f"  template <int F> static __device__ __forceinline__ void trace(Ctx& x, double* stg) {{")
