@@ -56,6 +56,31 @@ class Table:
         return len(self.frags) - 1
 
 
+class Pool:
+    """fp64 coefficients of the sparse DFMA code, placed in a __constant__ array so that each
+    DFMA reads its coefficient as a constant-bank operand (a literal would cost two uniform
+    register moves per DFMA: there are no 64-bit immediates)."""
+
+    def __init__(self, name):
+        self.name = name
+        self.vals = []
+        self.index = {}
+
+    def __call__(self, v):
+        v = float(v)
+        if v not in self.index:
+            self.index[v] = len(self.vals)
+            self.vals.append(v)
+        return f"{self.name}[{self.index[v]}]"
+
+
+POOL = None
+
+
+def lit(v):
+    return POOL(v) if POOL is not None else repr(float(v))
+
+
 def pad_rows(g, n):
     return list(g) + [None] * (n - len(g))
 
@@ -205,7 +230,7 @@ def emit_ck_dfma(b, d, K, bi, bo, IROWS):
     for l in sorted(nz):
         b(f"      {{ double x0, x1, x2; col_x<{src}, B>(x, {l}, x.ce, ca, q0, q1, q2, x0, x1, x2);")
         for c, k, v in nz[l]:
-            b(f"        y[{k}] = fma({float(v)!r}, x{c}, y[{k}]);")
+            b(f"        y[{k}] = fma({lit(v)}, x{c}, y[{k}]);")
         b("      }")
     b("    }")
     b("    __syncthreads();  // every read of D^d done")
@@ -245,7 +270,7 @@ def emit_ck_tail(b, d0, N, K):
         for l in sorted(nz):
             b(f"        {{ double x0, x1, x2; col_x<SRC_S, B>(x, {l}, x.te, ca, q0, q1, q2, x0, x1, x2);")
             for c, k, v in nz[l]:
-                b(f"          y[{k}] = fma({float(v)!r}, x{c}, y[{k}]);")
+                b(f"          y[{k}] = fma({lit(v)}, x{c}, y[{k}]);")
             b("        }")
         b("      }")
         b("      __syncwarp();  // every read of the element's D^d done")
@@ -280,7 +305,7 @@ def emit_trace01_dfma(b, R, B, Bt, IROWS, TS, faces=(0, 1), fname="trace01"):
         src = f"x.I[swz({k}, x.cc)]" if k < IROWS else f"x.dt * qg[{gk.index(k)}]"
         b(f"    {{ const double ik = {src};")
         for j, m, v in terms:
-            b(f"      t{j}[{m}] = fma({float(v)!r}, ik, t{j}[{m}]);")
+            b(f"      t{j}[{m}] = fma({lit(v)}, ik, t{j}[{m}]);")
             n += 1
         b("    }")
     b(f"    for (int m = 0; m < {Bt}; ++m) {{")
@@ -292,6 +317,8 @@ def emit_trace01_dfma(b, R, B, Bt, IROWS, TS, faces=(0, 1), fname="trace01"):
 
 
 def gen_order(N):
+    global POOL
+    POOL = Pool(f"cdf_N{N}")
     t = tables.load(N)
     K, R, f = t["K"], t["R"], t["f"]
     B, Bt = t["B"], t["Bt"]
@@ -450,6 +477,7 @@ def gen_order(N):
         terms = [(n, f[0][m][n]) for n in range(Bt) if f[0][m][n] != 0.0]
         expr = None
         for n, v in terms:
+            # literals here: the flux kernel's register budget (constant-bank operands spilled)
             expr = f"{float(v)!r} * t[{n}]" if expr is None else f"fma({float(v)!r}, t[{n}], {expr})"
         b(f"    {{ const double u = {expr or '0.0'};")
         if S[m] < 0:
@@ -457,8 +485,14 @@ def gen_order(N):
         else:
             b(f"      Y[swzf({m}, col)] = id ? t[{m}] : u; }}")
     b("  }")
+    pool = POOL.vals or [0.0]
+    cdecl = [f"// coefficients of the sparse DFMA code (constant-bank operands)",
+             f"__constant__ double cdf_N{N}[{len(pool)}] = {{"]
+    for s0 in range(0, len(pool), 6):
+        cdecl.append("  " + ", ".join(repr(v) for v in pool[s0:s0 + 6]) + ",")
+    cdecl.append("};")
     lines = [f"// GENERATED by paper_1903_11521_b200/gen/dmma.py for N = {N} -- do not edit.",
-             "#pragma once", "namespace ydg {", "namespace dm {", f"template <> struct DG<{N}> {{",
+             "#pragma once", "namespace ydg {", "namespace dm {"] + cdecl + [f"template <> struct DG<{N}> {{",
              f"  static constexpr int N = {N}, B = {B}, Bt = {Bt}, Bv = {Bv};",
              f"  static constexpr int SROWS = {SROWS};  // rows of S (D^d, d >= 1)",
              f"  static constexpr int IROWS = {IROWS};  // rows of the time-integral region",
