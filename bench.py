@@ -336,7 +336,9 @@ def run_ydg(args):
     ach_neigh = fl_neigh * nloc / (avg_neigh / 1e3) / 1e12
     # kernel names as ncu lists them: fp64 elastic = tensor-core kernels, fp32 = sparse FFMA
     # kernels, viscoelastic / N=6 fp64 = generic kernels
-    if cfg.P == 27 or (cfg.precision == 8 and cfg.N == 6):
+    if cfg.P == 27 and cfg.N <= 4 and os.environ.get("YDG_VISCO_GENERIC") != "1":
+        k_loc, k_nb, bound = "vm_local", "gen_neigh", "tensor"  # viscoelastic tensor-core local kernel
+    elif cfg.P == 27 or (cfg.precision == 8 and cfg.N == 6):
         k_loc, k_nb, bound = "gen_local", "gen_neigh", "alu"
     elif cfg.precision == 8:
         k_loc, k_nb, bound = "dm_local", "dm_flux", "tensor"

@@ -53,6 +53,7 @@ struct ydg_solver {
   int64_t bnd_lo = 0, bnd_hi = 0;  // leading / trailing owned tiles covering all tiles with ghosts
   // generic path (viscoelastic, or YDG_GENERIC=1): canonical layouts, CSR global matrices
   bool generic = false;
+  bool visco_tc = false;    // viscoelastic local kernel on FP64 tensor cores (visco.cu)
   void* src = nullptr;      // [e][p][9] viscoelastic source pattern values
   int64_t* nb64 = nullptr;  // [e][4]
   int8_t* jh_e = nullptr;   // [e][4]
@@ -468,7 +469,7 @@ int generic_step(ydg_solver* h, double dt, int nsteps, cudaStream_t s) {
   g.e0 = 0;
   g.n = h->ne;
   for (int n = 0; n < nsteps; ++n) {
-    CUDA_OR_FAIL(h, timed(h, 0, s, [&] { return gen_launch(g, true, s); }));
+    CUDA_OR_FAIL(h, timed(h, 0, s, [&] { return h->visco_tc ? visco_launch_local(g, s) : gen_launch(g, true, s); }));
     CUDA_OR_FAIL(h, timed(h, 1, s, [&] { return gen_launch(g, false, s); }));
   }
   return YDG_OK;
@@ -509,6 +510,9 @@ int ydg_create(int order, int quantities, int precision, int cuda_device, ydg_so
       int ecols[27][9], scols[27][3];
       generic_patterns(ecols, scols);
       e = gen_configure(h->B, h->Bt, quantities, ecols, scols);
+      const char* vg = std::getenv("YDG_VISCO_GENERIC");  // 1: CSR local kernel (comparison)
+      h->visco_tc = visco_supported(order, quantities) && !(vg && vg[0] == '1');
+      if (e == cudaSuccess && h->visco_tc) e = visco_configure(order, scols);
     } else {
       e = configure_kernels(order, precision);
     }
@@ -816,7 +820,7 @@ int ydg_query(ydg_solver* h, int what, double* v) {
     case YDG_Q_N_LOCAL: *v = static_cast<double>(h->nlocal); break;
     // canonical formulation of P:1312-1342 (local and neighbour flux with their own lifts,
     // DESIGN.md R22); the fp64 kernels execute fewer (one lift per face) -- not counted
-    case YDG_Q_NZ_FLOPS: *v = nz_flops_elastic(h->N, false); break;
+    case YDG_Q_NZ_FLOPS: *v = h->P == 27 ? nz_flops_visco(h->N) : nz_flops_elastic(h->N, false); break;
     case YDG_Q_ALG_BYTES: *v = alg_bytes_local(h) + alg_bytes_neigh(h); break;
     case YDG_Q_B: *v = h->B; break;
     case YDG_Q_BTILDE: *v = h->Bt; break;
@@ -826,8 +830,11 @@ int ydg_query(ydg_solver* h, int what, double* v) {
     case YDG_Q_NEIGH_BYTES: *v = alg_bytes_neigh(h); break;
     // fp64: the local kernel runs CK, time integral, volume, traces; both flux terms are in
     // the flux kernel.  fp32: the local flux is in the local kernel.
-    case YDG_Q_LOCAL_FLOPS: *v = nz_flops_local(h->N, h->prec == 8); break;
-    case YDG_Q_NEIGH_FLOPS: *v = nz_flops_elastic(h->N, false) - nz_flops_local(h->N, h->prec == 8); break;
+    case YDG_Q_LOCAL_FLOPS: *v = h->P == 27 ? nz_flops_visco_local(h->N) : nz_flops_local(h->N, h->prec == 8); break;
+    case YDG_Q_NEIGH_FLOPS:
+      *v = h->P == 27 ? nz_flops_visco(h->N) - nz_flops_visco_local(h->N)
+                      : nz_flops_elastic(h->N, false) - nz_flops_local(h->N, h->prec == 8);
+      break;
     default: return fail(h, YDG_ERR_ARG, "unknown query");
   }
   return YDG_OK;

@@ -1,0 +1,376 @@
+// Viscoelastic (P = 27, three mechanisms) local kernel on FP64 tensor cores, orders N <= 4.
+//
+// One persistent CTA per SM walks tiles of TE = 8 consecutive elements and runs the whole
+// element-local part of one ADER-DG step (SURVEY §8 rows A3-A6 with A9; P:1312-1341 and the
+// source term of reading R14):
+//
+//   D^0 = Q;  D^{d+1} = dt/(d+1) (sum_c Ktilde^c D^d A*^cT + D^d E^T);  I = dt sum_d D^d / (d+1)
+//   Q += sum_c Khat^c I A*^cT + I E^T + sum_i R^i (R^iT I) A+_i^T;   traces T_i = R^iT I (q < 9)
+//
+// Data columns are (quantity p, element e) -> p * 8 + e, so one 8-column DMMA B operand is one
+// quantity of the tile's 8 elements.  Warp w owns the three quantities of group g(w); every
+// product with a global matrix M (Ktilde^c, Khat^c, R^i, R^iT) runs as m8n8k4 tiles over the
+// generated, zero-block-free tile lists of generated/ydg_visco.cuh, with the warp's B fragments
+// computed straight into registers from shared memory (the star / flux-solver right-multiply
+// of 4 rows at a time: X^c = D A*^cT, Y_i = T_i A+_iT) -- no intermediate ever leaves the SM.
+// The time integral I lives in the accumulator layout in registers during the recursion.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "generic.h"
+#include "generated/ydg_visco.cuh"
+
+namespace ydg {
+namespace visco {
+
+constexpr int P = 27, TE = 8, W = 9, NTH = W * 32;
+constexpr int SD = P * TE + 12;  // D / I row stride in doubles (= 4 mod 16: conflict-free k-set loads)
+constexpr int TS = 9 * TE + 12;  // trace row stride
+
+__constant__ int c_scol[27][3];  // star-matrix column pattern of each row (api.cpp generic_patterns)
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+// Quantity group of warp w (quantities 3g..3g+2): the velocity group (no source term) and the
+// source-heavy stress groups go to the sub-partitions that hold two warps, not three.
+__device__ __forceinline__ int group_of(int w) { return w == 0 ? 3 : w == 1 ? 2 : w == 2 ? 0 : w == 3 ? 1 : w; }
+
+template <int N>
+struct Ctx {
+  using V = VT<N>;
+  const double* D;     // shared: D^d (recursion) / I (volume, traces) [BR][SD]
+  const double* TR;    // shared: traces [4][BtR][TS]
+  const double* FR;    // shared: A fragments [NFRAG][32]
+  const double* st;    // global: star of the lane's element [c][p][3]
+  const double* ap;    // global: A+ of the lane's element [face][p][9]
+  int lane, k, e, p0, q;
+  int coff[3][3];      // scols[p0+u][t] * 8 + e
+  double s[3][3];      // star coefficients of the current direction
+  double a[3][9];      // flux-solver coefficients of the current face
+  double b[2][3];      // B fragments (double-buffered one k-set ahead)
+  double b1[2];
+
+  __device__ __forceinline__ void star(int c) {
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+#pragma unroll
+      for (int t = 0; t < 3; ++t) s[u][t] = st[(c * P + p0 + u) * 3 + t];
+  }
+  __device__ __forceinline__ void chunk(int buf, int ks) {
+    const double* r = D + (4 * ks + k) * SD;
+    double v[3][3];
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+#pragma unroll
+      for (int t = 0; t < 3; ++t) v[u][t] = r[coff[u][t]];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) b[buf][u] = fma(s[u][2], v[u][2], fma(s[u][1], v[u][1], s[u][0] * v[u][0]));
+  }
+  __device__ __forceinline__ void mma(double (&acc)[3][2], int f, int buf) {
+    const double af = FR[f * 32 + lane];
+    dmma(acc[0], af, b[buf][0]);
+    dmma(acc[1], af, b[buf][1]);
+    dmma(acc[2], af, b[buf][2]);
+  }
+  __device__ __forceinline__ void ib(int buf, int ks) { b1[buf] = D[(4 * ks + k) * SD + q * TE + e]; }
+  __device__ __forceinline__ void mma1(double (&acc)[2], int f, int buf) { dmma(acc, FR[f * 32 + lane], b1[buf]); }
+  __device__ __forceinline__ void acoef(int i) {
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+#pragma unroll
+      for (int j = 0; j < 9; ++j) a[u][j] = ap[(i * P + p0 + u) * 9 + j];
+  }
+  __device__ __forceinline__ void ychunk(int buf, int i, int ks) {
+    const double* r = TR + (i * V::BtR + 4 * ks + k) * TS + e;
+    double t[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) t[j] = r[j * TE];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      double y = a[u][0] * t[0];
+#pragma unroll
+      for (int j = 1; j < 9; ++j) y = fma(a[u][j], t[j], y);
+      b[buf][u] = y;
+    }
+  }
+};
+
+template <int N, class X, int M>
+__device__ __forceinline__ void ck(X& x, double (&a)[M][3][2]) {
+  if constexpr (N == 1) vck1(x, a);
+  else if constexpr (N == 2) vck2(x, a);
+  else if constexpr (N == 3) vck3(x, a);
+  else vck4(x, a);
+}
+template <int N, class X, int M>
+__device__ __forceinline__ void vol(X& x, double (&a)[M][3][2]) {
+  if constexpr (N == 1) vvol1(x, a);
+  else if constexpr (N == 2) vvol2(x, a);
+  else if constexpr (N == 3) vvol3(x, a);
+  else vvol4(x, a);
+}
+template <int N, class X, int M>
+__device__ __forceinline__ void lift(X& x, double (&a)[M][3][2]) {
+  if constexpr (N == 1) vlift1(x, a);
+  else if constexpr (N == 2) vlift2(x, a);
+  else if constexpr (N == 3) vlift3(x, a);
+  else vlift4(x, a);
+}
+template <int N, class X, int M>
+__device__ __forceinline__ void traces(X& x, double (&t)[4][M][2]) {
+  if constexpr (N == 1) vtr1(x, t);
+  else if constexpr (N == 2) vtr2(x, t);
+  else if constexpr (N == 3) vtr3(x, t);
+  else vtr4(x, t);
+}
+
+// acc(row, p0+u, e) += sum_j E_e[p0+u][j] X[row][ecol_j][e] with the source pattern of group g
+// (reading R14; generic_patterns in api.cpp): normal stresses <- 9 normal memory variables,
+// shear stresses <- 3, memory variables <- themselves, velocities: none.
+template <int M>
+__device__ __forceinline__ void source(double (&acc)[M][3][2], const int (&rows)[M], const double* X,
+                                       const double* src, int p0, int g, int ae, int ne) {
+  if (g == 2) return;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int e = ae + h;
+    const double* E = src + (e < ne ? e : ne - 1) * P * 9;
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int p = p0 + u;
+      if (g == 0) {
+        double c[9];
+#pragma unroll
+        for (int j = 0; j < 9; ++j) c[j] = E[p * 9 + j];
+#pragma unroll
+        for (int mt = 0; mt < M; ++mt) {
+          if (rows[mt] < 0) continue;
+          const double* r = X + rows[mt] * SD + e;
+          double s = acc[mt][u][h];
+#pragma unroll
+          for (int j = 0; j < 9; ++j) s = fma(c[j], r[(9 + 6 * (j / 3) + j % 3) * TE], s);
+          acc[mt][u][h] = s;
+        }
+      } else if (g == 1) {
+        double c[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) c[j] = E[p * 9 + j];
+#pragma unroll
+        for (int mt = 0; mt < M; ++mt) {
+          if (rows[mt] < 0) continue;
+          const double* r = X + rows[mt] * SD + e;
+          double s = acc[mt][u][h];
+#pragma unroll
+          for (int j = 0; j < 3; ++j) s = fma(c[j], r[(9 + 6 * j + p) * TE], s);
+          acc[mt][u][h] = s;
+        }
+      } else {
+        const double c = E[p * 9];
+#pragma unroll
+        for (int mt = 0; mt < M; ++mt)
+          if (rows[mt] >= 0) acc[mt][u][h] = fma(c, X[rows[mt] * SD + p * TE + e], acc[mt][u][h]);
+      }
+    }
+  }
+}
+
+template <int M, class F>
+__device__ __forceinline__ void rows_of(F words, int ar, int (&rows)[M]) {
+#pragma unroll
+  for (int mt = 0; mt < M; ++mt) {
+    const int r = static_cast<int>((words(mt) >> (8 * ar)) & 0xffull);
+    rows[mt] = r == 0xff ? -1 : r;
+  }
+}
+
+template <int N>
+constexpr int dsz() {  // D buffer (also holds the traces after the recursion)
+  return VT<N>::BR * SD > 4 * VT<N>::BtR * TS ? VT<N>::BR * SD : 4 * VT<N>::BtR * TS;
+}
+template <int N>
+constexpr size_t smem_bytes() {
+  return (static_cast<size_t>(dsz<N>()) + VT<N>::BR * SD + VT<N>::NFRAG * 32) * sizeof(double);
+}
+
+template <int N>
+__global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
+  using V = VT<N>;
+  constexpr int B = V::B, Bt = V::Bt;
+  extern __shared__ __align__(16) double sm[];
+  double* D = sm;                   // D^d; after the recursion: traces [4][BtR][TS], Q staging
+  double* IS = D + dsz<N>();         // time integral I
+  double* TR = D;
+  double* FR = IS + V::BR * SD;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = group_of(w), p0 = 3 * g;
+  {
+    const double* f = vfrag<N>();
+    for (int i = tid; i < V::NFRAG * 32; i += NTH) FR[i] = f[i];
+    for (int i = tid; i < dsz<N>() + V::BR * SD; i += NTH) D[i] = 0.0;  // D and I: padding rows stay zero
+  }
+  Ctx<N> x;
+  x.D = D;
+  x.TR = TR;
+  x.FR = FR;
+  x.lane = lane;
+  x.k = lane & 3;
+  x.e = lane >> 2;
+  x.p0 = p0;
+  x.q = w;  // trace column of this warp (elastic quantity w < 9)
+#pragma unroll
+  for (int u = 0; u < 3; ++u)
+#pragma unroll
+    for (int t = 0; t < 3; ++t) x.coff[u][t] = c_scol[p0 + u][t] * TE + x.e;
+  const int ar = lane >> 2, ae = 2 * (lane & 3);  // accumulator row slot / first element
+  int rck[V::NCK], rq[V::NQ], rtr[V::NT];
+  rows_of(V::ck_rows, ar, rck);
+  rows_of(V::q_rows, ar, rq);
+  rows_of(V::tr_rows, ar, rtr);
+
+  const int64_t ntiles = (prm.n + TE - 1) / TE;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t e0 = prm.e0 + tile * TE;
+    const int64_t left = prm.e0 + prm.n - e0;
+    const int ne = static_cast<int>(left < TE ? left : TE);
+    const int el = x.e < ne ? x.e : ne - 1;
+    x.st = prm.star + (e0 + el) * 3 * P * 3;
+    x.ap = prm.aplus + (e0 + el) * 4 * P * 9;
+    const double* src = prm.src + e0 * P * 9;
+    __syncthreads();  // previous tile done with D / TR
+    x.D = D;
+    const double* Qt = prm.Q + e0 * P * B;
+    for (int i = tid; i < TE * P * B; i += NTH) {
+      const int ee = i / (P * B), r = i - ee * P * B, p = r / B, kk = r - p * B;
+      D[kk * SD + p * TE + ee] = ee < ne ? Qt[i] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int mt = 0; mt < V::NCK; ++mt)
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+        if (rck[mt] >= 0) {
+          const int o = rck[mt] * SD + (p0 + u) * TE + ae;
+          IS[o] = prm.dt * D[o];
+          IS[o + 1] = prm.dt * D[o + 1];
+        }
+#pragma unroll 1
+    for (int d = 0; d < N; ++d) {
+      double acc[V::NCK][3][2];
+#pragma unroll
+      for (int mt = 0; mt < V::NCK; ++mt)
+#pragma unroll
+        for (int u = 0; u < 3; ++u) acc[mt][u][0] = acc[mt][u][1] = 0.0;
+      ck<N>(x, acc);
+      source(acc, rck, D, src, p0, g, ae, ne);
+      __syncthreads();  // every warp done reading D^d
+      const double s1 = prm.scal[d], s2 = prm.scal[N + d];
+#pragma unroll
+      for (int mt = 0; mt < V::NCK; ++mt)
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+          if (rck[mt] >= 0) {
+            const int o = rck[mt] * SD + (p0 + u) * TE + ae;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const double v = s1 * acc[mt][u][h];
+              IS[o + h] = fma(s2, v, IS[o + h]);
+              D[o + h] = v;
+            }
+          }
+      __syncthreads();
+    }
+    x.D = IS;
+    // volume + source on I, then traces of the elastic columns
+    double qa[V::NQ][3][2];
+#pragma unroll
+    for (int mt = 0; mt < V::NQ; ++mt)
+#pragma unroll
+      for (int u = 0; u < 3; ++u) qa[mt][u][0] = qa[mt][u][1] = 0.0;
+    vol<N>(x, qa);
+    source(qa, rq, IS, src, p0, g, ae, ne);
+    {
+      double ta[4][V::NT][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int mt = 0; mt < V::NT; ++mt) ta[i][mt][0] = ta[i][mt][1] = 0.0;
+      traces<N>(x, ta);
+      __syncthreads();  // TR aliases D: every warp past the recursion's last reads
+      for (int i = tid; i < 4 * V::BtR * TS; i += NTH) TR[i] = 0.0;
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int mt = 0; mt < V::NT; ++mt)
+          if (rtr[mt] >= 0) {
+            double* t = TR + (i * V::BtR + rtr[mt]) * TS + w * TE + ae;
+            t[0] = ta[i][mt][0];
+            t[1] = ta[i][mt][1];
+          }
+    }
+    __syncthreads();  // traces complete; I no longer read
+    {
+      double* gt = prm.traces + e0 * 4 * Bt * 9;
+      for (int i = tid; i < ne * 4 * Bt * 9; i += NTH) {
+        const int ee = i / (4 * Bt * 9), r = i - ee * 4 * Bt * 9, f = r / (Bt * 9), mq = r - f * Bt * 9;
+        const int m = mq / 9, qq = mq - m * 9;
+        gt[i] = TR[(f * V::BtR + m) * TS + qq * TE + ee];
+      }
+    }
+    lift<N>(x, qa);
+#pragma unroll
+    for (int mt = 0; mt < V::NQ; ++mt)
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+        if (rq[mt] >= 0) {
+          double* o = IS + rq[mt] * SD + (p0 + u) * TE + ae;  // I no longer read
+          o[0] = qa[mt][u][0];
+          o[1] = qa[mt][u][1];
+        }
+    __syncthreads();
+    double* Qw = prm.Q + e0 * P * B;
+    for (int i = tid; i < ne * P * B; i += NTH) {
+      const int ee = i / (P * B), r = i - ee * P * B, p = r / B, kk = r - p * B;
+      Qw[i] += IS[kk * SD + p * TE + ee];
+    }
+  }
+}
+
+}  // namespace visco
+
+bool visco_supported(int N, int P) { return P == 27 && N >= 1 && N <= 4; }
+
+cudaError_t visco_configure(int N, const int (*scols)[3]) {
+  cudaError_t e = cudaMemcpyToSymbol(visco::c_scol, scols, sizeof(int) * 27 * 3);
+  if (e != cudaSuccess) return e;
+  switch (N) {
+    case 1: return cudaFuncSetAttribute(visco::vm_local<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(visco::smem_bytes<1>()));
+    case 2: return cudaFuncSetAttribute(visco::vm_local<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(visco::smem_bytes<2>()));
+    case 3: return cudaFuncSetAttribute(visco::vm_local<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(visco::smem_bytes<3>()));
+    case 4: return cudaFuncSetAttribute(visco::vm_local<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(visco::smem_bytes<4>()));
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t visco_launch_local(const GenParams& p, cudaStream_t s) {
+  const int64_t tiles = (p.n + visco::TE - 1) / visco::TE;
+  if (tiles <= 0) return cudaSuccess;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const unsigned g = static_cast<unsigned>(tiles < sms ? tiles : sms);
+  switch (p.N) {
+    case 1: visco::vm_local<1><<<g, visco::NTH, visco::smem_bytes<1>(), s>>>(p); break;
+    case 2: visco::vm_local<2><<<g, visco::NTH, visco::smem_bytes<2>(), s>>>(p); break;
+    case 3: visco::vm_local<3><<<g, visco::NTH, visco::smem_bytes<3>(), s>>>(p); break;
+    case 4: visco::vm_local<4><<<g, visco::NTH, visco::smem_bytes<4>(), s>>>(p); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ydg

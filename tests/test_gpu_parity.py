@@ -123,6 +123,24 @@ def test_c3_viscoelastic_replica():
     assert err["memory"] <= 1e-11, err
 
 
+@pytest.mark.parametrize("N", [1, 2, 3])
+def test_viscoelastic_orders(N):
+    """The viscoelastic tensor-core local kernel at the other orders it is generated for
+    (3x3x2 cubes: 108 elements = 13 full 8-element tiles + a ragged tile of 4)."""
+    cfg = _cfg("c3", N=N, nx=3, ny=3, nz=2, steps=2)
+    err, *_ = _parity(cfg)
+    assert err["all"] <= TOL[8], err
+    assert err["memory"] <= 1e-11, err
+
+
+def test_viscoelastic_csr_kernel(monkeypatch):
+    """YDG_VISCO_GENERIC=1 selects the CSR local kernel (the comparison path); it agrees too."""
+    monkeypatch.setenv("YDG_VISCO_GENERIC", "1")
+    cfg = synth.CONFIGS["c3"].replica(3, steps=1)
+    err, *_ = _parity(cfg)
+    assert err["all"] <= TOL[8], err
+
+
 def test_generic_path_elastic(monkeypatch):
     """The generic (CSR) kernels on the elastic c0 problem agree with the oracle too."""
     monkeypatch.setenv("YDG_GENERIC", "1")
