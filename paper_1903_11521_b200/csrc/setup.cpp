@@ -119,8 +119,10 @@ void star_cols(int P, int p, int cols[3]) {
                                {VV, VW, VW}, {VU, VW, VW}, {SXX, SXY, SXZ}, {SXY, SYY, SYZ},
                                {SXZ, SYZ, SZZ}};
   const int r = p < 9 ? p : (p - 9) % 6;
-  (void)P;
-  for (int k = 0; k < 3; ++k) cols[k] = el[r][k];
+  // viscoelastic: every non-velocity row on (VU, VV, VW) in order (zero where a shear row has
+  // no entry), so the tensor-core kernel's star chunks read three fixed columns
+  const bool vcols = P == 27 && (r < 6);
+  for (int k = 0; k < 3; ++k) cols[k] = vcols ? VU + k : el[r][k];
 }
 
 bool match_faces(int64_t ne, const int64_t* vid, Neighbours* out, std::string* err) {

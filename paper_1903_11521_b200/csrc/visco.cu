@@ -28,7 +28,11 @@ constexpr int P = 27, TE = 8, W = 9, NTH = W * 32;
 constexpr int SD = P * TE + 12;  // D / I row stride in doubles (= 4 mod 16: conflict-free k-set loads)
 constexpr int TS = 9 * TE + 12;  // trace row stride
 
-__constant__ int c_scol[27][3];  // star-matrix column pattern of each row (api.cpp generic_patterns)
+
+__device__ __forceinline__ void l2_prefetch(const void* p, int64_t bytes) {
+  const int n = static_cast<int>(bytes) & ~15;
+  if (n > 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(n) : "memory");
+}
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -49,7 +53,6 @@ struct Ctx {
   const double* st;    // global: star of the lane's element [c][p][3]
   const double* ap;    // global: A+ of the lane's element [face][p][9]
   int lane, k, e, p0, q;
-  int coff[3][3];      // scols[p0+u][t] * 8 + e
   double s[3][3];      // star coefficients of the current direction
   double a[3][9];      // flux-solver coefficients of the current face
   double b[2][3];      // B fragments (double-buffered one k-set ahead)
@@ -61,15 +64,21 @@ struct Ctx {
 #pragma unroll
       for (int t = 0; t < 3; ++t) s[u][t] = st[(c * P + p0 + u) * 3 + t];
   }
+  // star chunk X^c[4ks+k][p0+u][e]: every non-velocity row reads the velocity columns
+  // (VU, VV, VW) in order (setup.cpp star_cols, P = 27); the velocity rows read stresses
+  template <bool VEL>
   __device__ __forceinline__ void chunk(int buf, int ks) {
-    const double* r = D + (4 * ks + k) * SD;
-    double v[3][3];
+    const double* r = D + (4 * ks + k) * SD + e;
+    if constexpr (VEL) {
+      constexpr int cols[3][3] = {{0, 3, 5}, {3, 1, 4}, {5, 4, 2}};  // (SXX SXY SXZ) (SXY SYY SYZ) (SXZ SYZ SZZ)
 #pragma unroll
-    for (int u = 0; u < 3; ++u)
+      for (int u = 0; u < 3; ++u)
+        b[buf][u] = fma(s[u][2], r[cols[u][2] * TE], fma(s[u][1], r[cols[u][1] * TE], s[u][0] * r[cols[u][0] * TE]));
+    } else {
+      const double v0 = r[6 * TE], v1 = r[7 * TE], v2 = r[8 * TE];
 #pragma unroll
-      for (int t = 0; t < 3; ++t) v[u][t] = r[coff[u][t]];
-#pragma unroll
-    for (int u = 0; u < 3; ++u) b[buf][u] = fma(s[u][2], v[u][2], fma(s[u][1], v[u][1], s[u][0] * v[u][0]));
+      for (int u = 0; u < 3; ++u) b[buf][u] = fma(s[u][2], v2, fma(s[u][1], v1, s[u][0] * v0));
+    }
   }
   __device__ __forceinline__ void mma(double (&acc)[3][2], int f, int buf) {
     const double af = FR[f * 32 + lane];
@@ -98,6 +107,15 @@ struct Ctx {
       b[buf][u] = y;
     }
   }
+};
+
+// The generated products call x.chunk(buf, ks); View binds the row class of the warp.
+template <class C, bool VEL>
+struct View {
+  C& c;
+  __device__ __forceinline__ void star(int d) { c.star(d); }
+  __device__ __forceinline__ void chunk(int buf, int ks) { c.template chunk<VEL>(buf, ks); }
+  __device__ __forceinline__ void mma(double (&acc)[3][2], int f, int buf) { c.mma(acc, f, buf); }
 };
 
 template <int N, class X, int M>
@@ -139,7 +157,7 @@ __device__ __forceinline__ void source(double (&acc)[M][3][2], const int (&rows)
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int e = ae + h;
-    const double* E = src + (e < ne ? e : ne - 1) * P * 9;
+    const double* E = src + e * P * 9;  // zero-padded past ne
 #pragma unroll
     for (int u = 0; u < 3; ++u) {
       const int p = p0 + u;
@@ -194,7 +212,7 @@ constexpr int dsz() {  // D buffer (also holds the traces after the recursion)
 }
 template <int N>
 constexpr size_t smem_bytes() {
-  return (static_cast<size_t>(dsz<N>()) + VT<N>::BR * SD + VT<N>::NFRAG * 32) * sizeof(double);
+  return (static_cast<size_t>(dsz<N>()) + VT<N>::BR * SD + VT<N>::NFRAG * 32 + 2 * TE * P * 9) * sizeof(double);
 }
 
 template <int N>
@@ -206,6 +224,7 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
   double* IS = D + dsz<N>();         // time integral I
   double* TR = D;
   double* FR = IS + V::BR * SD;
+  double* CS = FR + V::NFRAG * 32;   // the tile's star matrices [e][c][p][3] and sources [e][p][9]
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int g = group_of(w), p0 = 3 * g;
   {
@@ -222,15 +241,9 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
   x.e = lane >> 2;
   x.p0 = p0;
   x.q = w;  // trace column of this warp (elastic quantity w < 9)
-#pragma unroll
-  for (int u = 0; u < 3; ++u)
-#pragma unroll
-    for (int t = 0; t < 3; ++t) x.coff[u][t] = c_scol[p0 + u][t] * TE + x.e;
   const int ar = lane >> 2, ae = 2 * (lane & 3);  // accumulator row slot / first element
-  int rck[V::NCK], rq[V::NQ], rtr[V::NT];
+  int rck[V::NCK];
   rows_of(V::ck_rows, ar, rck);
-  rows_of(V::q_rows, ar, rq);
-  rows_of(V::tr_rows, ar, rtr);
 
   const int64_t ntiles = (prm.n + TE - 1) / TE;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -238,15 +251,34 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
     const int64_t left = prm.e0 + prm.n - e0;
     const int ne = static_cast<int>(left < TE ? left : TE);
     const int el = x.e < ne ? x.e : ne - 1;
-    x.st = prm.star + (e0 + el) * 3 * P * 3;
+    x.st = CS + x.e * 3 * P * 3;
     x.ap = prm.aplus + (e0 + el) * 4 * P * 9;
-    const double* src = prm.src + e0 * P * 9;
-    __syncthreads();  // previous tile done with D / TR
+    const double* src = CS + TE * P * 9;
+    if (tid == 0 && tile + gridDim.x < ntiles) {  // next tile's streams -> L2 while this one computes
+      const int64_t n0 = prm.e0 + (tile + gridDim.x) * TE;
+      const int64_t nl = prm.e0 + prm.n - n0 < TE ? prm.e0 + prm.n - n0 : TE;
+      l2_prefetch(prm.Q + n0 * P * B, nl * P * B * 8);
+      l2_prefetch(prm.star + n0 * 3 * P * 3, nl * 3 * P * 3 * 8);
+      l2_prefetch(prm.src + n0 * P * 9, nl * P * 9 * 8);
+      l2_prefetch(prm.aplus + n0 * 4 * P * 9, nl * 4 * P * 9 * 8);
+    }
+    __syncthreads();  // previous tile done with D / TR / CS
     x.D = D;
-    const double* Qt = prm.Q + e0 * P * B;
-    for (int i = tid; i < TE * P * B; i += NTH) {
-      const int ee = i / (P * B), r = i - ee * P * B, p = r / B, kk = r - p * B;
-      D[kk * SD + p * TE + ee] = ee < ne ? Qt[i] : 0.0;
+    {
+      const double* Qt = prm.Q + e0 * P * B;
+      const double* St = prm.star + e0 * 3 * P * 3;
+      const double* Et = prm.src + e0 * P * 9;
+#pragma unroll 4
+      for (int i = tid; i < TE * P * B; i += NTH) {
+        const int ee = i / (P * B), r = i - ee * P * B, p = r / B, kk = r - p * B;
+        D[kk * SD + p * TE + ee] = ee < ne ? Qt[i] : 0.0;
+      }
+#pragma unroll 4
+      for (int i = tid; i < TE * P * 9; i += NTH) {
+        const bool in = i < ne * P * 9;
+        CS[i] = in ? St[i] : 0.0;
+        CS[TE * P * 9 + i] = in ? Et[i] : 0.0;
+      }
     }
     __syncthreads();
 #pragma unroll
@@ -255,8 +287,8 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
       for (int u = 0; u < 3; ++u)
         if (rck[mt] >= 0) {
           const int o = rck[mt] * SD + (p0 + u) * TE + ae;
-          IS[o] = prm.dt * D[o];
-          IS[o + 1] = prm.dt * D[o + 1];
+          const double2 d2 = *reinterpret_cast<const double2*>(D + o);
+          *reinterpret_cast<double2*>(IS + o) = make_double2(prm.dt * d2.x, prm.dt * d2.y);
         }
 #pragma unroll 1
     for (int d = 0; d < N; ++d) {
@@ -265,7 +297,13 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
       for (int mt = 0; mt < V::NCK; ++mt)
 #pragma unroll
         for (int u = 0; u < 3; ++u) acc[mt][u][0] = acc[mt][u][1] = 0.0;
-      ck<N>(x, acc);
+      if (g == 2) {
+        View<Ctx<N>, true> xv{x};
+        ck<N>(xv, acc);
+      } else {
+        View<Ctx<N>, false> xn{x};
+        ck<N>(xn, acc);
+      }
       source(acc, rck, D, src, p0, g, ae, ne);
       __syncthreads();  // every warp done reading D^d
       const double s1 = prm.scal[d], s2 = prm.scal[N + d];
@@ -275,23 +313,32 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
         for (int u = 0; u < 3; ++u)
           if (rck[mt] >= 0) {
             const int o = rck[mt] * SD + (p0 + u) * TE + ae;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const double v = s1 * acc[mt][u][h];
-              IS[o + h] = fma(s2, v, IS[o + h]);
-              D[o + h] = v;
-            }
+            const double v0 = s1 * acc[mt][u][0], v1 = s1 * acc[mt][u][1];
+            double2 i2 = *reinterpret_cast<const double2*>(IS + o);
+            i2.x = fma(s2, v0, i2.x);
+            i2.y = fma(s2, v1, i2.y);
+            *reinterpret_cast<double2*>(IS + o) = i2;
+            *reinterpret_cast<double2*>(D + o) = make_double2(v0, v1);
           }
       __syncthreads();
     }
     x.D = IS;
     // volume + source on I, then traces of the elastic columns
+    int rq[V::NQ], rtr[V::NT];
+    rows_of(V::q_rows, ar, rq);
+    rows_of(V::tr_rows, ar, rtr);
     double qa[V::NQ][3][2];
 #pragma unroll
     for (int mt = 0; mt < V::NQ; ++mt)
 #pragma unroll
       for (int u = 0; u < 3; ++u) qa[mt][u][0] = qa[mt][u][1] = 0.0;
-    vol<N>(x, qa);
+    if (g == 2) {
+      View<Ctx<N>, true> xv{x};
+      vol<N>(xv, qa);
+    } else {
+      View<Ctx<N>, false> xn{x};
+      vol<N>(xn, qa);
+    }
     source(qa, rq, IS, src, p0, g, ae, ne);
     {
       double ta[4][V::NT][2];
@@ -308,9 +355,8 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
 #pragma unroll
         for (int mt = 0; mt < V::NT; ++mt)
           if (rtr[mt] >= 0) {
-            double* t = TR + (i * V::BtR + rtr[mt]) * TS + w * TE + ae;
-            t[0] = ta[i][mt][0];
-            t[1] = ta[i][mt][1];
+            *reinterpret_cast<double2*>(TR + (i * V::BtR + rtr[mt]) * TS + w * TE + ae) =
+                make_double2(ta[i][mt][0], ta[i][mt][1]);
           }
     }
     __syncthreads();  // traces complete; I no longer read
@@ -328,12 +374,12 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
 #pragma unroll
       for (int u = 0; u < 3; ++u)
         if (rq[mt] >= 0) {
-          double* o = IS + rq[mt] * SD + (p0 + u) * TE + ae;  // I no longer read
-          o[0] = qa[mt][u][0];
-          o[1] = qa[mt][u][1];
+          *reinterpret_cast<double2*>(IS + rq[mt] * SD + (p0 + u) * TE + ae) =  // I no longer read
+              make_double2(qa[mt][u][0], qa[mt][u][1]);
         }
     __syncthreads();
     double* Qw = prm.Q + e0 * P * B;
+#pragma unroll 4
     for (int i = tid; i < ne * P * B; i += NTH) {
       const int ee = i / (P * B), r = i - ee * P * B, p = r / B, kk = r - p * B;
       Qw[i] += IS[kk * SD + p * TE + ee];
@@ -346,8 +392,11 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
 bool visco_supported(int N, int P) { return P == 27 && N >= 1 && N <= 4; }
 
 cudaError_t visco_configure(int N, const int (*scols)[3]) {
-  cudaError_t e = cudaMemcpyToSymbol(visco::c_scol, scols, sizeof(int) * 27 * 3);
-  if (e != cudaSuccess) return e;
+  // the kernel hard-codes the star column pattern; check it against the uploaded layout
+  static const int vel[3][3] = {{0, 3, 5}, {3, 1, 4}, {5, 4, 2}};
+  for (int p = 0; p < 27; ++p)
+    for (int t = 0; t < 3; ++t)
+      if (scols[p][t] != (p >= 6 && p < 9 ? vel[p - 6][t] : 6 + t)) return cudaErrorInvalidValue;
   switch (N) {
     case 1: return cudaFuncSetAttribute(visco::vm_local<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(visco::smem_bytes<1>()));
     case 2: return cudaFuncSetAttribute(visco::vm_local<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(visco::smem_bytes<2>()));
