@@ -337,7 +337,7 @@ def run_ydg(args):
     # kernel names as ncu lists them: fp64 elastic = tensor-core kernels, fp32 = sparse FFMA
     # kernels, viscoelastic / N=6 fp64 = generic kernels
     if cfg.P == 27 and cfg.N <= 4 and os.environ.get("YDG_VISCO_GENERIC") != "1":
-        k_loc, k_nb, bound = "vm_local", "gen_neigh", "tensor"  # viscoelastic tensor-core local kernel
+        k_loc, k_nb, bound = "vm_local", "vm_neigh", "tensor"  # viscoelastic tensor-core local kernel
     elif cfg.P == 27 or (cfg.precision == 8 and cfg.N == 6):
         k_loc, k_nb, bound = "gen_local", "gen_neigh", "alu"
     elif cfg.precision == 8:

@@ -470,7 +470,7 @@ int generic_step(ydg_solver* h, double dt, int nsteps, cudaStream_t s) {
   g.n = h->ne;
   for (int n = 0; n < nsteps; ++n) {
     CUDA_OR_FAIL(h, timed(h, 0, s, [&] { return h->visco_tc ? visco_launch_local(g, s) : gen_launch(g, true, s); }));
-    CUDA_OR_FAIL(h, timed(h, 1, s, [&] { return gen_launch(g, false, s); }));
+    CUDA_OR_FAIL(h, timed(h, 1, s, [&] { return h->visco_tc ? visco_launch_neigh(g, s) : gen_launch(g, false, s); }));
   }
   return YDG_OK;
 }

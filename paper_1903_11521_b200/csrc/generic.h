@@ -30,10 +30,11 @@ cudaError_t gen_configure(int B, int Bt, int P, const int (*ecols)[9], const int
 cudaError_t gen_launch(const GenParams& p, bool local, cudaStream_t s);
 int gen_tile_elems();
 
-// Viscoelastic (P = 27) local kernel on FP64 tensor cores, orders 1..4 (visco.cu); the
-// neighbour flux stays on gen_launch(p, false).
+// Viscoelastic (P = 27) local and neighbour-flux kernels on FP64 tensor cores, orders 1..4
+// (visco.cu).
 bool visco_supported(int N, int P);
 cudaError_t visco_configure(int N, const int (*scols)[3]);
 cudaError_t visco_launch_local(const GenParams& p, cudaStream_t s);
+cudaError_t visco_launch_neigh(const GenParams& p, cudaStream_t s);
 
 }  // namespace ydg

@@ -29,9 +29,11 @@ constexpr int SD = P * TE + 12;  // D / I row stride in doubles (= 4 mod 16: con
 constexpr int TS = 9 * TE + 12;  // trace row stride
 
 
+// Bulk L2 prefetch of [p, p + bytes), widened to 16-byte alignment (the instruction's rule).
 __device__ __forceinline__ void l2_prefetch(const void* p, int64_t bytes) {
-  const int n = static_cast<int>(bytes) & ~15;
-  if (n > 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(n) : "memory");
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p), a0 = a & ~uintptr_t(15);
+  const int n = static_cast<int>((a + bytes - a0 + 15) & ~int64_t(15));
+  if (bytes > 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(n) : "memory");
 }
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
@@ -387,6 +389,154 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
   }
 }
 
+
+// Neighbour flux: Q += sum_i R^i (f^{h_i} T^{nb_i}_{j_i}) A-_i^T.
+// Per tile: the neighbours' traces of the shared faces and the tile's Q^n arrive by
+// cp.async (the next tile's neighbour slots one tile ahead), are rotated by f^h (CSR in
+// shared memory, degree-block diagonal), then the same Y-chunk + DMMA lift as the local
+// kernel with A- accumulates the update, added to the staged Q^n and stored once.
+template <int N>
+constexpr int zsz() { return 4 * VT<N>::BtR * TS; }
+template <int N>
+constexpr int gsz() { return 4 * TE * VT<N>::Bt * 9; }
+template <int N>
+constexpr int zg() { return zsz<N>() + gsz<N>() > VT<N>::BR * SD ? zsz<N>() + gsz<N>() : VT<N>::BR * SD; }
+template <int N>
+constexpr int fnz() { return 3 * VT<N>::Bt * VT<N>::Bt; }  // bound on the nonzeros of f^0..2
+template <int N>
+constexpr size_t nsmem_bytes() {
+  return (static_cast<size_t>(VT<N>::NFRAG) * 32 + zg<N>() + TE * P * VT<N>::B + 2 * 4 * TE + fnz<N>()) *
+             sizeof(double) +
+         (2 * 4 * TE + 3 * VT<N>::Bt + 1 + fnz<N>()) * sizeof(int);
+}
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int N>
+__global__ void __launch_bounds__(NTH, 1) vm_neigh(const GenParams prm) {
+  using V = VT<N>;
+  constexpr int B = V::B, Bt = V::Bt, BtR = V::BtR;
+  extern __shared__ __align__(16) double sm[];
+  double* FR = sm;
+  double* Z = FR + V::NFRAG * 32;  // rotated neighbour traces [4][BtR][TS]
+  double* GT = Z + zsz<N>();       // gathered neighbour traces [e][face][n][9]
+  double* QS = Z;                  // Q-update staging [B][SD] (after the lift)
+  double* QB = Z + zg<N>();        // the tile's Q^n, element-major as in HBM
+  int64_t* NB = reinterpret_cast<int64_t*>(QB + TE * P * B);  // [2][e][face] neighbour ids
+  double* FV = reinterpret_cast<double*>(NB + 2 * 4 * TE);      // f^h CSR values
+  int* JH = reinterpret_cast<int*>(FV + fnz<N>());             // [2][e*4+face] j | h << 2
+  int* FP = JH + 2 * 4 * TE;                                   // CSR row pointers, columns
+  int* FC = FP + 3 * Bt + 1;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = group_of(w), p0 = 3 * g;
+  {
+    const double* f = vfrag<N>();
+    for (int i = tid; i < V::NFRAG * 32; i += NTH) FR[i] = f[i];
+    for (int i = tid; i <= 3 * Bt; i += NTH) FP[i] = prm.f_ptr[i];
+    const int nnz = prm.f_ptr[3 * Bt];
+    for (int i = tid; i < nnz && i < fnz<N>(); i += NTH) {
+      FC[i] = prm.f_col[i];
+      FV[i] = prm.f_val[i];
+    }
+  }
+  Ctx<N> x;
+  x.TR = Z;
+  x.FR = FR;
+  x.lane = lane;
+  x.k = lane & 3;
+  x.e = lane >> 2;
+  x.p0 = p0;
+  const int ar = lane >> 2, ae = 2 * (lane & 3);
+  const int64_t ntiles = (prm.n + TE - 1) / TE;
+  auto slots = [&](int64_t t, int buf) {  // neighbour ids / j|h of tile t -> slot buffer buf
+    const int64_t n0 = prm.e0 + t * TE;
+    const int nl = static_cast<int>(prm.e0 + prm.n - n0 < TE ? prm.e0 + prm.n - n0 : TE);
+    if (tid < nl * 4) {
+      cp_async8(NB + buf * 4 * TE + tid, prm.nb + n0 * 4 + tid);
+      JH[buf * 4 * TE + tid] = prm.jh[n0 * 4 + tid];
+    }
+  };
+  if (blockIdx.x < ntiles) slots(blockIdx.x, 0);
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int buf = it & 1;
+    const int64_t e0 = prm.e0 + tile * TE;
+    const int64_t left = prm.e0 + prm.n - e0;
+    const int ne = static_cast<int>(left < TE ? left : TE);
+    const int el = x.e < ne ? x.e : ne - 1;
+    x.ap = prm.aminus + (e0 + el) * 4 * P * 9;
+    cp_async_wait_all();
+    __syncthreads();  // slots of this tile landed; previous tile done with Z / GT / QS / QB
+    {
+      const int64_t* nb = NB + buf * 4 * TE;
+      const int* jh = JH + buf * 4 * TE;
+      for (int i = tid; i < ne * 4 * Bt * 9; i += NTH) {
+        const int ef = i / (Bt * 9), nq = i - ef * Bt * 9;
+        cp_async8(GT + i, prm.traces + (nb[ef] * 4 + (jh[ef] & 3)) * Bt * 9 + nq);
+      }
+      const double* Qt = prm.Q + e0 * P * B;
+      for (int i = tid; i < ne * P * B; i += NTH) cp_async8(QB + i, Qt + i);
+      if (tile + gridDim.x < ntiles) {
+        slots(tile + gridDim.x, buf ^ 1);
+        if (tid == 0) {
+          const int64_t n0 = prm.e0 + (tile + gridDim.x) * TE;
+          const int64_t nl = prm.e0 + prm.n - n0 < TE ? prm.e0 + prm.n - n0 : TE;
+          l2_prefetch(prm.Q + n0 * P * B, nl * P * B * 8);
+          l2_prefetch(prm.aminus + n0 * 4 * P * 9, nl * 4 * P * 9 * 8);
+        }
+      }
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    {
+      const int* jh = JH + buf * 4 * TE;
+      for (int i = tid; i < 4 * BtR * 9 * TE; i += NTH) {
+        const int ee = i & (TE - 1), q = (i >> 3) % 9, fm = i / (9 * TE), m = fm % BtR, f = fm / BtR;
+        double s = 0.0;
+        if (m < Bt && ee < ne) {
+          const int row = (jh[ee * 4 + f] >> 2) * Bt + m;
+          const double* gt = GT + (ee * 4 + f) * Bt * 9 + q;
+          for (int t = FP[row]; t < FP[row + 1]; ++t) s = fma(FV[t], gt[FC[t] * 9], s);
+        }
+        Z[(f * BtR + m) * TS + q * TE + ee] = s;
+      }
+    }
+    __syncthreads();
+    double qa[V::NQ][3][2];
+#pragma unroll
+    for (int mt = 0; mt < V::NQ; ++mt)
+#pragma unroll
+      for (int u = 0; u < 3; ++u) qa[mt][u][0] = qa[mt][u][1] = 0.0;
+    lift<N>(x, qa);
+    int rq[V::NQ];
+    rows_of(V::q_rows, ar, rq);
+    __syncthreads();  // every warp done reading Z
+#pragma unroll
+    for (int mt = 0; mt < V::NQ; ++mt)
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+        if (rq[mt] >= 0)
+          *reinterpret_cast<double2*>(QS + rq[mt] * SD + (p0 + u) * TE + ae) = make_double2(qa[mt][u][0], qa[mt][u][1]);
+    __syncthreads();
+    double* Qw = prm.Q + e0 * P * B;
+#pragma unroll 4
+    for (int i = tid; i < ne * P * B; i += NTH) {
+      const int ee = i / (P * B), r = i - ee * P * B, p = r / B, kk = r - p * B;
+      Qw[i] = QB[i] + QS[kk * SD + p * TE + ee];
+    }
+  }
+}
+
 }  // namespace visco
 
 bool visco_supported(int N, int P) { return P == 27 && N >= 1 && N <= 4; }
@@ -397,6 +547,14 @@ cudaError_t visco_configure(int N, const int (*scols)[3]) {
   for (int p = 0; p < 27; ++p)
     for (int t = 0; t < 3; ++t)
       if (scols[p][t] != (p >= 6 && p < 9 ? vel[p - 6][t] : 6 + t)) return cudaErrorInvalidValue;
+  cudaError_t e = cudaSuccess;
+  switch (N) {
+    case 1: e = cudaFuncSetAttribute(visco::vm_neigh<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(visco::nsmem_bytes<1>())); break;
+    case 2: e = cudaFuncSetAttribute(visco::vm_neigh<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(visco::nsmem_bytes<2>())); break;
+    case 3: e = cudaFuncSetAttribute(visco::vm_neigh<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(visco::nsmem_bytes<3>())); break;
+    case 4: e = cudaFuncSetAttribute(visco::vm_neigh<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(visco::nsmem_bytes<4>())); break;
+  }
+  if (e != cudaSuccess) return e;
   switch (N) {
     case 1: return cudaFuncSetAttribute(visco::vm_local<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(visco::smem_bytes<1>()));
     case 2: return cudaFuncSetAttribute(visco::vm_local<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(visco::smem_bytes<2>()));
@@ -404,6 +562,22 @@ cudaError_t visco_configure(int N, const int (*scols)[3]) {
     case 4: return cudaFuncSetAttribute(visco::vm_local<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(visco::smem_bytes<4>()));
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t visco_launch_neigh(const GenParams& p, cudaStream_t s) {
+  const int64_t tiles = (p.n + visco::TE - 1) / visco::TE;
+  if (tiles <= 0) return cudaSuccess;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const unsigned g = static_cast<unsigned>(tiles < sms ? tiles : sms);
+  switch (p.N) {
+    case 1: visco::vm_neigh<1><<<g, visco::NTH, visco::nsmem_bytes<1>(), s>>>(p); break;
+    case 2: visco::vm_neigh<2><<<g, visco::NTH, visco::nsmem_bytes<2>(), s>>>(p); break;
+    case 3: visco::vm_neigh<3><<<g, visco::NTH, visco::nsmem_bytes<3>(), s>>>(p); break;
+    case 4: visco::vm_neigh<4><<<g, visco::NTH, visco::nsmem_bytes<4>(), s>>>(p); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t visco_launch_local(const GenParams& p, cudaStream_t s) {
