@@ -407,7 +407,7 @@ template <int N>
 constexpr size_t nsmem_bytes() {
   return (static_cast<size_t>(VT<N>::NFRAG) * 32 + zg<N>() + TE * P * VT<N>::B + 2 * 4 * TE + fnz<N>()) *
              sizeof(double) +
-         (2 * 4 * TE + 3 * VT<N>::Bt + 1 + fnz<N>()) * sizeof(int);
+         (2 * 4 * TE + 3 * VT<N>::Bt + 1) * sizeof(int);
 }
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
@@ -433,20 +433,31 @@ __global__ void __launch_bounds__(NTH, 1) vm_neigh(const GenParams prm) {
   double* QS = Z;                  // Q-update staging [B][SD] (after the lift)
   double* QB = Z + zg<N>();        // the tile's Q^n, element-major as in HBM
   int64_t* NB = reinterpret_cast<int64_t*>(QB + TE * P * B);  // [2][e][face] neighbour ids
-  double* FV = reinterpret_cast<double*>(NB + 2 * 4 * TE);      // f^h CSR values
-  int* JH = reinterpret_cast<int*>(FV + fnz<N>());             // [2][e*4+face] j | h << 2
-  int* FP = JH + 2 * 4 * TE;                                   // CSR row pointers, columns
-  int* FC = FP + 3 * Bt + 1;
+  double* FD = reinterpret_cast<double*>(NB + 2 * 4 * TE);      // f^h dense [h][m][n]
+  int* JH = reinterpret_cast<int*>(FD + fnz<N>());             // [2][e*4+face] j | h << 2
+  int* LO = JH + 2 * 4 * TE;                                   // per (h, m): first nonzero column
+  int* WIDE = LO + 3 * Bt;                                     // any row wider than N + 1 columns
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int g = group_of(w), p0 = 3 * g;
   {
     const double* f = vfrag<N>();
     for (int i = tid; i < V::NFRAG * 32; i += NTH) FR[i] = f[i];
-    for (int i = tid; i <= 3 * Bt; i += NTH) FP[i] = prm.f_ptr[i];
-    const int nnz = prm.f_ptr[3 * Bt];
-    for (int i = tid; i < nnz && i < fnz<N>(); i += NTH) {
-      FC[i] = prm.f_col[i];
-      FV[i] = prm.f_val[i];
+    // f^h is block diagonal by degree (width <= N + 1 per row): dense rows + column windows
+    if (tid == 0) *WIDE = 0;
+    for (int i = tid; i < fnz<N>(); i += NTH) FD[i] = 0.0;
+    __syncthreads();
+    for (int row = tid; row < 3 * Bt; row += NTH) {
+      int lo = Bt, hi = -1;
+      for (int t = prm.f_ptr[row]; t < prm.f_ptr[row + 1]; ++t) {
+        const int c = prm.f_col[t];
+        FD[row * Bt + c] = prm.f_val[t];
+        lo = c < lo ? c : lo;
+        hi = c > hi ? c : hi;
+      }
+      if (hi < lo) lo = hi = 0;
+      if (lo + N + 1 > Bt) lo = Bt - (N + 1) > 0 ? Bt - (N + 1) : 0;  // keep the window inside the row
+      if (hi >= lo + N + 1) atomicOr(WIDE, 1);
+      LO[row] = lo;
     }
   }
   Ctx<N> x;
@@ -506,7 +517,14 @@ __global__ void __launch_bounds__(NTH, 1) vm_neigh(const GenParams prm) {
         if (m < Bt && ee < ne) {
           const int row = (jh[ee * 4 + f] >> 2) * Bt + m;
           const double* gt = GT + (ee * 4 + f) * Bt * 9 + q;
-          for (int t = FP[row]; t < FP[row + 1]; ++t) s = fma(FV[t], gt[FC[t] * 9], s);
+          const double* fr = FD + row * Bt;
+          if (!*WIDE) {
+            const int lo = LO[row];
+#pragma unroll
+            for (int n = 0; n <= N && n < Bt; ++n) s = fma(fr[lo + n], gt[(lo + n) * 9], s);
+          } else {
+            for (int n = 0; n < Bt; ++n) s = fma(fr[n], gt[n * 9], s);
+          }
         }
         Z[(f * BtR + m) * TS + q * TE + ee] = s;
       }
