@@ -102,11 +102,11 @@ struct Ctx {
 #pragma unroll
     for (int j = 0; j < 9; ++j) t[j] = r[j * TE];
 #pragma unroll
-    for (int u = 0; u < 3; ++u) {
-      double y = a[u][0] * t[0];
-#pragma unroll
-      for (int j = 1; j < 9; ++j) y = fma(a[u][j], t[j], y);
-      b[buf][u] = y;
+    for (int u = 0; u < 3; ++u) {  // three short chains (DFMA latency), summed
+      const double y0 = fma(a[u][2], t[2], fma(a[u][1], t[1], a[u][0] * t[0]));
+      const double y1 = fma(a[u][5], t[5], fma(a[u][4], t[4], a[u][3] * t[3]));
+      const double y2 = fma(a[u][8], t[8], fma(a[u][7], t[7], a[u][6] * t[6]));
+      b[buf][u] = y0 + y1 + y2;
     }
   }
 };
@@ -171,10 +171,11 @@ __device__ __forceinline__ void source(double (&acc)[M][3][2], const int (&rows)
         for (int mt = 0; mt < M; ++mt) {
           if (rows[mt] < 0) continue;
           const double* r = X + rows[mt] * SD + e;
-          double s = acc[mt][u][h];
+          double s3[3];
 #pragma unroll
-          for (int j = 0; j < 9; ++j) s = fma(c[j], r[(9 + 6 * (j / 3) + j % 3) * TE], s);
-          acc[mt][u][h] = s;
+          for (int l = 0; l < 3; ++l)  // mechanism l: one short chain each
+            s3[l] = fma(c[3 * l + 2], r[(11 + 6 * l) * TE], fma(c[3 * l + 1], r[(10 + 6 * l) * TE], c[3 * l] * r[(9 + 6 * l) * TE]));
+          acc[mt][u][h] += s3[0] + s3[1] + s3[2];
         }
       } else if (g == 1) {
         double c[3];
