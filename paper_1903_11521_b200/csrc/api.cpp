@@ -294,9 +294,9 @@ cudaStream_t pick_stream(ydg_solver* h, void* s) { return s ? static_cast<cudaSt
 // (reading R14: E[sigma_s][theta^l_t] for t normal when s normal, t = s when s shear;
 // E[theta^l_s][theta^l_s]; velocity rows have no source).  Unused slots repeat a column
 // with a zero coefficient.
-void generic_patterns(int (*ecols)[9], int (*scols)[3]) {
+void generic_patterns(int P, int (*ecols)[9], int (*scols)[3]) {
   for (int p = 0; p < 27; ++p) {
-    star_cols(27, p, scols[p]);
+    star_cols(P, p < P ? p : p % 9, scols[p]);  // the layout element_coeffs uploads for P
     int n = 0;
     if (p < 6) {
       for (int l = 0; l < 3; ++l)
@@ -397,7 +397,7 @@ int generic_upload_mesh(ydg_solver* h, const double* xyz, const double* material
     CUDA_OR_FAIL(h, cudaMemcpy(h->jh_e, jh.data(), jh.size(), cudaMemcpyHostToDevice));
   }
   int ecols[27][9], scols[27][3];
-  generic_patterns(ecols, scols);
+  generic_patterns(P, ecols, scols);
   const int64_t chunk = 65536;
   std::vector<double> st, ap, am, sr;
   for (int64_t e0 = 0; e0 < ne; e0 += chunk) {
@@ -508,7 +508,7 @@ int ydg_create(int order, int quantities, int precision, int cuda_device, ydg_so
   if (e == cudaSuccess) {
     if (generic) {
       int ecols[27][9], scols[27][3];
-      generic_patterns(ecols, scols);
+      generic_patterns(quantities, ecols, scols);
       e = gen_configure(h->B, h->Bt, quantities, ecols, scols);
       const char* vg = std::getenv("YDG_VISCO_GENERIC");  // 1: CSR local kernel (comparison)
       h->visco_tc = visco_supported(order, quantities) && !(vg && vg[0] == '1');
