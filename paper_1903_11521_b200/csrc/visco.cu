@@ -25,7 +25,7 @@ namespace ydg {
 namespace visco {
 
 constexpr int P = 27, TE = 8, W = 9, NTH = W * 32;
-constexpr int SD = P * TE + 12;  // D / I row stride in doubles (= 4 mod 16: conflict-free k-set loads)
+constexpr int SD = P * TE;       // D / I row stride in doubles (216 = 8 mod 16: conflict-free combination rows)
 constexpr int TS = 9 * TE + 12;  // trace row stride
 
 
@@ -52,44 +52,20 @@ struct Ctx {
   const double* D;     // shared: D^d (recursion) / I (volume, traces) [BR][SD]
   const double* TR;    // shared: traces [4][BtR][TS]
   const double* FR;    // shared: A fragments [NFRAG][32]
-  const double* st;    // global: star of the lane's element [c][p][3]
-  const double* ap;    // global: A+ of the lane's element [face][p][9]
+  const double* ap;    // global: A+- of the lane's element [face][p][9]
   int lane, k, e, p0, q;
-  double s[3][3];      // star coefficients of the current direction
   double a[3][9];      // flux-solver coefficients of the current face
-  double b[2][3];      // B fragments (double-buffered one k-set ahead)
+  double b[2][3];      // lift B fragments (double-buffered one k-set ahead)
   double b1[2];
 
-  __device__ __forceinline__ void star(int c) {
-#pragma unroll
-    for (int u = 0; u < 3; ++u)
-#pragma unroll
-      for (int t = 0; t < 3; ++t) s[u][t] = st[(c * P + p0 + u) * 3 + t];
-  }
-  // star chunk X^c[4ks+k][p0+u][e]: every non-velocity row reads the velocity columns
-  // (VU, VV, VW) in order (setup.cpp star_cols, P = 27); the velocity rows read stresses
-  template <bool VEL>
-  __device__ __forceinline__ void chunk(int buf, int ks) {
-    const double* r = D + (4 * ks + k) * SD + e;
-    if constexpr (VEL) {
-      constexpr int cols[3][3] = {{0, 3, 5}, {3, 1, 4}, {5, 4, 2}};  // (SXX SXY SXZ) (SXY SYY SYZ) (SXZ SYZ SZZ)
-#pragma unroll
-      for (int u = 0; u < 3; ++u)
-        b[buf][u] = fma(s[u][2], r[cols[u][2] * TE], fma(s[u][1], r[cols[u][1] * TE], s[u][0] * r[cols[u][0] * TE]));
-    } else {
-      const double v0 = r[6 * TE], v1 = r[7 * TE], v2 = r[8 * TE];
-#pragma unroll
-      for (int u = 0; u < 3; ++u) b[buf][u] = fma(s[u][2], v2, fma(s[u][1], v1, s[u][0] * v0));
-    }
-  }
+  __device__ __forceinline__ void ib(int buf, int ks) { b1[buf] = D[(4 * ks + k) * SD + q * TE + e]; }
+  __device__ __forceinline__ void mma1(double (&acc)[2], int f, int buf) { dmma(acc, FR[f * 32 + lane], b1[buf]); }
   __device__ __forceinline__ void mma(double (&acc)[3][2], int f, int buf) {
     const double af = FR[f * 32 + lane];
     dmma(acc[0], af, b[buf][0]);
     dmma(acc[1], af, b[buf][1]);
     dmma(acc[2], af, b[buf][2]);
   }
-  __device__ __forceinline__ void ib(int buf, int ks) { b1[buf] = D[(4 * ks + k) * SD + q * TE + e]; }
-  __device__ __forceinline__ void mma1(double (&acc)[2], int f, int buf) { dmma(acc, FR[f * 32 + lane], b1[buf]); }
   __device__ __forceinline__ void acoef(int i) {
 #pragma unroll
     for (int u = 0; u < 3; ++u)
@@ -111,24 +87,15 @@ struct Ctx {
   }
 };
 
-// The generated products call x.chunk(buf, ks); View binds the row class of the warp.
-template <class C, bool VEL>
-struct View {
-  C& c;
-  __device__ __forceinline__ void star(int d) { c.star(d); }
-  __device__ __forceinline__ void chunk(int buf, int ks) { c.template chunk<VEL>(buf, ks); }
-  __device__ __forceinline__ void mma(double (&acc)[3][2], int f, int buf) { c.mma(acc, f, buf); }
-};
-
 template <int N, class X, int M>
-__device__ __forceinline__ void ck(X& x, double (&a)[M][3][2]) {
+__device__ __forceinline__ void ck(X& x, double (&a)[3][M][2]) {
   if constexpr (N == 1) vck1(x, a);
   else if constexpr (N == 2) vck2(x, a);
   else if constexpr (N == 3) vck3(x, a);
   else vck4(x, a);
 }
 template <int N, class X, int M>
-__device__ __forceinline__ void vol(X& x, double (&a)[M][3][2]) {
+__device__ __forceinline__ void vol(X& x, double (&a)[3][M][2]) {
   if constexpr (N == 1) vvol1(x, a);
   else if constexpr (N == 2) vvol2(x, a);
   else if constexpr (N == 3) vvol3(x, a);
@@ -149,57 +116,6 @@ __device__ __forceinline__ void traces(X& x, double (&t)[4][M][2]) {
   else vtr4(x, t);
 }
 
-// acc(row, p0+u, e) += sum_j E_e[p0+u][j] X[row][ecol_j][e] with the source pattern of group g
-// (reading R14; generic_patterns in api.cpp): normal stresses <- 9 normal memory variables,
-// shear stresses <- 3, memory variables <- themselves, velocities: none.
-template <int M>
-__device__ __forceinline__ void source(double (&acc)[M][3][2], const int (&rows)[M], const double* X,
-                                       const double* src, int p0, int g, int ae, int ne) {
-  if (g == 2) return;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int e = ae + h;
-    const double* E = src + e * P * 9;  // zero-padded past ne
-#pragma unroll
-    for (int u = 0; u < 3; ++u) {
-      const int p = p0 + u;
-      if (g == 0) {
-        double c[9];
-#pragma unroll
-        for (int j = 0; j < 9; ++j) c[j] = E[p * 9 + j];
-#pragma unroll
-        for (int mt = 0; mt < M; ++mt) {
-          if (rows[mt] < 0) continue;
-          const double* r = X + rows[mt] * SD + e;
-          double s3[3];
-#pragma unroll
-          for (int l = 0; l < 3; ++l)  // mechanism l: one short chain each
-            s3[l] = fma(c[3 * l + 2], r[(11 + 6 * l) * TE], fma(c[3 * l + 1], r[(10 + 6 * l) * TE], c[3 * l] * r[(9 + 6 * l) * TE]));
-          acc[mt][u][h] += s3[0] + s3[1] + s3[2];
-        }
-      } else if (g == 1) {
-        double c[3];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) c[j] = E[p * 9 + j];
-#pragma unroll
-        for (int mt = 0; mt < M; ++mt) {
-          if (rows[mt] < 0) continue;
-          const double* r = X + rows[mt] * SD + e;
-          double s = acc[mt][u][h];
-#pragma unroll
-          for (int j = 0; j < 3; ++j) s = fma(c[j], r[(9 + 6 * j + p) * TE], s);
-          acc[mt][u][h] = s;
-        }
-      } else {
-        const double c = E[p * 9];
-#pragma unroll
-        for (int mt = 0; mt < M; ++mt)
-          if (rows[mt] >= 0) acc[mt][u][h] = fma(c, X[rows[mt] * SD + p * TE + e], acc[mt][u][h]);
-      }
-    }
-  }
-}
-
 template <int M, class F>
 __device__ __forceinline__ void rows_of(F words, int ar, int (&rows)[M]) {
 #pragma unroll
@@ -209,13 +125,93 @@ __device__ __forceinline__ void rows_of(F words, int ar, int (&rows)[M]) {
   }
 }
 
+// Star / source combination of one (row r, element e) of the left-first products
+// Z^c_t = M^c X_t (c = 0..2, t = the 9 elastic quantities; Z[c][r][t][e] in shared memory):
+//   out_p = sum_c sum_t A*^c[p][t] Z^c_t + sum_j E[p][j] X_j        (reading R14 source)
+// Every non-velocity row reads the velocity columns (VU, VV, VW) in order, the velocity rows
+// the stresses (SXX SXY SXZ) (SXY SYY SYZ) (SXZ SYZ SZZ) (setup.cpp star_cols, P = 27); the
+// source couples normal stresses to the 9 normal memory variables, shear stresses to 3, and
+// each memory variable to itself.  emit(p, value) receives every output exactly once.
+constexpr int ZS = 9 * TE;   // Z row stride
+constexpr int CSS = 10;      // star coefficients per (element, row): [c][t], padded
+constexpr int CSE = P * CSS;
+constexpr int CEE = 56;      // source coefficients per element (54 used)
+
+template <int B>
+__device__ __forceinline__ double star_row(int p, const double* cs, const double (&z)[3][3]) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    s0 = fma(cs[p * CSS + t], z[0][t], s0);
+    s1 = fma(cs[p * CSS + 3 + t], z[1][t], s1);
+    s2 = fma(cs[p * CSS + 6 + t], z[2][t], s2);
+  }
+  return (s0 + s1) + s2;
+}
+__device__ __forceinline__ double source_row(int p, const double* ce, const double (&m)[18]) {
+  double sr = 0.0;
+  if (p < 3) {
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+#pragma unroll
+      for (int t = 0; t < 3; ++t) sr = fma(ce[p * 9 + 3 * l + t], m[6 * l + t], sr);
+  } else if (p < 6) {
+#pragma unroll
+    for (int l = 0; l < 3; ++l) sr = fma(ce[27 + (p - 3) * 3 + l], m[6 * l + p], sr);
+  } else if (p >= 9) {
+    sr = ce[36 + p - 9] * m[p - 9];
+  }
+  return sr;
+}
+
+// VEL_FIRST: the velocity rows (stress columns) before the others, with every Z value of the
+// thread loaded up front -- the volume writes its result into the thread's own Z slots.
+template <int B, bool VEL_FIRST, class Emit>
+__device__ __forceinline__ void combine(const double* zr, const double* xr, const double* cs, const double* ce, Emit emit) {
+  constexpr int cols[3][3] = {{0, 3, 5}, {3, 1, 4}, {5, 4, 2}};
+  double m[18], zv[3][3];
+#pragma unroll
+  for (int j = 0; j < 18; ++j) m[j] = xr[(9 + j) * TE];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int t = 0; t < 3; ++t) zv[c][t] = zr[c * B * ZS + (6 + t) * TE];
+  auto vel_rows = [&]() {
+    double zs[3][6];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int t = 0; t < 6; ++t) zs[c][t] = zr[c * B * ZS + t * TE];
+    double v[3];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      double z[3][3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int t = 0; t < 3; ++t) z[c][t] = zs[c][cols[u][t]];
+      v[u] = star_row<B>(6 + u, cs, z);
+    }
+#pragma unroll
+    for (int u = 0; u < 3; ++u) emit(6 + u, v[u]);
+  };
+  if (VEL_FIRST) vel_rows();
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    if (p >= 6 && p < 9) continue;
+    emit(p, star_row<B>(p, cs, zv) + source_row(p, ce, m));
+  }
+  if (!VEL_FIRST) vel_rows();
+}
+
 template <int N>
 constexpr int dsz() {  // D buffer (also holds the traces after the recursion)
   return VT<N>::BR * SD > 4 * VT<N>::BtR * TS ? VT<N>::BR * SD : 4 * VT<N>::BtR * TS;
 }
 template <int N>
 constexpr size_t smem_bytes() {
-  return (static_cast<size_t>(dsz<N>()) + VT<N>::BR * SD + VT<N>::NFRAG * 32 + 2 * TE * P * 9) * sizeof(double);
+  return (static_cast<size_t>(dsz<N>()) + 3 * VT<N>::B * ZS + VT<N>::NFRAG * 32 + TE * (CSE + CEE)) *
+         sizeof(double);
 }
 
 template <int N>
@@ -223,17 +219,18 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
   using V = VT<N>;
   constexpr int B = V::B, Bt = V::Bt;
   extern __shared__ __align__(16) double sm[];
-  double* D = sm;                   // D^d; after the recursion: traces [4][BtR][TS], Q staging
-  double* IS = D + dsz<N>();         // time integral I
+  double* D = sm;                   // D^d, then I; after the traces: traces [4][BtR][TS], Q staging
   double* TR = D;
-  double* FR = IS + V::BR * SD;
-  double* CS = FR + V::NFRAG * 32;   // the tile's star matrices [e][c][p][3] and sources [e][p][9]
+  double* Z = D + dsz<N>();         // left-first products Z^c_t [3][B][ZS]; after the volume: its result
+  double* FR = Z + 3 * B * ZS;
+  double* CS = FR + V::NFRAG * 32;  // the tile's star rows [e][p][c*3+t] and sources [e][56]
+  double* CE = CS + TE * CSE;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int g = group_of(w), p0 = 3 * g;
   {
     const double* f = vfrag<N>();
     for (int i = tid; i < V::NFRAG * 32; i += NTH) FR[i] = f[i];
-    for (int i = tid; i < dsz<N>() + V::BR * SD; i += NTH) D[i] = 0.0;  // D and I: padding rows stay zero
+    for (int i = tid; i < dsz<N>(); i += NTH) D[i] = 0.0;  // padding rows stay zero
   }
   Ctx<N> x;
   x.D = D;
@@ -243,10 +240,10 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
   x.k = lane & 3;
   x.e = lane >> 2;
   x.p0 = p0;
-  x.q = w;  // trace column of this warp (elastic quantity w < 9)
+  x.q = w;  // left-first / trace column of this warp (elastic quantity w < 9)
   const int ar = lane >> 2, ae = 2 * (lane & 3);  // accumulator row slot / first element
-  int rck[V::NCK];
-  rows_of(V::ck_rows, ar, rck);
+  const bool comb = tid < TE * B;                 // combination thread: (row cr, element ce)
+  const int cr = tid >> 3, cel = tid & (TE - 1);
 
   const int64_t ntiles = (prm.n + TE - 1) / TE;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -254,9 +251,7 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
     const int64_t left = prm.e0 + prm.n - e0;
     const int ne = static_cast<int>(left < TE ? left : TE);
     const int el = x.e < ne ? x.e : ne - 1;
-    x.st = CS + x.e * 3 * P * 3;
     x.ap = prm.aplus + (e0 + el) * 4 * P * 9;
-    const double* src = CS + TE * P * 9;
     if (tid == 0 && tile + gridDim.x < ntiles) {  // next tile's streams -> L2 while this one computes
       const int64_t n0 = prm.e0 + (tile + gridDim.x) * TE;
       const int64_t nl = prm.e0 + prm.n - n0 < TE ? prm.e0 + prm.n - n0 : TE;
@@ -265,8 +260,7 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
       l2_prefetch(prm.src + n0 * P * 9, nl * P * 9 * 8);
       l2_prefetch(prm.aplus + n0 * 4 * P * 9, nl * 4 * P * 9 * 8);
     }
-    __syncthreads();  // previous tile done with D / TR / CS
-    x.D = D;
+    __syncthreads();  // previous tile done with every buffer
     {
       const double* Qt = prm.Q + e0 * P * B;
       const double* St = prm.star + e0 * 3 * P * 3;
@@ -277,92 +271,100 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
         D[kk * SD + p * TE + ee] = ee < ne ? Qt[i] : 0.0;
       }
 #pragma unroll 4
-      for (int i = tid; i < TE * P * 9; i += NTH) {
-        const bool in = i < ne * P * 9;
-        CS[i] = in ? St[i] : 0.0;
-        CS[TE * P * 9 + i] = in ? Et[i] : 0.0;
+      for (int i = tid; i < TE * 3 * P * 3; i += NTH) {  // [e][c][p][t] -> [e][p][c*3+t]
+        const int ee = i / (3 * P * 3), r = i - ee * 3 * P * 3, c = r / (P * 3), pt = r - c * P * 3;
+        CS[ee * CSE + (pt / 3) * CSS + c * 3 + pt % 3] = ee < ne ? St[i] : 0.0;
+      }
+      for (int i = tid; i < TE * CEE; i += NTH) {  // compact source rows
+        const int ee = i / CEE, j = i - ee * CEE;
+        const int p = j < 27 ? j / 9 : j < 36 ? 3 + (j - 27) / 3 : j < 54 ? 9 + (j - 36) : -1;
+        const int slot = j < 27 ? j % 9 : j < 36 ? (j - 27) % 3 : 0;
+        CE[i] = (ee < ne && p >= 0) ? Et[(ee * P + p) * 9 + slot] : 0.0;
       }
     }
     __syncthreads();
+    double I[P];
+    if (comb) {
 #pragma unroll
-    for (int mt = 0; mt < V::NCK; ++mt)
-#pragma unroll
-      for (int u = 0; u < 3; ++u)
-        if (rck[mt] >= 0) {
-          const int o = rck[mt] * SD + (p0 + u) * TE + ae;
-          const double2 d2 = *reinterpret_cast<const double2*>(D + o);
-          *reinterpret_cast<double2*>(IS + o) = make_double2(prm.dt * d2.x, prm.dt * d2.y);
-        }
+      for (int p = 0; p < P; ++p) I[p] = prm.dt * D[cr * SD + p * TE + cel];
+    }
 #pragma unroll 1
     for (int d = 0; d < N; ++d) {
-      double acc[V::NCK][3][2];
+      {
+        double acc[3][V::NCK][2];
 #pragma unroll
-      for (int mt = 0; mt < V::NCK; ++mt)
+        for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int u = 0; u < 3; ++u) acc[mt][u][0] = acc[mt][u][1] = 0.0;
-      if (g == 2) {
-        View<Ctx<N>, true> xv{x};
-        ck<N>(xv, acc);
-      } else {
-        View<Ctx<N>, false> xn{x};
-        ck<N>(xn, acc);
+          for (int mt = 0; mt < V::NCK; ++mt) acc[c][mt][0] = acc[c][mt][1] = 0.0;
+        ck<N>(x, acc);
+        int rck[V::NCK];
+        rows_of(V::ck_rows, ar, rck);
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int mt = 0; mt < V::NCK; ++mt)
+            if (rck[mt] >= 0)
+              *reinterpret_cast<double2*>(Z + (c * B + rck[mt]) * ZS + w * TE + ae) = make_double2(acc[c][mt][0], acc[c][mt][1]);
       }
-      source(acc, rck, D, src, p0, g, ae, ne);
-      __syncthreads();  // every warp done reading D^d
-      const double s1 = prm.scal[d], s2 = prm.scal[N + d];
-#pragma unroll
-      for (int mt = 0; mt < V::NCK; ++mt)
-#pragma unroll
-        for (int u = 0; u < 3; ++u)
-          if (rck[mt] >= 0) {
-            const int o = rck[mt] * SD + (p0 + u) * TE + ae;
-            const double v0 = s1 * acc[mt][u][0], v1 = s1 * acc[mt][u][1];
-            double2 i2 = *reinterpret_cast<const double2*>(IS + o);
-            i2.x = fma(s2, v0, i2.x);
-            i2.y = fma(s2, v1, i2.y);
-            *reinterpret_cast<double2*>(IS + o) = i2;
-            *reinterpret_cast<double2*>(D + o) = make_double2(v0, v1);
-          }
+      __syncthreads();  // Z complete, every warp done reading D^d
+      if (comb) {
+        const double s1 = prm.scal[d], s2 = prm.scal[N + d];
+        const bool last = d + 1 == N;
+        double* dr = D + cr * SD + cel;
+        combine<B, false>(Z + cr * ZS + cel, dr, CS + cel * CSE, CE + cel * CEE, [&](int p, double v) {
+          v *= s1;
+          I[p] = fma(s2, v, I[p]);
+          dr[p * TE] = last ? I[p] : v;  // D^{d+1}; after the last step the time integral
+        });
+      }
       __syncthreads();
     }
-    x.D = IS;
-    // volume + source on I, then traces of the elastic columns
-    int rq[V::NQ], rtr[V::NT];
-    rows_of(V::q_rows, ar, rq);
-    rows_of(V::tr_rows, ar, rtr);
-    double qa[V::NQ][3][2];
-#pragma unroll
-    for (int mt = 0; mt < V::NQ; ++mt)
-#pragma unroll
-      for (int u = 0; u < 3; ++u) qa[mt][u][0] = qa[mt][u][1] = 0.0;
-    if (g == 2) {
-      View<Ctx<N>, true> xv{x};
-      vol<N>(xv, qa);
-    } else {
-      View<Ctx<N>, false> xn{x};
-      vol<N>(xn, qa);
-    }
-    source(qa, rq, IS, src, p0, g, ae, ne);
+    // volume (left-first) and the traces of the elastic columns, both from I
+    double ta[4][V::NT][2];
     {
-      double ta[4][V::NT][2];
+      double acc[3][V::NQ][2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int mt = 0; mt < V::NT; ++mt) ta[i][mt][0] = ta[i][mt][1] = 0.0;
-      traces<N>(x, ta);
-      __syncthreads();  // TR aliases D: every warp past the recursion's last reads
-      for (int i = tid; i < 4 * V::BtR * TS; i += NTH) TR[i] = 0.0;
-      __syncthreads();
+        for (int mt = 0; mt < V::NQ; ++mt) acc[c][mt][0] = acc[c][mt][1] = 0.0;
+      vol<N>(x, acc);
+      int rq[V::NQ];
+      rows_of(V::q_rows, ar, rq);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int mt = 0; mt < V::NQ; ++mt)
+          if (rq[mt] >= 0)
+            *reinterpret_cast<double2*>(Z + (c * B + rq[mt]) * ZS + w * TE + ae) = make_double2(acc[c][mt][0], acc[c][mt][1]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int mt = 0; mt < V::NT; ++mt) ta[i][mt][0] = ta[i][mt][1] = 0.0;
+    traces<N>(x, ta);
+    __syncthreads();  // volume products complete
+    if (comb) {  // volume result V[r][p][e] into the thread's own Z slots (c, t) = (p / 9, p % 9)
+      double* zr = Z + cr * ZS + cel;
+      combine<B, true>(zr, D + cr * SD + cel, CS + cel * CSE, CE + cel * CEE,
+                       [&](int p, double v) { zr[(p / 9) * B * ZS + (p % 9) * TE] = v; });
+    }
+    __syncthreads();  // I no longer read: the traces take the D buffer
+    {
+      int rtr[V::NT];
+      rows_of(V::tr_rows, ar, rtr);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int mt = 0; mt < V::NT; ++mt)
-          if (rtr[mt] >= 0) {
+          if (rtr[mt] >= 0)
             *reinterpret_cast<double2*>(TR + (i * V::BtR + rtr[mt]) * TS + w * TE + ae) =
                 make_double2(ta[i][mt][0], ta[i][mt][1]);
-          }
+      for (int i = tid; i < 4 * (V::BtR - Bt) * 9 * TE; i += NTH) {  // padding rows of the traces
+        const int f = i / ((V::BtR - Bt) * 9 * TE), r = i - f * (V::BtR - Bt) * 9 * TE;
+        TR[(f * V::BtR + Bt + r / (9 * TE)) * TS + r % (9 * TE)] = 0.0;
+      }
     }
-    __syncthreads();  // traces complete; I no longer read
+    __syncthreads();
     {
       double* gt = prm.traces + e0 * 4 * Bt * 9;
       for (int i = tid; i < ne * 4 * Bt * 9; i += NTH) {
@@ -371,25 +373,40 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
         gt[i] = TR[(f * V::BtR + m) * TS + qq * TE + ee];
       }
     }
+    // local flux lifted onto the volume result
+    double qa[V::NQ][3][2];
+    int rq[V::NQ];
+    rows_of(V::q_rows, ar, rq);
+#pragma unroll
+    for (int mt = 0; mt < V::NQ; ++mt)
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const int p = p0 + u;
+        if (rq[mt] >= 0) {
+          const double* v = Z + ((p / 9) * B + rq[mt]) * ZS + (p % 9) * TE + ae;
+          qa[mt][u][0] = v[0];
+          qa[mt][u][1] = v[TE * 0 + 1];
+        } else {
+          qa[mt][u][0] = qa[mt][u][1] = 0.0;
+        }
+      }
     lift<N>(x, qa);
+    __syncthreads();  // every warp done reading the traces
 #pragma unroll
     for (int mt = 0; mt < V::NQ; ++mt)
 #pragma unroll
       for (int u = 0; u < 3; ++u)
-        if (rq[mt] >= 0) {
-          *reinterpret_cast<double2*>(IS + rq[mt] * SD + (p0 + u) * TE + ae) =  // I no longer read
-              make_double2(qa[mt][u][0], qa[mt][u][1]);
-        }
+        if (rq[mt] >= 0)
+          *reinterpret_cast<double2*>(D + rq[mt] * SD + (p0 + u) * TE + ae) = make_double2(qa[mt][u][0], qa[mt][u][1]);
     __syncthreads();
     double* Qw = prm.Q + e0 * P * B;
 #pragma unroll 4
     for (int i = tid; i < ne * P * B; i += NTH) {
       const int ee = i / (P * B), r = i - ee * P * B, p = r / B, kk = r - p * B;
-      Qw[i] += IS[kk * SD + p * TE + ee];
+      Qw[i] += D[kk * SD + p * TE + ee];
     }
   }
 }
-
 
 // Neighbour flux: Q += sum_i R^i (f^{h_i} T^{nb_i}_{j_i}) A-_i^T.
 // Per tile: the neighbours' traces of the shared faces and the tile's Q^n arrive by

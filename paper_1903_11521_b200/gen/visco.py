@@ -10,14 +10,13 @@ the B fragments built from shared memory are bank-conflict free.  Zero 8x4 block
 skipped (the zero-block exploitation of P:1351-1374).
 
 Emits ``csrc/generated/ydg_visco.cuh``: per order N <= 4 the row tables, the A-fragment
-table and four straight-line product functions (CK step, volume, traces, lift) written
+table and four straight-line product functions (CK step and volume left-first, i.e.
+Z^c_t = M^c D_t per elastic quantity t; traces; lift) written
 against a small context interface implemented in csrc/visco.cu:
 
-    x.star(c)              load the tile's star coefficients of reference direction c
-    x.chunk(buf, ks)       B fragments (3 quantity columns) of X^c = D A*^cT, rows 4ks..4ks+3
-    x.mma(acc, f, buf)     acc[u] += frag f x B[buf][u], u = 0..2
-    x.ib(buf, ks)          B fragment of one quantity column of I (traces)
+    x.ib(buf, ks)          B fragment of the warp's quantity column of D / I, rows 4ks..4ks+3
     x.mma1(acc, f, buf)    acc += frag f x B1[buf]
+    x.mma(acc, f, buf)     acc[u] += frag f x B[buf][u], u = 0..2 (lift)
     x.acoef(i)             flux-solver coefficients of face i (lift)
     x.ychunk(buf, i, ks)   B fragments of Y_i = T_i A+_iT, rows 4ks..4ks+3 of face i
 
@@ -152,34 +151,41 @@ def gen_order(N):
         body.append("}")
         return body
 
-    # CK step: sum_c Ktilde^c X^c, X^c = D A*^cT (chunks per (c, k-set))
+    # CK step, left-first: warp t computes Z^c_t = Ktilde^c D_t for c = 0..2 (one B fragment per
+    # k-set serves the three directions); the star / source combination follows in shared memory
     og = part["ck"]
     items = []
     ntile = 0
-    for c in range(3):
-        for ks, lst in _tiles([ck[c]], og, nks_b):
-            items.append((c, ks, [(0, mt, fr.add(ck[c], rows, ks)) for (_, mt, rows) in lst]))
-            ntile += len(lst)
+    for ks in range(nks_b):
+        lst = []
+        for c in range(3):
+            for (_, mt, rows) in _tiles([ck[c]], og, nks_b)[ks][1]:
+                lst.append((c, mt, fr.add(ck[c], rows, ks)))
+        items.append((0, ks, lst))
+        ntile += len(lst)
     counts["ck"] = ntile
-    L += seq_body(f"vck{N}", f"X& x, double (&a)[{len(og)}][3][2]", items,
-                  lambda c: [f"  x.star({c});"],
-                  lambda c, b, ks: f"x.chunk({b}, {ks});",
-                  lambda c, mi, mt, f, b: f"x.mma(a[{mt}], {f}, {b});")
+    L += seq_body(f"vck{N}", f"X& x, double (&a)[3][{len(og)}][2]", items,
+                  lambda _: [],
+                  lambda _, b, ks: f"x.ib({b}, {ks});",
+                  lambda _, c, mt, f, b: f"x.mma1(a[{c}][{mt}], {f}, {b});")
     ck_rows = [_rowword(g) for g in og]
 
-    # volume (K^c, chunks of X^c = I A*^cT) and lift (R^i, chunks of Y_i) share the output rows
+    # volume, left-first (W^c_t = Khat^c I_t), and lift (R^i, chunks of Y_i) share the output rows
     og = part["q"]
     items = []
     ntile = 0
-    for c in range(3):
-        for ks, lst in _tiles([vol[c]], og, nks_b):
-            items.append((c, ks, [(0, mt, fr.add(vol[c], rows, ks)) for (_, mt, rows) in lst]))
-            ntile += len(lst)
+    for ks in range(nks_b):
+        lst = []
+        for c in range(3):
+            for (_, mt, rows) in _tiles([vol[c]], og, nks_b)[ks][1]:
+                lst.append((c, mt, fr.add(vol[c], rows, ks)))
+        items.append((0, ks, lst))
+        ntile += len(lst)
     counts["vol"] = ntile
-    L += seq_body(f"vvol{N}", f"X& x, double (&a)[{len(og)}][3][2]", items,
-                  lambda c: [f"  x.star({c});"],
-                  lambda c, b, ks: f"x.chunk({b}, {ks});",
-                  lambda c, mi, mt, f, b: f"x.mma(a[{mt}], {f}, {b});")
+    L += seq_body(f"vvol{N}", f"X& x, double (&a)[3][{len(og)}][2]", items,
+                  lambda _: [],
+                  lambda _, b, ks: f"x.ib({b}, {ks});",
+                  lambda _, c, mt, f, b: f"x.mma1(a[{c}][{mt}], {f}, {b});")
     items = []
     ntile = 0
     for i in range(4):
