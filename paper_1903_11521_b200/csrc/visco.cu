@@ -135,17 +135,15 @@ __device__ __forceinline__ void rows_of(F words, int ar, int (&rows)[M]) {
 constexpr int ZS = 9 * TE;   // Z row stride
 constexpr int CSS = 10;      // star coefficients per (element, row): [c][t], padded
 constexpr int CSE = P * CSS;
-constexpr int CEE = 56;      // source coefficients per element (54 used)
+constexpr int CEE = 57;      // source coefficients per element (54 used; odd stride: no bank conflicts)
 
 template <int B>
 __device__ __forceinline__ double star_row(int p, const double* cs, const double (&z)[3][3]) {
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-#pragma unroll
-  for (int t = 0; t < 3; ++t) {
-    s0 = fma(cs[p * CSS + t], z[0][t], s0);
-    s1 = fma(cs[p * CSS + 3 + t], z[1][t], s1);
-    s2 = fma(cs[p * CSS + 6 + t], z[2][t], s2);
-  }
+  const double2* c2 = reinterpret_cast<const double2*>(cs + p * CSS);  // [c*3+t], 16-byte loads
+  const double2 a01 = c2[0], a23 = c2[1], a45 = c2[2], a67 = c2[3], a89 = c2[4];
+  const double s0 = fma(a23.x, z[0][2], fma(a01.y, z[0][1], a01.x * z[0][0]));
+  const double s1 = fma(a45.y, z[1][2], fma(a45.x, z[1][1], a23.y * z[1][0]));
+  const double s2 = fma(a89.x, z[2][2], fma(a67.y, z[2][1], a67.x * z[2][0]));
   return (s0 + s1) + s2;
 }
 __device__ __forceinline__ double source_row(int p, const double* ce, const double (&m)[18]) {
@@ -217,7 +215,7 @@ constexpr size_t smem_bytes() {
 template <int N>
 __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
   using V = VT<N>;
-  constexpr int B = V::B, Bt = V::Bt;
+  constexpr int B = V::B, Bt = V::Bt, KB = (B + 3) / 4;
   extern __shared__ __align__(16) double sm[];
   double* D = sm;                   // D^d, then I; after the traces: traces [4][BtR][TS], Q staging
   double* TR = D;
