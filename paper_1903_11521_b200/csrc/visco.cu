@@ -25,7 +25,7 @@ namespace ydg {
 namespace visco {
 
 constexpr int P = 27, TE = 8, W = 9, NTH = W * 32;
-constexpr int SD = P * TE;       // D / I row stride in doubles (216 = 8 mod 16: conflict-free combination rows)
+constexpr int SD = P * TE + 1;   // D / I row stride in doubles (odd: consecutive rows on distinct banks)
 constexpr int TS = 9 * TE + 12;  // trace row stride
 
 
@@ -34,6 +34,11 @@ __device__ __forceinline__ void l2_prefetch(const void* p, int64_t bytes) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(p), a0 = a & ~uintptr_t(15);
   const int n = static_cast<int>((a + bytes - a0 + 15) & ~int64_t(15));
   if (bytes > 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void st2(double* p, double a, double b) {  // (odd row strides: 8-byte aligned only)
+  p[0] = a;
+  p[1] = b;
 }
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
@@ -132,7 +137,7 @@ __device__ __forceinline__ void rows_of(F words, int ar, int (&rows)[M]) {
 // the stresses (SXX SXY SXZ) (SXY SYY SYZ) (SXZ SYZ SZZ) (setup.cpp star_cols, P = 27); the
 // source couples normal stresses to the 9 normal memory variables, shear stresses to 3, and
 // each memory variable to itself.  emit(p, value) receives every output exactly once.
-constexpr int ZS = 9 * TE;   // Z row stride
+constexpr int ZS = 9 * TE + 1;  // Z row stride (odd)
 constexpr int CSS = 10;      // star coefficients per (element, row): [c][t], padded
 constexpr int CSE = P * CSS;
 constexpr int CEE = 57;      // source coefficients per element (54 used; odd stride: no bank conflicts)
@@ -203,13 +208,14 @@ __device__ __forceinline__ void combine(const double* zr, const double* xr, cons
 }
 
 template <int N>
-constexpr int dsz() {  // D buffer (also holds the traces after the recursion)
-  return VT<N>::BR * SD > 4 * VT<N>::BtR * TS ? VT<N>::BR * SD : 4 * VT<N>::BtR * TS;
+constexpr int dsz() {  // D buffer (also holds the traces after the recursion); even: 16-byte alignment
+  return ((VT<N>::BR * SD > 4 * VT<N>::BtR * TS ? VT<N>::BR * SD : 4 * VT<N>::BtR * TS) + 1) & ~1;
 }
 template <int N>
+constexpr int zsize() { return (3 * VT<N>::B * ZS + 1) & ~1; }
+template <int N>
 constexpr size_t smem_bytes() {
-  return (static_cast<size_t>(dsz<N>()) + 3 * VT<N>::B * ZS + VT<N>::NFRAG * 32 + TE * (CSE + CEE)) *
-         sizeof(double);
+  return (static_cast<size_t>(dsz<N>()) + zsize<N>() + VT<N>::NFRAG * 32 + TE * (CSE + CEE)) * sizeof(double);
 }
 
 template <int N>
@@ -220,7 +226,7 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
   double* D = sm;                   // D^d, then I; after the traces: traces [4][BtR][TS], Q staging
   double* TR = D;
   double* Z = D + dsz<N>();         // left-first products Z^c_t [3][B][ZS]; after the volume: its result
-  double* FR = Z + 3 * B * ZS;
+  double* FR = Z + zsize<N>();
   double* CS = FR + V::NFRAG * 32;  // the tile's star rows [e][p][c*3+t] and sources [e][56]
   double* CE = CS + TE * CSE;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -240,8 +246,11 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
   x.p0 = p0;
   x.q = w;  // left-first / trace column of this warp (elastic quantity w < 9)
   const int ar = lane >> 2, ae = 2 * (lane & 3);  // accumulator row slot / first element
-  const bool comb = tid < TE * B;                 // combination thread: (row cr, element ce)
-  const int cr = tid >> 3, cel = tid & (TE - 1);
+  // combination thread (row cr, element cel): warps 0..7 take rows 0..31 of element w (the
+  // element's coefficients are warp-uniform: broadcast loads), warp 8 the rows >= 32
+  const int cr = w < TE ? lane : 32 + lane % (B > 32 ? B - 32 : 1);
+  const int cel = w < TE ? w : lane / (B > 32 ? B - 32 : 1);
+  const bool comb = w < TE ? lane < B : (B > 32 && lane < TE * (B - 32));
 
   const int64_t ntiles = (prm.n + TE - 1) / TE;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -302,7 +311,7 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
 #pragma unroll
           for (int mt = 0; mt < V::NCK; ++mt)
             if (rck[mt] >= 0)
-              *reinterpret_cast<double2*>(Z + (c * B + rck[mt]) * ZS + w * TE + ae) = make_double2(acc[c][mt][0], acc[c][mt][1]);
+              st2(Z + (c * B + rck[mt]) * ZS + w * TE + ae, acc[c][mt][0], acc[c][mt][1]);
       }
       __syncthreads();  // Z complete, every warp done reading D^d
       if (comb) {
@@ -333,7 +342,7 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
 #pragma unroll
         for (int mt = 0; mt < V::NQ; ++mt)
           if (rq[mt] >= 0)
-            *reinterpret_cast<double2*>(Z + (c * B + rq[mt]) * ZS + w * TE + ae) = make_double2(acc[c][mt][0], acc[c][mt][1]);
+            st2(Z + (c * B + rq[mt]) * ZS + w * TE + ae, acc[c][mt][0], acc[c][mt][1]);
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -395,7 +404,7 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
 #pragma unroll
       for (int u = 0; u < 3; ++u)
         if (rq[mt] >= 0)
-          *reinterpret_cast<double2*>(D + rq[mt] * SD + (p0 + u) * TE + ae) = make_double2(qa[mt][u][0], qa[mt][u][1]);
+          st2(D + rq[mt] * SD + (p0 + u) * TE + ae, qa[mt][u][0], qa[mt][u][1]);
     __syncthreads();
     double* Qw = prm.Q + e0 * P * B;
 #pragma unroll 4
@@ -560,7 +569,7 @@ __global__ void __launch_bounds__(NTH, 1) vm_neigh(const GenParams prm) {
 #pragma unroll
       for (int u = 0; u < 3; ++u)
         if (rq[mt] >= 0)
-          *reinterpret_cast<double2*>(QS + rq[mt] * SD + (p0 + u) * TE + ae) = make_double2(qa[mt][u][0], qa[mt][u][1]);
+          st2(QS + rq[mt] * SD + (p0 + u) * TE + ae, qa[mt][u][0], qa[mt][u][1]);
     __syncthreads();
     double* Qw = prm.Q + e0 * P * B;
 #pragma unroll 4
