@@ -144,11 +144,10 @@ constexpr int CEE = 57;      // source coefficients per element (54 used; odd st
 
 template <int B>
 __device__ __forceinline__ double star_row(int p, const double* cs, const double (&z)[3][3]) {
-  const double2* c2 = reinterpret_cast<const double2*>(cs + p * CSS);  // [c*3+t], 16-byte loads
-  const double2 a01 = c2[0], a23 = c2[1], a45 = c2[2], a67 = c2[3], a89 = c2[4];
-  const double s0 = fma(a23.x, z[0][2], fma(a01.y, z[0][1], a01.x * z[0][0]));
-  const double s1 = fma(a45.y, z[1][2], fma(a45.x, z[1][1], a23.y * z[1][0]));
-  const double s2 = fma(a89.x, z[2][2], fma(a67.y, z[2][1], a67.x * z[2][0]));
+  const double* c = cs + p * CSS;  // [c*3+t]; warp-uniform addresses (broadcast)
+  const double s0 = fma(c[2], z[0][2], fma(c[1], z[0][1], c[0] * z[0][0]));
+  const double s1 = fma(c[5], z[1][2], fma(c[4], z[1][1], c[3] * z[1][0]));
+  const double s2 = fma(c[8], z[2][2], fma(c[7], z[2][1], c[6] * z[2][0]));
   return (s0 + s1) + s2;
 }
 __device__ __forceinline__ double source_row(int p, const double* ce, const double (&m)[18]) {
