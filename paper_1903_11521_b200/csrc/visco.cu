@@ -415,32 +415,30 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
 }
 
 // Neighbour flux: Q += sum_i R^i (f^{h_i} T^{nb_i}_{j_i}) A-_i^T.
-// Per tile: the neighbours' traces of the shared faces and the tile's Q^n arrive by
-// cp.async (the next tile's neighbour slots one tile ahead), are rotated by f^h (CSR in
-// shared memory, degree-block diagonal), then the same Y-chunk + DMMA lift as the local
-// kernel with A- accumulates the update, added to the staged Q^n and stored once.
+// Software-pipelined over the CTA's tiles: while tile t is rotated and lifted, the
+// neighbours' traces of tile t+1 (cp.async, double-buffered), its Q^n and the neighbour
+// slots of tile t+2 are in flight.  The rotation by f^h runs over dense degree-block
+// windows; the lift (Y chunks + DMMA, as in the local kernel with A-) accumulates onto
+// Q^n, and the result leaves through a shared staging block with coalesced stores.
 template <int N>
 constexpr int zsz() { return 4 * VT<N>::BtR * TS; }
 template <int N>
 constexpr int gsz() { return 4 * TE * VT<N>::Bt * 9; }
 template <int N>
-constexpr int zg() { return zsz<N>() + gsz<N>() > VT<N>::BR * SD ? zsz<N>() + gsz<N>() : VT<N>::BR * SD; }
+constexpr int fnz() { return 3 * VT<N>::Bt * VT<N>::Bt; }  // dense f^0..2
 template <int N>
-constexpr int fnz() { return 3 * VT<N>::Bt * VT<N>::Bt; }  // bound on the nonzeros of f^0..2
+constexpr int nreg() {  // GT0 | Z | GT1 (the Q staging spans GT0+Z or Z+GT1) | QB
+  return gsz<N>() + zsz<N>() + gsz<N>() + TE * P * VT<N>::B;
+}
 template <int N>
 constexpr size_t nsmem_bytes() {
-  return (static_cast<size_t>(VT<N>::NFRAG) * 32 + zg<N>() + TE * P * VT<N>::B + 2 * 4 * TE + fnz<N>()) *
-             sizeof(double) +
-         (2 * 4 * TE + 3 * VT<N>::Bt + 1) * sizeof(int);
+  static_assert(gsz<N>() + zsz<N>() >= TE * P * VT<N>::B, "Q staging fits GT + Z");
+  return (static_cast<size_t>(VT<N>::NLIFTF) * 32 + nreg<N>() + 3 * 4 * TE + fnz<N>()) * sizeof(double) +
+         (3 * 4 * TE + 3 * VT<N>::Bt + 1) * sizeof(int);
 }
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
                "l"(src)
                : "memory");
 }
@@ -451,21 +449,21 @@ __global__ void __launch_bounds__(NTH, 1) vm_neigh(const GenParams prm) {
   using V = VT<N>;
   constexpr int B = V::B, Bt = V::Bt, BtR = V::BtR;
   extern __shared__ __align__(16) double sm[];
-  double* FR = sm;
-  double* Z = FR + V::NFRAG * 32;  // rotated neighbour traces [4][BtR][TS]
-  double* GT = Z + zsz<N>();       // gathered neighbour traces [e][face][n][9]
-  double* QS = Z;                  // Q-update staging [B][SD] (after the lift)
-  double* QB = Z + zg<N>();        // the tile's Q^n, element-major as in HBM
-  int64_t* NB = reinterpret_cast<int64_t*>(QB + TE * P * B);  // [2][e][face] neighbour ids
-  double* FD = reinterpret_cast<double*>(NB + 2 * 4 * TE);      // f^h dense [h][m][n]
-  int* JH = reinterpret_cast<int*>(FD + fnz<N>());             // [2][e*4+face] j | h << 2
-  int* LO = JH + 2 * 4 * TE;                                   // per (h, m): first nonzero column
+  double* FR = sm;                          // the lift's A fragments (table slots 0..NLIFTF-1)
+  double* GT0 = FR + V::NLIFTF * 32;        // gathered neighbour traces [e][face][n][9], even tiles
+  double* Z = GT0 + gsz<N>();               // rotated neighbour traces [4][BtR][TS]
+  double* GT1 = Z + zsz<N>();               // odd tiles
+  double* QB = GT1 + gsz<N>();              // the tile's Q^n, element-major as in HBM
+  int64_t* NB = reinterpret_cast<int64_t*>(QB + TE * P * B);  // [3][e*4+face] neighbour ids
+  double* FD = reinterpret_cast<double*>(NB + 3 * 4 * TE);      // f^h dense [h][m][n]
+  int* JH = reinterpret_cast<int*>(FD + fnz<N>());             // [3][e*4+face] j | h << 2
+  int* LO = JH + 3 * 4 * TE;                                   // per (h, m): first nonzero column
   int* WIDE = LO + 3 * Bt;                                     // any row wider than N + 1 columns
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int g = group_of(w), p0 = 3 * g;
   {
     const double* f = vfrag<N>();
-    for (int i = tid; i < V::NFRAG * 32; i += NTH) FR[i] = f[i];
+    for (int i = tid; i < V::NLIFTF * 32; i += NTH) FR[i] = f[i];
     // f^h is block diagonal by degree (width <= N + 1 per row): dense rows + column windows
     if (tid == 0) *WIDE = 0;
     for (int i = tid; i < fnz<N>(); i += NTH) FD[i] = 0.0;
@@ -493,48 +491,60 @@ __global__ void __launch_bounds__(NTH, 1) vm_neigh(const GenParams prm) {
   x.p0 = p0;
   const int ar = lane >> 2, ae = 2 * (lane & 3);
   const int64_t ntiles = (prm.n + TE - 1) / TE;
+  auto count = [&](int64_t t) {
+    const int64_t n0 = prm.e0 + t * TE;
+    return static_cast<int>(prm.e0 + prm.n - n0 < TE ? prm.e0 + prm.n - n0 : TE);
+  };
   auto slots = [&](int64_t t, int buf) {  // neighbour ids / j|h of tile t -> slot buffer buf
     const int64_t n0 = prm.e0 + t * TE;
-    const int nl = static_cast<int>(prm.e0 + prm.n - n0 < TE ? prm.e0 + prm.n - n0 : TE);
-    if (tid < nl * 4) {
+    if (tid < count(t) * 4) {
       cp_async8(NB + buf * 4 * TE + tid, prm.nb + n0 * 4 + tid);
       JH[buf * 4 * TE + tid] = prm.jh[n0 * 4 + tid];
     }
   };
-  if (blockIdx.x < ntiles) slots(blockIdx.x, 0);
+  auto gathers = [&](int64_t t, int sbuf, double* gt) {
+    const int64_t* nb = NB + sbuf * 4 * TE;
+    const int* jh = JH + sbuf * 4 * TE;
+    for (int i = tid; i < count(t) * 4 * Bt * 9; i += NTH) {
+      const int ef = i / (Bt * 9), nq = i - ef * Bt * 9;
+      cp_async8(gt + i, prm.traces + (nb[ef] * 4 + (jh[ef] & 3)) * Bt * 9 + nq);
+    }
+  };
+  auto qload = [&](int64_t t) {
+    const double* Qt = prm.Q + (prm.e0 + t * TE) * P * B;
+    for (int i = tid; i < count(t) * P * B; i += NTH) cp_async8(QB + i, Qt + i);
+  };
+  if (blockIdx.x < ntiles) {  // prologue: slots of the first two tiles, traces + Q^n of the first
+    slots(blockIdx.x, 0);
+    cp_async_wait_all();
+    __syncthreads();
+    gathers(blockIdx.x, 0, GT0);
+    qload(blockIdx.x);
+    if (blockIdx.x + gridDim.x < ntiles) slots(blockIdx.x + gridDim.x, 1);
+  }
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const int buf = it & 1;
+    const int cur = it & 1, sb = it % 3;
+    double* GT = cur ? GT1 : GT0;
+    double* QS = cur ? Z : GT0;  // Q staging: GT0 + Z or Z + GT1, never the next tile's GT
     const int64_t e0 = prm.e0 + tile * TE;
-    const int64_t left = prm.e0 + prm.n - e0;
-    const int ne = static_cast<int>(left < TE ? left : TE);
+    const int ne = count(tile);
     const int el = x.e < ne ? x.e : ne - 1;
     x.ap = prm.aminus + (e0 + el) * 4 * P * 9;
     cp_async_wait_all();
-    __syncthreads();  // slots of this tile landed; previous tile done with Z / GT / QS / QB
-    {
-      const int64_t* nb = NB + buf * 4 * TE;
-      const int* jh = JH + buf * 4 * TE;
-      for (int i = tid; i < ne * 4 * Bt * 9; i += NTH) {
-        const int ef = i / (Bt * 9), nq = i - ef * Bt * 9;
-        cp_async8(GT + i, prm.traces + (nb[ef] * 4 + (jh[ef] & 3)) * Bt * 9 + nq);
+    __syncthreads();  // traces + Q^n of this tile and the next tile's slots landed; staging free
+    const int64_t nxt = tile + gridDim.x;
+    if (nxt < ntiles) {
+      gathers(nxt, (it + 1) % 3, cur ? GT0 : GT1);
+      if (nxt + gridDim.x < ntiles) slots(nxt + gridDim.x, (it + 2) % 3);
+      if (tid == 0) {
+        const int64_t n0 = prm.e0 + nxt * TE;
+        l2_prefetch(prm.Q + n0 * P * B, count(nxt) * P * B * 8);
+        l2_prefetch(prm.aminus + n0 * 4 * P * 9, count(nxt) * 4 * P * 9 * 8);
       }
-      const double* Qt = prm.Q + e0 * P * B;
-      for (int i = tid; i < ne * P * B; i += NTH) cp_async8(QB + i, Qt + i);
-      if (tile + gridDim.x < ntiles) {
-        slots(tile + gridDim.x, buf ^ 1);
-        if (tid == 0) {
-          const int64_t n0 = prm.e0 + (tile + gridDim.x) * TE;
-          const int64_t nl = prm.e0 + prm.n - n0 < TE ? prm.e0 + prm.n - n0 : TE;
-          l2_prefetch(prm.Q + n0 * P * B, nl * P * B * 8);
-          l2_prefetch(prm.aminus + n0 * 4 * P * 9, nl * 4 * P * 9 * 8);
-        }
-      }
-      cp_async_wait_all();
     }
-    __syncthreads();
     {
-      const int* jh = JH + buf * 4 * TE;
+      const int* jh = JH + sb * 4 * TE;
       for (int i = tid; i < 4 * BtR * 9 * TE; i += NTH) {
         const int ee = i & (TE - 1), q = (i >> 3) % 9, fm = i / (9 * TE), m = fm % BtR, f = fm / BtR;
         double s = 0.0;
@@ -553,29 +563,32 @@ __global__ void __launch_bounds__(NTH, 1) vm_neigh(const GenParams prm) {
         Z[(f * BtR + m) * TS + q * TE + ee] = s;
       }
     }
-    __syncthreads();
+    // the lift accumulates onto Q^n (element-major in QB)
     double qa[V::NQ][3][2];
+    int rq[V::NQ];
+    rows_of(V::q_rows, ar, rq);
 #pragma unroll
     for (int mt = 0; mt < V::NQ; ++mt)
 #pragma unroll
-      for (int u = 0; u < 3; ++u) qa[mt][u][0] = qa[mt][u][1] = 0.0;
+      for (int u = 0; u < 3; ++u)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          qa[mt][u][h] = (rq[mt] >= 0 && ae + h < ne) ? QB[((ae + h) * P + p0 + u) * B + rq[mt]] : 0.0;
+    __syncthreads();  // Z complete; QB read
+    if (nxt < ntiles) qload(nxt);
     lift<N>(x, qa);
-    int rq[V::NQ];
-    rows_of(V::q_rows, ar, rq);
     __syncthreads();  // every warp done reading Z
 #pragma unroll
     for (int mt = 0; mt < V::NQ; ++mt)
 #pragma unroll
       for (int u = 0; u < 3; ++u)
-        if (rq[mt] >= 0)
-          st2(QS + rq[mt] * SD + (p0 + u) * TE + ae, qa[mt][u][0], qa[mt][u][1]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (rq[mt] >= 0) QS[((ae + h) * P + p0 + u) * B + rq[mt]] = qa[mt][u][h];
     __syncthreads();
     double* Qw = prm.Q + e0 * P * B;
 #pragma unroll 4
-    for (int i = tid; i < ne * P * B; i += NTH) {
-      const int ee = i / (P * B), r = i - ee * P * B, p = r / B, kk = r - p * B;
-      Qw[i] = QB[i] + QS[kk * SD + p * TE + ee];
-    }
+    for (int i = tid; i < ne * P * B; i += NTH) Qw[i] = QS[i];
   }
 }
 

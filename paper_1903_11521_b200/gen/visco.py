@@ -151,6 +151,22 @@ def gen_order(N):
         body.append("}")
         return body
 
+    # lift first: its fragments take table slots 0..NLIFTF-1 (the neighbour kernel stages
+    # only those)
+    og = part["q"]
+    items = []
+    ntile = 0
+    for i in range(4):
+        for ks, lst in _tiles([lift[i]], og, nks_t):
+            items.append((i, ks, [(0, mt, fr.add(lift[i], rows, ks)) for (_, mt, rows) in lst]))
+            ntile += len(lst)
+    counts["lift"] = ntile
+    nliftf = len(fr.vals)
+    L += seq_body(f"vlift{N}", f"X& x, double (&a)[{len(og)}][3][2]", items,
+                  lambda i: [f"  x.acoef({i});"],
+                  lambda i, b, ks: f"x.ychunk({b}, {i}, {ks});",
+                  lambda i, mi, mt, f, b: f"x.mma(a[{mt}], {f}, {b});")
+
     # CK step, left-first: warp t computes Z^c_t = Ktilde^c D_t for c = 0..2 (one B fragment per
     # k-set serves the three directions); the star / source combination follows in shared memory
     og = part["ck"]
@@ -186,17 +202,6 @@ def gen_order(N):
                   lambda _: [],
                   lambda _, b, ks: f"x.ib({b}, {ks});",
                   lambda _, c, mt, f, b: f"x.mma1(a[{c}][{mt}], {f}, {b});")
-    items = []
-    ntile = 0
-    for i in range(4):
-        for ks, lst in _tiles([lift[i]], og, nks_t):
-            items.append((i, ks, [(0, mt, fr.add(lift[i], rows, ks)) for (_, mt, rows) in lst]))
-            ntile += len(lst)
-    counts["lift"] = ntile
-    L += seq_body(f"vlift{N}", f"X& x, double (&a)[{len(og)}][3][2]", items,
-                  lambda i: [f"  x.acoef({i});"],
-                  lambda i, b, ks: f"x.ychunk({b}, {i}, {ks});",
-                  lambda i, mi, mt, f, b: f"x.mma(a[{mt}], {f}, {b});")
     q_rows = [_rowword(g) for g in og]
 
     # traces T_i = R^iT I of one quantity column per warp (all faces per k-set)
@@ -220,7 +225,7 @@ def gen_order(N):
     head = [f"template <> struct VT<{N}> {{",
             f"  static constexpr int B = {B}, Bt = {Bt}, BR = {4 * nks_b}, BtR = {4 * nks_t};",
             f"  static constexpr int NCK = {len(ck_rows)}, NQ = {len(q_rows)}, NT = {len(tr_rows)};",
-            f"  static constexpr int NFRAG = {len(fr.vals)};",
+            f"  static constexpr int NFRAG = {len(fr.vals)}, NLIFTF = {nliftf};",
             arr("ck_rows", ck_rows), arr("q_rows", q_rows), arr("tr_rows", tr_rows),
             "};"]
     flat = [v for f in fr.vals for v in f]
