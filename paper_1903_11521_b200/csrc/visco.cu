@@ -76,6 +76,10 @@ struct Ctx {
     for (int u = 0; u < 3; ++u)
 #pragma unroll
       for (int j = 0; j < 9; ++j) a[u][j] = ap[(i * P + p0 + u) * 9 + j];
+    if (i < 3)  // the next face's rows -> L1 (three 72-byte rows per lane)
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(ap + ((i + 1) * P + p0 + u) * 9));
   }
   __device__ __forceinline__ void ychunk(int buf, int i, int ks) {
     const double* r = TR + (i * V::BtR + 4 * ks + k) * TS + e;
