@@ -296,6 +296,7 @@ def run_ydg(args):
     ydg.ydg_profile(h, False)
     ms_max = allmax(ms, world)
     nz = ydg.ydg_query(h, ydg.YDG_Q_NZ_FLOPS)
+    kpath = int(ydg.ydg_query(h, ydg.YDG_Q_KERNEL_PATH))
     fl_local = ydg.ydg_query(h, ydg.YDG_Q_LOCAL_FLOPS)
     fl_neigh = ydg.ydg_query(h, ydg.YDG_Q_NEIGH_FLOPS)
     by_local = ydg.ydg_query(h, ydg.YDG_Q_LOCAL_BYTES)
@@ -334,16 +335,9 @@ def run_ydg(args):
     peak = FP64_PEAK_TFLOPS if cfg.precision == 8 else FP32_PEAK_TFLOPS
     ach_local = fl_local * nloc / (avg_local / 1e3) / 1e12 if world == 1 else fl_local * nloc / (t_local / args.steps / 1e3) / 1e12
     ach_neigh = fl_neigh * nloc / (avg_neigh / 1e3) / 1e12
-    # kernel names as ncu lists them: fp64 elastic = tensor-core kernels, fp32 = sparse FFMA
-    # kernels, viscoelastic / N=6 fp64 = generic kernels
-    if cfg.P == 27 and cfg.N <= 4 and os.environ.get("YDG_VISCO_GENERIC") != "1":
-        k_loc, k_nb, bound = "vm_local", "vm_neigh", "tensor"  # viscoelastic tensor-core local kernel
-    elif cfg.P == 27 or (cfg.precision == 8 and cfg.N == 6):
-        k_loc, k_nb, bound = "gen_local", "gen_neigh", "alu"
-    elif cfg.precision == 8:
-        k_loc, k_nb, bound = "dm_local", "dm_flux", "tensor"
-    else:
-        k_loc, k_nb, bound = "ader_local", "ader_neigh", "alu"
+    # kernel names as ncu lists them, from the path the library reports it runs
+    k_loc, k_nb, bound = {0: ("dm_local", "dm_flux", "tensor"), 1: ("ader_local", "ader_neigh", "alu"),
+                          2: ("vm_local", "vm_neigh", "tensor"), 3: ("gen_local", "gen_neigh", "alu")}[kpath]
     dominant = k_loc if t_local >= t_neigh else k_nb
     traffic = load_traffic(cfg.name)
     dom_ach = ach_local if dominant == k_loc else ach_neigh

@@ -58,7 +58,10 @@ enum {
   YDG_Q_NEIGH_FLOPS = 12,      /* nonzero flops / element of the neighbour kernel          */
   YDG_Q_PROF_LOCAL_MS = 13,    /* profiling: summed device time of local-kernel launches   */
   YDG_Q_PROF_NEIGH_MS = 14,    /* profiling: summed device time of neighbour launches      */
-  YDG_Q_PROF_LAUNCHES = 15     /* profiling: number of timed kernel launches               */
+  YDG_Q_PROF_LAUNCHES = 15,    /* profiling: number of timed kernel launches               */
+  YDG_Q_KERNEL_PATH = 16       /* kernels a step runs: 0 fp64 elastic tensor-core (dm_local/
+                                  dm_flux), 1 fp32 sparse FFMA (ader_*), 2 viscoelastic
+                                  tensor-core (vm_local/vm_neigh), 3 generic CSR (gen_*)    */
 };
 
 typedef struct ydg_solver ydg_solver; /* opaque, owned by the library */

@@ -398,6 +398,10 @@ int generic_upload_mesh(ydg_solver* h, const double* xyz, const double* material
   }
   int ecols[27][9], scols[27][3];
   generic_patterns(P, ecols, scols);
+  if (P == 27) {
+    if (!(anel[0] > 0.0) || !std::isfinite(anel[0])) h->visco_tc = false;
+    for (int l = 0; l < 3; ++l) h->gp.wratio[l] = h->visco_tc ? anel[l] / anel[0] : 1.0;
+  }
   const int64_t chunk = 65536;
   std::vector<double> st, ap, am, sr;
   for (int64_t e0 = 0; e0 < ne; e0 += chunk) {
@@ -419,6 +423,18 @@ int generic_upload_mesh(ydg_solver* h, const double* xyz, const double* material
               return fail(h, YDG_ERR_MESH, "flux solver couples a memory variable (unexpected)");
             }
           }
+    if (P == 27 && h->visco_tc) {  // the tensor-core kernel scales mechanism 0's memory-variable rows
+      for (int64_t t = 0; t < n && h->visco_tc; ++t)
+        for (int cc = 0; cc < 3; ++cc)
+          for (int sv = 0; sv < 6; ++sv)
+            for (int l = 1; l < 3; ++l)
+              for (int k = 0; k < 3; ++k) {
+                const double b = c.star[((t * 3 + cc) * P + 9 + sv) * 3 + k];
+                const double v = c.star[((t * 3 + cc) * P + 9 + 6 * l + sv) * 3 + k];
+                if (std::fabs(v - h->gp.wratio[l] * b) > 1e-13 * (std::fabs(v) + std::fabs(b)) + 1e-300)
+                  h->visco_tc = false;  // not proportional: the CSR kernels take over
+              }
+    }
     CUDA_OR_FAIL(h, cudaMemcpy(static_cast<double*>(h->star) + e0 * 3 * P * 3, c.star.data(), c.star.size() * 8,
                                cudaMemcpyHostToDevice));
     CUDA_OR_FAIL(h, cudaMemcpy(static_cast<double*>(h->aplus) + e0 * 4 * P * 9, ap.data(), ap.size() * 8,
@@ -828,6 +844,7 @@ int ydg_query(ydg_solver* h, int what, double* v) {
     case YDG_Q_LAUNCHES_PER_STEP: *v = h->nranks > 1 ? 5 : 2; break;
     case YDG_Q_LOCAL_BYTES: *v = alg_bytes_local(h); break;
     case YDG_Q_NEIGH_BYTES: *v = alg_bytes_neigh(h); break;
+    case YDG_Q_KERNEL_PATH: *v = h->generic ? (h->visco_tc ? 2 : 3) : (h->prec == 8 ? 0 : 1); break;
     // fp64: the local kernel runs CK, time integral, volume, traces; both flux terms are in
     // the flux kernel.  fp32: the local flux is in the local kernel.
     case YDG_Q_LOCAL_FLOPS: *v = h->P == 27 ? nz_flops_visco_local(h->N) : nz_flops_local(h->N, h->prec == 8); break;

@@ -22,6 +22,8 @@ struct GenParams {
   int64_t e0, n;        // element range of this launch
   double dt;
   double scal[12];      // dt/(d+1), d < N; dt/(d+2), d < N
+  double wratio[3];     // omega_l / omega_0: the memory-variable star rows of mechanism l are
+                        // wratio[l] x those of mechanism 0 (checked at upload; visco.cu)
 };
 
 size_t gen_local_smem(int B, int Bt, int P);

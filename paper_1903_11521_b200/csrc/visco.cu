@@ -173,7 +173,8 @@ __device__ __forceinline__ double source_row(int p, const double* ce, const doub
 // VEL_FIRST: the velocity rows (stress columns) before the others, with every Z value of the
 // thread loaded up front -- the volume writes its result into the thread's own Z slots.
 template <int B, bool VEL_FIRST, class Emit>
-__device__ __forceinline__ void combine(const double* zr, const double* xr, const double* cs, const double* ce, Emit emit) {
+__device__ __forceinline__ void combine(const double* zr, const double* xr, const double* cs, const double* ce,
+                                        const double (&wr)[3], Emit emit) {
   constexpr int cols[3][3] = {{0, 3, 5}, {3, 1, 4}, {5, 4, 2}};
   double m[18], zv[3][3];
 #pragma unroll
@@ -202,10 +203,20 @@ __device__ __forceinline__ void combine(const double* zr, const double* xr, cons
     for (int u = 0; u < 3; ++u) emit(6 + u, v[u]);
   };
   if (VEL_FIRST) vel_rows();
+  // memory variables: the star rows of mechanism l are omega_l / omega_0 times those of
+  // mechanism 0 (A^d rows -omega_l eps(v); checked at upload), so 6 rows are contracted
+  double base[6];
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     if (p >= 6 && p < 9) continue;
-    emit(p, star_row<B>(p, cs, zv) + source_row(p, ce, m));
+    double sv;
+    if (p < 15) {
+      sv = star_row<B>(p, cs, zv);
+      if (p >= 9) base[p - 9] = sv;
+    } else {
+      sv = wr[(p - 9) / 6] * base[(p - 9) % 6];
+    }
+    emit(p, sv + source_row(p, ce, m));
   }
   if (!VEL_FIRST) vel_rows();
 }
@@ -321,7 +332,7 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
         const double s1 = prm.scal[d], s2 = prm.scal[N + d];
         const bool last = d + 1 == N;
         double* dr = D + cr * SD + cel;
-        combine<B, false>(Z + cr * ZS + cel, dr, CS + cel * CSE, CE + cel * CEE, [&](int p, double v) {
+        combine<B, false>(Z + cr * ZS + cel, dr, CS + cel * CSE, CE + cel * CEE, prm.wratio, [&](int p, double v) {
           v *= s1;
           I[p] = fma(s2, v, I[p]);
           dr[p * TE] = last ? I[p] : v;  // D^{d+1}; after the last step the time integral
@@ -355,7 +366,7 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
     __syncthreads();  // volume products complete
     if (comb) {  // volume result V[r][p][e] into the thread's own Z slots (c, t) = (p / 9, p % 9)
       double* zr = Z + cr * ZS + cel;
-      combine<B, true>(zr, D + cr * SD + cel, CS + cel * CSE, CE + cel * CEE,
+      combine<B, true>(zr, D + cr * SD + cel, CS + cel * CSE, CE + cel * CEE, prm.wratio,
                        [&](int p, double v) { zr[(p / 9) * B * ZS + (p % 9) * TE] = v; });
     }
     __syncthreads();  // I no longer read: the traces take the D buffer

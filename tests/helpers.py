@@ -16,10 +16,14 @@ def make_inputs(cfg):
     return xyz, vid, mat, Q, an
 
 
+LAST_PATH = {}  # kernel path (ydg_query YDG_Q_KERNEL_PATH) of the last run_gpu call
+
+
 def run_gpu(cfg, xyz, vid, mat, Q, an=None, nsteps=None, dt=None):
     import paper_1903_11521_b200 as ydg
     h = ydg.ydg_create(cfg.N, cfg.P, cfg.precision)
     ydg.ydg_upload_mesh(h, xyz, vid, mat, an)
+    LAST_PATH["path"] = int(ydg.ydg_query(h, ydg.YDG_Q_KERNEL_PATH))
     ydg.ydg_upload_dofs(h, 0, Q.astype(h.dtype))
     ydg.ydg_step(h, cfg.dt if dt is None else dt, cfg.steps if nsteps is None else nsteps)
     out = ydg.ydg_download_dofs(h, 0, Q.shape[0])

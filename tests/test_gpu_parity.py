@@ -8,7 +8,7 @@ import pytest
 
 import synth
 from oracle import mesh as omesh
-from tests.helpers import make_inputs, rel_err, run_gpu, run_oracle
+from tests.helpers import LAST_PATH, make_inputs, rel_err, run_gpu, run_oracle
 
 pytestmark = pytest.mark.gpu
 
@@ -119,6 +119,7 @@ def test_c3_viscoelastic_replica():
     generic CUDA path vs the oracle of reading R14."""
     cfg = synth.CONFIGS["c3"].replica(3, steps=2)
     err, *_ = _parity(cfg)
+    assert LAST_PATH["path"] == 2  # the viscoelastic tensor-core kernels ran
     assert err["all"] <= TOL[8], err
     assert err["memory"] <= 1e-11, err
 
@@ -129,6 +130,7 @@ def test_viscoelastic_orders(N):
     (3x3x2 cubes: 108 elements = 13 full 8-element tiles + a ragged tile of 4)."""
     cfg = _cfg("c3", N=N, nx=3, ny=3, nz=2, steps=2)
     err, *_ = _parity(cfg)
+    assert LAST_PATH["path"] == 2
     assert err["all"] <= TOL[8], err
     assert err["memory"] <= 1e-11, err
 
@@ -138,6 +140,7 @@ def test_viscoelastic_csr_kernel(monkeypatch):
     monkeypatch.setenv("YDG_VISCO_GENERIC", "1")
     cfg = synth.CONFIGS["c3"].replica(3, steps=1)
     err, *_ = _parity(cfg)
+    assert LAST_PATH["path"] == 3
     assert err["all"] <= TOL[8], err
 
 
