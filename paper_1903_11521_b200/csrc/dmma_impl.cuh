@@ -109,7 +109,7 @@ __device__ __forceinline__ double afrag_s(const Ctx& x, int i) { return x.fs[i *
 #ifndef YDG_FLUX_FS
 #define YDG_FLUX_FS 0
 #endif
-constexpr bool kLocalFs = YDG_LOCAL_FS, kFluxFs = YDG_FLUX_FS;
+constexpr bool kLocalFs = YDG_LOCAL_FS, kFluxFs = YDG_FLUX_FS || kFluxGroups > 1;
 // capacity of the local kernel's fragment buffer (fragments of 256 B; the rest of the
 // product reads the global table)
 #ifndef YDG_LOCAL_FS_CAP
@@ -495,6 +495,8 @@ struct Layout {
   // coefficients, slots, j|h, mbarriers
   static constexpr int FACEF = kLF * G::TS;  // doubles of one face of a flux CTA
   static constexpr int FLUX = 2 * FACEF + 2 * G::Bt * kRSF + kFaceCoeffs * kLF + 16 + 2;  // + slots, j|h, mbarriers
+  static constexpr int FLUXG = (FLUX + 15) & ~15;  // one group's region (128-byte aligned)
+  static constexpr int FLUXCTA = kFluxGroups * FLUXG + (kFluxFs ? G::LIFT_NF * 32 : 0);
 };
 
 // ---- asynchronous copy helpers (TMA bulk copies + mbarrier, Ampere-style cp.async)
@@ -730,12 +732,22 @@ __global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_local(const __grid_consta
 // (e, m) builds the Godunov flux of row m from T and Z (godunov_flux), writing Y (rows
 // [m][288]), and the warp lifts its own columns of Y with DMMAs into Q.
 template <int N>
-__global__ void __launch_bounds__(kTF, kFluxCtas) dm_flux(const __grid_constant__ StepParams<double> prm) {
+__global__ void __launch_bounds__(kTF * kFluxGroups, kFluxGroups == 1 ? kFluxCtas : 1)
+    dm_flux(const __grid_constant__ StepParams<double> prm) {
   using G = DG<N>;
   using Lay = Layout<N>;
   constexpr int B = G::B, Bt = G::Bt, TS = G::TS, FACE = Lay::FACE, FACEF = Lay::FACEF;
   constexpr int FCN = kFaceCoeffs * kLF;  // factored flux solvers of one (tile, face, half)
-  extern __shared__ __align__(128) double smem[];
+  extern __shared__ __align__(128) double smem_cta[];
+  // group grp (3 warps) of the CTA works as one virtual CTA vb of a grid of vgrid
+  const int grp = threadIdx.x / kTF, tid = threadIdx.x % kTF;
+  const int64_t vb = static_cast<int64_t>(blockIdx.x) * kFluxGroups + grp;
+  const int64_t vgrid = static_cast<int64_t>(gridDim.x) * kFluxGroups;
+  double* smem = smem_cta + grp * Lay::FLUXG;
+  auto gsync = [&]() {
+    if constexpr (kFluxGroups == 1) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "n"(kTF) : "memory");
+  };
   double* O = smem;                    // own face block [lane][TS] of the CTA's 8 elements
   double* NB = smem + FACEF;           // [lane][TS] neighbour face blocks
   double* Y0 = smem + 2 * FACEF;       // [2][Bt][72]: rotated neighbour rows, then the flux
@@ -745,19 +757,25 @@ __global__ void __launch_bounds__(kTF, kFluxCtas) dm_flux(const __grid_constant_
   int8_t* JHX = JH + kJH;                               // [16] of the next item's (tile, face)
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(JHX + kJH);  // own, nb
   Ctx x;
-  x.lane = threadIdx.x & 31;
-  x.w = threadIdx.x >> 5;
+  x.lane = tid & 31;
+  x.w = tid >> 5;
   x.col0 = 3 * x.w * kLF;
   x.sh4 = 8 * (x.lane & 3);
   x.sh8 = 8 * (x.lane >> 2);
   x.frags = frag_table<N>();
+  if constexpr (kFluxFs) {  // the lift's A fragments, once per CTA
+    double* fs = smem_cta + kFluxGroups * Lay::FLUXG;
+    for (int i = threadIdx.x; i < G::LIFT_NF * 32; i += kTF * kFluxGroups) fs[i] = x.frags[G::LIFT_F0 * 32 + i];
+    x.fs = fs;
+    __syncthreads();
+  }
   const int64_t nitems = prm.ntiles * kHalves;  // (tile, half) work units
-  if (blockIdx.x >= nitems) return;
-  if (threadIdx.x == 0) {
+  if (vb >= nitems) return;
+  if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
   }
-  __syncthreads();
+  gsync();
   // Items k = (unit, face) in this CTA's order, unit = (tile, half); item k's "own" copy
   // (thread 0) brings the unit's face block, its flux coefficients and j|h, and the
   // neighbour slots and j|h of item k+1, so no global load sits on the per-face path.
@@ -786,8 +804,8 @@ __global__ void __launch_bounds__(kTF, kFluxCtas) dm_flux(const __grid_constant_
     }
   };
   {
-    const int64_t u0 = blockIdx.x;
-    if (threadIdx.x == 0) {
+    const int64_t u0 = vb;
+    if (tid == 0) {
       const int64_t tile = prm.tile0 + u0 / kHalves, half = u0 % kHalves;
       int32_t nbs[kLF];
       int8_t jhs[kLF];
@@ -803,11 +821,11 @@ __global__ void __launch_bounds__(kTF, kFluxCtas) dm_flux(const __grid_constant_
   unsigned ph_o = 0, ph_n = 0;
   // thread roles: rotation (element re, column rp) for threads < 72; Godunov rows
   // m = rp + 12 i of element re
-  const int re = threadIdx.x % kLF, rp = threadIdx.x / kLF;
-  for (int64_t u = blockIdx.x; u < nitems; u += gridDim.x) {
+  const int re = tid % kLF, rp = tid / kLF;
+  for (int64_t u = vb; u < nitems; u += vgrid) {
     const int64_t tile = prm.tile0 + u / kHalves, half = u % kHalves;
     x.qcol0 = 3 * x.w * kL + half * kLF;
-    const bool more = u + gridDim.x < nitems;
+    const bool more = u + vgrid < nitems;
 #pragma unroll
     for (int F = 0; F < 4; ++F) {
       // Y buffer F & 1: last read by the paired lift of faces F-2, F-1 (followed by a barrier)
@@ -817,7 +835,7 @@ __global__ void __launch_bounds__(kTF, kFluxCtas) dm_flux(const __grid_constant_
       ph_o ^= 1;
       mbar_wait(&bar[1], ph_n);  // neighbour blocks of this item
       ph_n ^= 1;
-      if (threadIdx.x < kP * kLF) {  // z = f^h t on column rp of element re's neighbour block -> Y
+      if (tid < kP * kLF) {  // z = f^h t on column rp of element re's neighbour block -> Y
         const int h = JH[half * kLF + re] >> 2;
         const double* zc = NB + re * TS + rp;
         double t[Bt];
@@ -828,12 +846,12 @@ __global__ void __launch_bounds__(kTF, kFluxCtas) dm_flux(const __grid_constant_
       double fc[kFaceCoeffs];
 #pragma unroll
       for (int k = 0; k < kFaceCoeffs; ++k) fc[k] = FC[k * kLF + re];
-      __syncthreads();  // rotated rows visible; every read of NB (and of NBX, JHX) done
-      if (threadIdx.x == 0 && has_next) {
-        const int nhalf = F < 3 ? half : (u + gridDim.x) % kHalves;
+      gsync();  // rotated rows visible; every read of NB (and of NBX, JHX) done
+      if (tid == 0 && has_next) {
+        const int nhalf = F < 3 ? half : (u + vgrid) % kHalves;
         issue_nb(NBX, JHX + nhalf * kLF);
-      } else if (threadIdx.x == 32 && F == 3 && more) {  // next unit's Q -> L2
-        prefetch_l2(prm.Q + (prm.tile0 + (u + gridDim.x) / kHalves) * B * kRS, B * kRS * sizeof(double));
+      } else if (tid == 32 && F == 3 && more) {  // next unit's Q -> L2
+        prefetch_l2(prm.Q + (prm.tile0 + (u + vgrid) / kHalves) * B * kRS, B * kRS * sizeof(double));
       }
       {  // Godunov flux of rows m = rp, rp + 12, ... of element re, in place in Y
         const double* T = O + re * TS;
@@ -849,12 +867,12 @@ __global__ void __launch_bounds__(kTF, kFluxCtas) dm_flux(const __grid_constant_
           for (int q = 0; q < kP; ++q) Y[swzf(m, q * kLF + re)] = y[q];
         }
       }
-      __syncthreads();  // every read of O, FC, JH done; Y complete
-      if (threadIdx.x == 0 && has_next) {  // item k+1's own copy (and item k+2's slots)
-        const int64_t nu = F < 3 ? u : u + gridDim.x;
+      gsync();  // every read of O, FC, JH done; Y complete
+      if (tid == 0 && has_next) {  // item k+1's own copy (and item k+2's slots)
+        const int64_t nu = F < 3 ? u : u + vgrid;
         const int nF = F < 3 ? F + 1 : 0;
-        const bool nn = nF < 3 || nu + gridDim.x < nitems;
-        issue_own(nu, nF, nF < 3 ? nu : nu + gridDim.x, nF < 3 ? nF + 1 : 0, nn);
+        const bool nn = nF < 3 || nu + vgrid < nitems;
+        issue_own(nu, nF, nF < 3 ? nu : nu + vgrid, nF < 3 ? nF + 1 : 0, nn);
       }
       // lift and Q update per pair of faces (both Y buffers), two m-tiles at a time; the
       // unit's Q stays in L2 across its two updates.  The next pair's rotation rewrites the
@@ -863,7 +881,7 @@ __global__ void __launch_bounds__(kTF, kFluxCtas) dm_flux(const __grid_constant_
         double* Qt = prm.Q + tile * B * kRS;
         if (F == 1) G::template lift2<0>(x, Y0, Y0 + Bt * kRSF, Qt);
         else G::template lift2<1>(x, Y0, Y0 + Bt * kRSF, Qt);
-        __syncthreads();
+        gsync();
       }
     }
   }

@@ -98,7 +98,7 @@ const void* pick_neigh(int N, int eb) {
 // fp64 tensor-core kernels: kDmWarps warps (dmma_impl.cuh kW); fp32 sparse kernels: 9 warps
 int block_threads(int elem_bytes) { return elem_bytes == 8 ? kDmWarps * 32 : kP * kLanes; }
 // fp64 flux kernel: 3 warps per CTA (8-element halves of the 16-element tiles)
-int flux_threads(int elem_bytes) { return elem_bytes == 8 ? 3 * 32 : kP * kLanes; }
+int flux_threads(int elem_bytes) { return elem_bytes == 8 ? 3 * 32 * kFluxGroups : kP * kLanes; }
 int nB(int N) { return (N + 1) * (N + 2) * (N + 3) / 6; }
 int nBt(int N) { return (N + 1) * (N + 2) / 2; }
 
@@ -158,7 +158,9 @@ cudaError_t launch_neigh(int N, const StepParams<T>& p, int grid, cudaStream_t s
   const void* f = pick_neigh(N, sizeof(T));
   if (!f) return cudaErrorInvalidValue;
   void* args[] = {const_cast<StepParams<T>*>(&p)};
-  return cudaLaunchKernel(f, dim3(grid), dim3(flux_threads(sizeof(T))), args, neigh_smem_bytes(N, sizeof(T)), s);
+  // fp64: grid counts 3-warp groups (virtual CTAs); kFluxGroups of them share one CTA
+  const int ctas = sizeof(T) == 8 ? (grid + kFluxGroups - 1) / kFluxGroups : grid;
+  return cudaLaunchKernel(f, dim3(ctas), dim3(flux_threads(sizeof(T))), args, neigh_smem_bytes(N, sizeof(T)), s);
 }
 template <typename T>
 cudaError_t launch_to_tiled(int P, int B, int L, const T* canon, T* tiled, int64_t first, int64_t count,

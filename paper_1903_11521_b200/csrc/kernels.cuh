@@ -14,6 +14,13 @@ constexpr int kLanes = 32;   // elements per tile of the fp32 kernels
 constexpr int kDmLanes = YDG_DM_LANES;
 constexpr int kDmWarps = 3 * (kDmLanes / 8);
 constexpr int kDmCtasPerSm = 12 / kDmWarps;
+// fp64 flux kernel: 3-warp groups (8-element halves) per CTA.  1: one group per CTA, four
+// CTAs per SM; 4: one CTA per SM whose four groups share the lift's A fragments staged in
+// shared memory (named barriers per group).
+#ifndef YDG_FLUX_GROUPS
+#define YDG_FLUX_GROUPS 4
+#endif
+constexpr int kFluxGroups = YDG_FLUX_GROUPS;
 constexpr int kMaxN = 6;
 
 template <typename T>
