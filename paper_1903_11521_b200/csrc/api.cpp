@@ -671,7 +671,7 @@ int ydg_upload_mesh(ydg_solver* h, int64_t ne, const double* xyz, const int64_t*
   // grids: resident CTAs per SM x SMs
   int sms = 0, occ_l = 0, occ_n = 0;
   CUDA_OR_FAIL(h, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->dev));
-  occ_l = eb == 8 ? kDmCtasPerSm : 1;  // fp64: 12 warps per SM in kDmCtasPerSm CTAs
+  occ_l = eb == 8 ? kDmCtasPerSm : 1;  // fp64: 12 warps per SM in kDmCtasPerSm 6-warp groups
   occ_n = eb == 8 ? 4 : 1;  // fp64 flux kernel: four 3-warp groups (8-element halves) per SM
   h->grid_local = sms * occ_l;
   h->grid_neigh = sms * occ_n;

@@ -68,6 +68,12 @@ struct Ctx {
   double a[9];        // star matrices, row p = 3g + xk: a[3c + j] = A*^c[p][q_j]
   int q0, q1, q2;     // star columns of row p
   double dt;
+  int tid, grp;       // thread index within the (group of the) CTA, group index
+  int shcap;          // grouped local kernel: fragments held in the shared buffer
+  __device__ __forceinline__ void sync() const {  // barrier of the thread's group
+    if (kLocalGroups == 1) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "n"(kT) : "memory");
+  }
   const double* scal;  // kernel-parameter space: dt/(d+1) at [d], dt/(d+2) at [N + d]
   int N;
 };
@@ -109,14 +115,17 @@ __device__ __forceinline__ double afrag_s(const Ctx& x, int i) { return x.fs[i *
 #ifndef YDG_FLUX_FS
 #define YDG_FLUX_FS 0
 #endif
-constexpr bool kLocalFs = YDG_LOCAL_FS, kFluxFs = YDG_FLUX_FS || kFluxGroups > 1;
+constexpr bool kLocalFs = YDG_LOCAL_FS && kLocalGroups == 1, kFluxFs = YDG_FLUX_FS || kFluxGroups > 1;
 // capacity of the local kernel's fragment buffer (fragments of 256 B; the rest of the
 // product reads the global table)
 #ifndef YDG_LOCAL_FS_CAP
 #define YDG_LOCAL_FS_CAP 56
 #endif
 constexpr int kLocalFsCap = YDG_LOCAL_FS_CAP;
+// g: table index; r: index within the product's staged region.  The grouped kernel holds
+// table slots [0, shcap) (CK step 0, then the volume) in a static shared buffer.
 __device__ __forceinline__ double afrag_l(const Ctx& x, int g, int r) {
+  if constexpr (kLocalGroups > 1) return g < x.shcap ? afrag_s(x, g) : afrag(x, g);
   return (kLocalFs && r < kLocalFsCap) ? afrag_s(x, r) : afrag(x, g);
 }
 __device__ __forceinline__ double afrag_f(const Ctx& x, int g, int r) { return kFluxFs ? afrag_s(x, r) : afrag(x, g); }
@@ -251,7 +260,7 @@ __device__ __forceinline__ void ck_wb(Ctx& x, const double (&acc)[kU][2], int d,
 // Rows [LO, HI) of the time-integral region receive no derivative: I = dt * Q.
 template <int LO, int HI>
 __device__ __forceinline__ void scale_irows(Ctx& x) {
-  for (int i = threadIdx.x; i < (HI - LO) * kRS; i += kT) {
+  for (int i = x.tid; i < (HI - LO) * kRS; i += kT) {
     double* v = x.I + (LO + i / kRS) * kRS + i % kRS;
     *v = x.dt * *v;
   }
@@ -491,6 +500,13 @@ struct Layout {
   static constexpr int FSMAX0 = G::CK0_NF > G::VOL_NF ? G::CK0_NF : G::VOL_NF;
   static constexpr int FSMAX = kLocalFs ? (FSMAX0 < kLocalFsCap ? FSMAX0 : kLocalFsCap) : 0;
   static constexpr int LOCAL = FOFF + FSMAX * 32 + 2;  // + two mbarriers
+  static constexpr int LOCALG = (LOCAL + 15) & ~15;     // one group's region (grouped kernel)
+  // grouped kernel: CK step 0's fragments, then the volume's, as many as fit in 227 KB
+  static constexpr int LSH0 = (227 * 1024 / 8 - kLocalGroups * LOCALG) / 32;
+  // (table slots = shared slots: CK step 0's fragments first, the volume's next)
+  static constexpr bool LSH_OK = G::CK0_F0 == 0 && G::VOL_F0 == G::CK0_NF;
+  static constexpr int LSH = (kLocalGroups == 1 || !LSH_OK) ? 0 : (LSH0 < G::CK0_NF + G::VOL_NF ? LSH0 : G::CK0_NF + G::VOL_NF);
+  static constexpr int LOCALCTA = kLocalGroups == 1 ? LOCAL : kLocalGroups * LOCALG + LSH * 32;
   // flux kernel (8-element CTAs): own face block, neighbour blocks, two Y buffers,
   // coefficients, slots, j|h, mbarriers
   static constexpr int FACEF = kLF * G::TS;  // doubles of one face of a flux CTA
@@ -548,14 +564,16 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
 }
 
 __device__ __forceinline__ void init_ctx(Ctx& x) {
-  x.lane = threadIdx.x & 31;
-  x.w = threadIdx.x >> 5;
+  x.tid = threadIdx.x % kT;
+  x.grp = threadIdx.x / kT;
+  x.lane = x.tid & 31;
+  x.w = x.tid >> 5;
   x.col0 = 3 * (x.w / kCT) * kL + 8 * (x.w % kCT);
   x.sh4 = 8 * (x.lane & 3);
   x.sh8 = 8 * (x.lane >> 2);
   x.xe = 8 * (x.w % kCT) + (x.lane & 7);
   x.xk = x.lane >> 3;
-  x.cc = threadIdx.x;
+  x.cc = x.tid;
   x.ce = x.cc % kL;
   x.cp = x.cc / kL;
   x.te = 3 * x.w + x.lane / kP;
@@ -574,33 +592,44 @@ __device__ __forceinline__ void stage_frags(const Ctx& x, int F0, int NF) {
 template <int N>
 __device__ __forceinline__ void after_ck0(Ctx& x) {
   if constexpr (kLocalFs)
-    if (threadIdx.x == 0) stage_frags<N>(x, DG<N>::VOL_F0, DG<N>::VOL_NF < kLocalFsCap ? DG<N>::VOL_NF : kLocalFsCap);
+    if (x.tid == 0) stage_frags<N>(x, DG<N>::VOL_F0, DG<N>::VOL_NF < kLocalFsCap ? DG<N>::VOL_NF : kLocalFsCap);
 }
 
 // CK + time integral, face traces R^iT I (stored for the flux kernel) and
 // the volume term for 32-element tiles.
 template <int N>
-__global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_local(const __grid_constant__ StepParams<double> prm) {
+__global__ void __launch_bounds__(kT * kLocalGroups, kLocalGroups == 1 ? kDmCtasPerSm : 1)
+    dm_local(const __grid_constant__ StepParams<double> prm) {
   using G = DG<N>;
   using Lay = Layout<N>;
   constexpr int B = G::B;
-  extern __shared__ __align__(128) double smem[];
+  extern __shared__ __align__(128) double smem_cta[];
   Ctx x;
   init_ctx(x);
+  double* smem = smem_cta + x.grp * Lay::LOCALG;  // this group's region
+  // group grp of the CTA works as virtual CTA vb of a grid of vgrid
+  const int64_t vb = static_cast<int64_t>(blockIdx.x) * kLocalGroups + x.grp;
+  const int64_t vgrid = static_cast<int64_t>(gridDim.x) * kLocalGroups;
+  x.shcap = Lay::LSH;
   x.I = smem;
   x.S = smem + G::IROWS * kRS;
   x.xb = smem + Lay::ROWS * kRS + x.w * kXBUF * kXW;
   x.frags = frag_table<N>();
-  x.fs = smem + Lay::FOFF;
+  x.fs = kLocalGroups > 1 ? smem_cta + kLocalGroups * Lay::LOCALG : smem + Lay::FOFF;
   x.fbar = reinterpret_cast<unsigned long long*>(smem + Lay::FOFF + Lay::FSMAX * 32);
   unsigned long long* qbar = x.fbar + 1;
   unsigned qph = 0;
-  if (threadIdx.x == 0) {
+  if constexpr (kLocalGroups > 1) {  // static fragment buffer: CK step 0, then the volume
+    double* fs = const_cast<double*>(x.fs);
+    for (int i = threadIdx.x; i < Lay::LSH * 32; i += kT * kLocalGroups) fs[i] = x.frags[i];
+    __syncthreads();
+  }
+  if (x.tid == 0) {
     mbar_init(x.fbar, 1);
     mbar_init(qbar, 1);
-    if (kLocalFs && blockIdx.x < prm.ntiles) stage_frags<N>(x, G::CK0_F0, G::CK0_NF < kLocalFsCap ? G::CK0_NF : kLocalFsCap);
+    if (kLocalFs && vb < prm.ntiles) stage_frags<N>(x, G::CK0_F0, G::CK0_NF < kLocalFsCap ? G::CK0_NF : kLocalFsCap);
   }
-  __syncthreads();
+  x.sync();
   x.dt = prm.dt;
   x.scal = prm.scal;
   x.N = N;
@@ -620,12 +649,12 @@ __global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_local(const __grid_consta
     x.q1 = static_cast<int>((w >> 5) & 31);
     x.q2 = static_cast<int>((w >> 10) & 31);
   }
-  for (int64_t it = blockIdx.x; it < prm.ntiles; it += gridDim.x) {
+  for (int64_t it = vb; it < prm.ntiles; it += vgrid) {
     const int64_t tile = prm.tile0 + it;
     double* Qt = prm.Q + tile * B * kRS;
     YDG_PHASE(0);
-    if (threadIdx.x == 0 && it + gridDim.x < prm.ntiles) {  // next tile of this CTA -> L2
-      const int64_t nt = tile + gridDim.x;
+    if (x.tid == 0 && it + vgrid < prm.ntiles) {  // next tile of this CTA -> L2
+      const int64_t nt = tile + vgrid;
       prefetch_l2(prm.Q + nt * B * kRS, B * kRS * sizeof(double));
       prefetch_l2(prm.star + nt * 3 * kP * 3 * kL, 3 * kP * 3 * kL * sizeof(double));
     }
@@ -633,7 +662,7 @@ __global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_local(const __grid_consta
     {  // stage Q^n of the tile in shared memory (rows of I, continuing into S): 16-byte
        // cp.async chunks, all in flight at once
       constexpr int kChunks = B * kRS / 2;
-      for (int c = threadIdx.x; c < kChunks; c += blockDim.x) {
+      for (int c = x.tid; c < kChunks; c += kT) {
         const int row = c / (kRS / 2), cc = 2 * (c % (kRS / 2));
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(x.I + swz(row, cc))),
                      "l"(Qt + row * kRS + cc)
@@ -648,7 +677,7 @@ __global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_local(const __grid_consta
       for (int j = 0; j < 3; ++j) x.a[3 * c + j] = ld_stream(st + ((c * kP + xp) * 3 + j) * kL);
     cp_async_wait_all();
     if constexpr (kLocalFs) mbar_wait(x.fbar, 0);  // CK step 0 fragments (first of two loads per tile)
-    __syncthreads();
+    x.sync();
     YDG_PHASE(1);
     G::ck(x);  // ends with a barrier: the time integral is complete
     // traces T_F = R^FT I of the four faces -> staging -> one TMA bulk store per face;
@@ -658,19 +687,19 @@ __global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_local(const __grid_consta
     if constexpr (G::TR01_DFMA) {
       G::trace01(x, stg0, stg1);  // faces 0 and 1: sparse DFMA
       fence_proxy_async();
-      __syncthreads();
-      if (threadIdx.x == 0) {
+      x.sync();
+      if (x.tid == 0) {
         bulk_s2g(gtr, stg0, Lay::FACE * sizeof(double));
         bulk_s2g(gtr + Lay::FACE, stg1, Lay::FACE * sizeof(double));
       }
     }
     if constexpr (G::TR23_DFMA) {
-      if (threadIdx.x == 0) bulk_wait_read<0>();  // faces 0, 1 have left the staging blocks
-      __syncthreads();
+      if (x.tid == 0) bulk_wait_read<0>();  // faces 0, 1 have left the staging blocks
+      x.sync();
       G::trace23(x, stg0, stg1);  // faces 2 and 3: sparse DFMA
       fence_proxy_async();
-      __syncthreads();
-      if (threadIdx.x == 0) {
+      x.sync();
+      if (x.tid == 0) {
         bulk_s2g(gtr + 2 * Lay::FACE, stg0, Lay::FACE * sizeof(double));
         bulk_s2g(gtr + 3 * Lay::FACE, stg1, Lay::FACE * sizeof(double));
       }
@@ -679,21 +708,21 @@ __global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_local(const __grid_consta
     for (int F = F0; F < 4; ++F) {  // tensor-core faces
       double* stg = (F & 1) ? stg1 : stg0;
       if (F >= 2) {
-        if (threadIdx.x == 0) bulk_wait_read<1>();  // the store of face F-2 has left stg
-        __syncthreads();
+        if (x.tid == 0) bulk_wait_read<1>();  // the store of face F-2 has left stg
+        x.sync();
       }
       if (F == 0) G::template trace<0>(x, stg);
       else if (F == 1) G::template trace<1>(x, stg);
       else if (F == 2) G::template trace<2>(x, stg);
       else G::template trace<3>(x, stg);
       fence_proxy_async();
-      __syncthreads();
-      if (threadIdx.x == 0) bulk_s2g(gtr + F * Lay::FACE, stg, Lay::FACE * sizeof(double));
+      x.sync();
+      if (x.tid == 0) bulk_s2g(gtr + F * Lay::FACE, stg, Lay::FACE * sizeof(double));
     }
     YDG_PHASE(8);
-    if (threadIdx.x == 0) bulk_wait_read<0>();
-    __syncthreads();  // the staging blocks overlap the X buffers of the volume term
-    if (threadIdx.x == 0) {  // rows < IROWS of Q^n -> S (free now) for the volume's update
+    if (x.tid == 0) bulk_wait_read<0>();
+    x.sync();  // the staging blocks overlap the X buffers of the volume term
+    if (x.tid == 0) {  // rows < IROWS of Q^n -> S (free now) for the volume's update
       mbar_expect_tx(qbar, G::IROWS * kRS * sizeof(double));
       bulk_g2s(x.S, Qt, G::IROWS * kRS * sizeof(double), qbar);
     }
@@ -708,12 +737,12 @@ __global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_local(const __grid_consta
       qph ^= 1;
       G::add_volume(x, Qt, acc, x.S);
     }
-    __syncthreads();  // before the next tile overwrites the shared regions
-    if (kLocalFs && threadIdx.x == 0 && it + gridDim.x < prm.ntiles)
+    x.sync();  // before the next tile overwrites the shared regions
+    if (kLocalFs && x.tid == 0 && it + vgrid < prm.ntiles)
       stage_frags<N>(x, G::CK0_F0, G::CK0_NF < kLocalFsCap ? G::CK0_NF : kLocalFsCap);
     YDG_PHASE(11);
 #ifdef YDG_PHASES
-    if (threadIdx.x == 0 && blockIdx.x == 0 && it >= 2 * gridDim.x && it < 6 * gridDim.x) {
+    if (x.tid == 0 && vb == 0 && it >= 2 * vgrid && it < 6 * vgrid) {
       printf("PH tile %lld: stage %lld ck %lld %lld %lld %lld %lld %lld traces %lld wait %lld vol %lld addq %lld total %lld\n",
              (long long)it, ph_t[1] - ph_t[0], ph_t[2] - ph_t[1], ph_t[3] - ph_t[2], ph_t[4] - ph_t[3],
              ph_t[5] - ph_t[4], ph_t[6] - ph_t[5], ph_t[7] - ph_t[6], ph_t[8] - ph_t[7], ph_t[9] - ph_t[8],
@@ -721,7 +750,7 @@ __global__ void __launch_bounds__(kT, kDmCtasPerSm) dm_local(const __grid_consta
     }
 #endif
   }
-  if (threadIdx.x == 0) bulk_wait_all();
+  if (x.tid == 0) bulk_wait_all();
 }
 
 // Flux kernel: local and neighbour flux with one lift per face:

@@ -96,7 +96,7 @@ const void* pick_neigh(int N, int eb) {
   return nullptr;
 }
 // fp64 tensor-core kernels: kDmWarps warps (dmma_impl.cuh kW); fp32 sparse kernels: 9 warps
-int block_threads(int elem_bytes) { return elem_bytes == 8 ? kDmWarps * 32 : kP * kLanes; }
+int block_threads(int elem_bytes) { return elem_bytes == 8 ? kDmWarps * 32 * kLocalGroups : kP * kLanes; }
 // fp64 flux kernel: 3 warps per CTA (8-element halves of the 16-element tiles)
 int flux_threads(int elem_bytes) { return elem_bytes == 8 ? 3 * 32 * kFluxGroups : kP * kLanes; }
 int nB(int N) { return (N + 1) * (N + 2) * (N + 3) / 6; }
@@ -151,7 +151,9 @@ cudaError_t launch_local(int N, const StepParams<T>& p, int grid, cudaStream_t s
   const void* f = pick_local(N, sizeof(T));
   if (!f) return cudaErrorInvalidValue;
   void* args[] = {const_cast<StepParams<T>*>(&p)};
-  return cudaLaunchKernel(f, dim3(grid), dim3(block_threads(sizeof(T))), args, local_smem_bytes(N, sizeof(T)), s);
+  // fp64: grid counts 6-warp groups (virtual CTAs); kLocalGroups of them share one CTA
+  const int ctas = sizeof(T) == 8 ? (grid + kLocalGroups - 1) / kLocalGroups : grid;
+  return cudaLaunchKernel(f, dim3(ctas), dim3(block_threads(sizeof(T))), args, local_smem_bytes(N, sizeof(T)), s);
 }
 template <typename T>
 cudaError_t launch_neigh(int N, const StepParams<T>& p, int grid, cudaStream_t s) {

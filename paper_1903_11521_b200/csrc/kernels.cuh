@@ -17,6 +17,12 @@ constexpr int kDmCtasPerSm = 12 / kDmWarps;
 // fp64 flux kernel: 3-warp groups (8-element halves) per CTA.  1: one group per CTA, four
 // CTAs per SM; 4: one CTA per SM whose four groups share the lift's A fragments staged in
 // shared memory (named barriers per group).
+// fp64 local kernel: 1: kDmCtasPerSm CTAs per SM; 2: one CTA per SM of two 6-warp groups
+// sharing CK step 0's and (part of) the volume's A fragments in shared memory
+#ifndef YDG_LOCAL_GROUPS
+#define YDG_LOCAL_GROUPS 2
+#endif
+constexpr int kLocalGroups = YDG_LOCAL_GROUPS;
 #ifndef YDG_FLUX_GROUPS
 #define YDG_FLUX_GROUPS 4
 #endif

@@ -233,11 +233,11 @@ def emit_ck_dfma(b, d, K, bi, bo, IROWS):
             b(f"        y[{k}] = fma({lit(v)}, x{c}, y[{k}]);")
         b("      }")
     b("    }")
-    b("    __syncthreads();  // every read of D^d done")
+    b("    x.sync();  // every read of D^d done")
     b(f"    if (x.cc < kRS) col_wb<{1 if d == 0 else 0}, {bo}>(x, x.cc, y, {d});")
     if d == 0 and IROWS > bo:
         b(f"    scale_irows<{bo}, {IROWS}>(x);  // rows of I fed by D^0 only: dt * Q")
-    b("    __syncthreads();")
+    b("    x.sync();")
     b("  }")
     return -n  # negative: nonzero FMAs (not tiles)
 
@@ -277,7 +277,7 @@ def emit_ck_tail(b, d0, N, K):
         b(f"      if (x.tc >= 0) col_wb<0, {bo}>(x, x.tc, y, {d});")
         b("      __syncwarp();")
         b("    }")
-    b("    __syncthreads();  // the time integral is complete")
+    b("    x.sync();  // the time integral is complete")
     b("  }")
     return -n
 
@@ -359,12 +359,12 @@ def gen_order(N):
             regions["CK0"] = (f0, len(tab.frags))
         counts[f"ck{d}"] = emit_xprod(b, plan, f"ck{d}", tl, "SRC_Q" if d == 0 else "SRC_S",
                                       fbase=f0 if d == 0 else None)
-        b("    __syncthreads();  // every read of D^d done")
+        b("    x.sync();  // every read of D^d done")
         for mt, og in enumerate(tl["out"]):
             b(f"    ck_wb<{1 if d == 0 else 0}, B>(x, acc[{mt}], {d}, {row_word64(og)});")
         if d == 0 and IROWS > bo:
             b(f"    scale_irows<{bo}, {IROWS}>(x);  // rows of I fed by D^0 only: dt * Q")
-        b("    __syncthreads();")
+        b("    x.sync();")
         b("  }")
     b("  static __device__ __forceinline__ void ck(Ctx& x) {")
     for d in range(tail0 if tail0 is not None else N):
