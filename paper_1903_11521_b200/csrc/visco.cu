@@ -36,6 +36,18 @@ __device__ __forceinline__ void l2_prefetch(const void* p, int64_t bytes) {
   if (bytes > 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(n) : "memory");
 }
 
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+
 __device__ __forceinline__ void st2(double* p, double a, double b) {  // (odd row strides: 8-byte aligned only)
   p[0] = a;
   p[1] = b;
@@ -267,6 +279,17 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
   const bool comb = w < TE ? lane < B : (B > 32 && lane < TE * (B - 32));
 
   const int64_t ntiles = (prm.n + TE - 1) / TE;
+  // Q^n of a tile -> Z (element-major, as in HBM) by cp.async: the first tile's now, each
+  // next tile's while the current one is lifted (Z is free then)
+  auto issue_q = [&](int64_t t) {
+    const int64_t n0 = prm.e0 + t * TE;
+    const int nl = static_cast<int>(prm.e0 + prm.n - n0 < TE ? prm.e0 + prm.n - n0 : TE);
+    const double* Qt = prm.Q + n0 * P * B;  // n0 % 8 == 0: 16-byte aligned
+    const int n = nl * P * B;
+    for (int i = tid; i < n / 2; i += NTH) cp_async16(Z + 2 * i, Qt + 2 * i);
+    if ((n & 1) && tid == 0) cp_async8(Z + n - 1, Qt + n - 1);
+  };
+  if (blockIdx.x < ntiles) issue_q(blockIdx.x);
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t e0 = prm.e0 + tile * TE;
     const int64_t left = prm.e0 + prm.n - e0;
@@ -281,15 +304,15 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
       l2_prefetch(prm.src + n0 * P * 9, nl * P * 9 * 8);
       l2_prefetch(prm.aplus + n0 * 4 * P * 9, nl * 4 * P * 9 * 8);
     }
-    __syncthreads();  // previous tile done with every buffer
+    cp_async_wait_all();
+    __syncthreads();  // previous tile done with every buffer; this tile's Q^n in Z
     {
-      const double* Qt = prm.Q + e0 * P * B;
       const double* St = prm.star + e0 * 3 * P * 3;
       const double* Et = prm.src + e0 * P * 9;
 #pragma unroll 4
       for (int i = tid; i < TE * P * B; i += NTH) {
         const int ee = i / (P * B), r = i - ee * P * B, p = r / B, kk = r - p * B;
-        D[kk * SD + p * TE + ee] = ee < ne ? Qt[i] : 0.0;
+        D[kk * SD + p * TE + ee] = ee < ne ? Z[i] : 0.0;
       }
 #pragma unroll 4
       for (int i = tid; i < TE * 3 * P * 3; i += NTH) {  // [e][c][p][t] -> [e][p][c*3+t]
@@ -412,7 +435,8 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
         }
       }
     lift<N>(x, qa);
-    __syncthreads();  // every warp done reading the traces
+    __syncthreads();  // every warp done reading the traces and Z
+    if (tile + gridDim.x < ntiles) issue_q(tile + gridDim.x);
 #pragma unroll
     for (int mt = 0; mt < V::NQ; ++mt)
 #pragma unroll
@@ -452,12 +476,6 @@ constexpr size_t nsmem_bytes() {
          (3 * 4 * TE + 3 * VT<N>::Bt + 1) * sizeof(int);
 }
 
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <int N>
 __global__ void __launch_bounds__(NTH, 1) vm_neigh(const GenParams prm) {
