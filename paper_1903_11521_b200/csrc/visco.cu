@@ -290,6 +290,29 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
     if ((n & 1) && tid == 0) cp_async8(Z + n - 1, Qt + n - 1);
   };
   if (blockIdx.x < ntiles) issue_q(blockIdx.x);
+  // the tile's star rows [e][c][p][t] -> CS [e][p][c*3+t] and compact source rows -> CE,
+  // by cp.async (asynchronously for the next tile, once the current one's volume is done)
+  auto coeffs = [&](int64_t t, bool async) {
+    const int64_t n0 = prm.e0 + t * TE;
+    const int nl = static_cast<int>(prm.e0 + prm.n - n0 < TE ? prm.e0 + prm.n - n0 : TE);
+    const double* St = prm.star + n0 * 3 * P * 3;
+    const double* Et = prm.src + n0 * P * 9;
+    for (int i = tid; i < TE * 3 * P * 3; i += NTH) {
+      const int ee = i / (3 * P * 3), r = i - ee * 3 * P * 3, c = r / (P * 3), pt = r - c * P * 3;
+      double* d = CS + ee * CSE + (pt / 3) * CSS + c * 3 + pt % 3;
+      if (ee >= nl) *d = 0.0;
+      else if (async) cp_async8(d, St + i);
+      else *d = St[i];
+    }
+    for (int i = tid; i < TE * CEE; i += NTH) {
+      const int ee = i / CEE, j = i - ee * CEE;
+      const int p = j < 27 ? j / 9 : j < 36 ? 3 + (j - 27) / 3 : j < 54 ? 9 + (j - 36) : -1;
+      const int slot = j < 27 ? j % 9 : j < 36 ? (j - 27) % 3 : 0;
+      if (ee >= nl || p < 0) CE[i] = 0.0;
+      else if (async) cp_async8(CE + i, Et + (ee * P + p) * 9 + slot);
+      else CE[i] = Et[(ee * P + p) * 9 + slot];
+    }
+  };
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t e0 = prm.e0 + tile * TE;
     const int64_t left = prm.e0 + prm.n - e0;
@@ -307,24 +330,12 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
     cp_async_wait_all();
     __syncthreads();  // previous tile done with every buffer; this tile's Q^n in Z
     {
-      const double* St = prm.star + e0 * 3 * P * 3;
-      const double* Et = prm.src + e0 * P * 9;
 #pragma unroll 4
       for (int i = tid; i < TE * P * B; i += NTH) {
         const int ee = i / (P * B), r = i - ee * P * B, p = r / B, kk = r - p * B;
         D[kk * SD + p * TE + ee] = ee < ne ? Z[i] : 0.0;
       }
-#pragma unroll 4
-      for (int i = tid; i < TE * 3 * P * 3; i += NTH) {  // [e][c][p][t] -> [e][p][c*3+t]
-        const int ee = i / (3 * P * 3), r = i - ee * 3 * P * 3, c = r / (P * 3), pt = r - c * P * 3;
-        CS[ee * CSE + (pt / 3) * CSS + c * 3 + pt % 3] = ee < ne ? St[i] : 0.0;
-      }
-      for (int i = tid; i < TE * CEE; i += NTH) {  // compact source rows
-        const int ee = i / CEE, j = i - ee * CEE;
-        const int p = j < 27 ? j / 9 : j < 36 ? 3 + (j - 27) / 3 : j < 54 ? 9 + (j - 36) : -1;
-        const int slot = j < 27 ? j % 9 : j < 36 ? (j - 27) % 3 : 0;
-        CE[i] = (ee < ne && p >= 0) ? Et[(ee * P + p) * 9 + slot] : 0.0;
-      }
+      if (tile == blockIdx.x) coeffs(tile, false);  // later tiles: staged during the previous tile
     }
     __syncthreads();
     double I[P];
@@ -392,7 +403,8 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
       combine<B, true>(zr, D + cr * SD + cel, CS + cel * CSE, CE + cel * CEE, prm.wratio,
                        [&](int p, double v) { zr[(p / 9) * B * ZS + (p % 9) * TE] = v; });
     }
-    __syncthreads();  // I no longer read: the traces take the D buffer
+    __syncthreads();  // I no longer read: the traces take the D buffer; CS / CE free
+    if (tile + gridDim.x < ntiles) coeffs(tile + gridDim.x, true);
     {
       int rtr[V::NT];
       rows_of(V::tr_rows, ar, rtr);
