@@ -361,6 +361,17 @@ __device__ __forceinline__ void smem_bf(const Ctx& x, const double* Y, unsigned 
   for (int k = 0; k < kU; ++k) bf[k] = Y[swzf(row, x.col0 + k * kLF + (x.lane >> 2))];
 }
 __device__ __forceinline__ int qcolf(const Ctx& x, int k) { return x.qcol0 + k * kL + 2 * (x.lane & 3); }
+// Q rows of the flux kernel's read-modify-write (coherent loads: the first pair's update
+// is re-read by the second); YDG_FLUX_QNA=1: L1 no-allocate
+__device__ __forceinline__ double2 ld_q2(const double* p) {
+#if defined(YDG_FLUX_QNA) && YDG_FLUX_QNA
+  double2 v;
+  asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+#else
+  return *reinterpret_cast<const double2*>(p);
+#endif
+}
 __device__ __forceinline__ void load_qf(const Ctx& x, const double* Qt, unsigned long long w0, unsigned long long w1,
                                         double2 (&q)[2][kU]) {
 #pragma unroll
@@ -368,7 +379,7 @@ __device__ __forceinline__ void load_qf(const Ctx& x, const double* Qt, unsigned
     const int row = mrow(x, k2 ? w1 : w0);
 #pragma unroll
     for (int k = 0; k < kU; ++k)
-      q[k2][k] = row == 0xff ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(Qt + row * kRS + qcolf(x, k));
+      q[k2][k] = row == 0xff ? make_double2(0.0, 0.0) : ld_q2(Qt + row * kRS + qcolf(x, k));
   }
 }
 __device__ __forceinline__ void store_qf(const Ctx& x, double* Qt, unsigned long long w0, unsigned long long w1,
