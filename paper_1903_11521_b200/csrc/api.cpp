@@ -672,7 +672,9 @@ int ydg_upload_mesh(ydg_solver* h, int64_t ne, const double* xyz, const int64_t*
   int sms = 0, occ_l = 0, occ_n = 0;
   CUDA_OR_FAIL(h, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->dev));
   occ_l = eb == 8 ? kDmCtasPerSm : 1;  // fp64: 12 warps per SM in kDmCtasPerSm 6-warp groups
-  occ_n = eb == 8 ? 4 : 1;  // fp64 flux kernel: four 3-warp groups (8-element halves) per SM
+  // fp64 flux kernel: 3-warp groups (8-element halves); four single-group CTAs per SM, or
+  // one CTA of kFluxGroups groups
+  occ_n = eb == 8 ? (kFluxGroups > 1 ? kFluxGroups : 4) : 1;
   h->grid_local = sms * occ_l;
   h->grid_neigh = sms * occ_n;
   h->have_mesh = true;
