@@ -101,12 +101,17 @@ __device__ const double* fh_table();
 
 // A fragments: read-only, reused by every warp and tile -> keep in L1 (evict_last); other
 // streaming loads use evict_first so they do not push the fragment table out.
-__device__ __forceinline__ double afrag(const Ctx& x, int tid) {
+__device__ __forceinline__ double afrag_g(const Ctx& x, int tid) {
   double v;
   asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(x.frags + tid * 32 + x.lane));
   return v;
 }
 __device__ __forceinline__ double afrag_s(const Ctx& x, int i) { return x.fs[i * 32 + x.lane]; }
+// table slot tid: the grouped local kernel holds slots [0, shcap) in shared memory
+__device__ __forceinline__ double afrag(const Ctx& x, int tid) {
+  if constexpr (kLocalGroups > 1) return tid < x.shcap ? afrag_s(x, tid) : afrag_g(x, tid);
+  return afrag_g(x, tid);
+}
 // Products whose fragments may be staged in shared memory: CK step 0 and the volume term
 // (local kernel), the lift (flux kernel).  With two CTAs per SM there is no room: off.
 #ifndef YDG_LOCAL_FS
@@ -125,10 +130,10 @@ constexpr int kLocalFsCap = YDG_LOCAL_FS_CAP;
 // g: table index; r: index within the product's staged region.  The grouped kernel holds
 // table slots [0, shcap) (CK step 0, then the volume) in a static shared buffer.
 __device__ __forceinline__ double afrag_l(const Ctx& x, int g, int r) {
-  if constexpr (kLocalGroups > 1) return g < x.shcap ? afrag_s(x, g) : afrag(x, g);
-  return (kLocalFs && r < kLocalFsCap) ? afrag_s(x, r) : afrag(x, g);
+  if constexpr (kLocalGroups > 1) return afrag(x, g);
+  return (kLocalFs && r < kLocalFsCap) ? afrag_s(x, r) : afrag_g(x, g);
 }
-__device__ __forceinline__ double afrag_f(const Ctx& x, int g, int r) { return kFluxFs ? afrag_s(x, r) : afrag(x, g); }
+__device__ __forceinline__ double afrag_f(const Ctx& x, int g, int r) { return kFluxFs ? afrag_s(x, r) : afrag_g(x, g); }
 __device__ __forceinline__ double ld_stream(const double* p) {
   double v;
   asm("ld.global.nc.L1::evict_first.f64 %0, [%1];" : "=d"(v) : "l"(p));
@@ -514,9 +519,9 @@ struct Layout {
   static constexpr int LOCALG = (LOCAL + 15) & ~15;     // one group's region (grouped kernel)
   // grouped kernel: CK step 0's fragments, then the volume's, as many as fit in 227 KB
   static constexpr int LSH0 = (227 * 1024 / 8 - kLocalGroups * LOCALG) / 32;
-  // (table slots = shared slots: CK step 0's fragments first, the volume's next)
-  static constexpr bool LSH_OK = G::CK0_F0 == 0 && G::VOL_F0 == G::CK0_NF;
-  static constexpr int LSH = (kLocalGroups == 1 || !LSH_OK) ? 0 : (LSH0 < G::CK0_NF + G::VOL_NF ? LSH0 : G::CK0_NF + G::VOL_NF);
+  // (shared slots = the first table slots: CK step 0's fragments, the volume's next, then
+  // the traces'; the flux kernel's lift fragments follow all of them)
+  static constexpr int LSH = kLocalGroups == 1 ? 0 : (LSH0 < G::LIFT_F0 ? LSH0 : G::LIFT_F0);
   static constexpr int LOCALCTA = kLocalGroups == 1 ? LOCAL : kLocalGroups * LOCALG + LSH * 32;
   // flux kernel (8-element CTAs): own face block, neighbour blocks, two Y buffers,
   // coefficients, slots, j|h, mbarriers
@@ -797,6 +802,7 @@ __global__ void __launch_bounds__(kTF * kFluxGroups, kFluxGroups == 1 ? kFluxCta
   int8_t* JHX = JH + kJH;                               // [16] of the next item's (tile, face)
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(JHX + kJH);  // own, nb
   Ctx x;
+  x.shcap = 0;  // (the local kernel's shared fragment slots)
   x.lane = tid & 31;
   x.w = tid >> 5;
   x.col0 = 3 * x.w * kLF;
