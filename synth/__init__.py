@@ -42,8 +42,12 @@ _M2 = np.uint64(0x94D049BB133111EB)
 STREAM_JITTER = 1
 STREAM_MATERIAL = 2
 STREAM_DOFS = 3
+STREAM_VPERM = 4
 
 KUHN_PERMS = tuple(itertools.permutations(range(3)))
+# the 12 even permutations of an element's 4 local vertices (keep det J > 0)
+EVEN_PERMS4 = tuple(p for p in itertools.permutations(range(4))
+                    if sum(1 for i in range(4) for j in range(i + 1, 4) if p[i] > p[j]) % 2 == 0)
 
 
 def _mix64(z):
@@ -101,6 +105,7 @@ class Config:
     material: str = "uniform"  # or "two_layer"
     seed: int = 0
     jitter: float = 0.1
+    vperm: bool = False  # per-element random even vertex permutation (all 48 (i, j, h) cases)
 
     @property
     def n_elements(self):
@@ -122,7 +127,10 @@ class Config:
         """Same N / P / precision / distributions on a smaller periodic mesh."""
         return Config(name or f"{self.name}-r{nx}", self.N, self.P, self.precision, nx,
                       ny or nx, nz or nx, steps if steps is not None else self.steps,
-                      self.material, self.seed, self.jitter)
+                      self.material, self.seed, self.jitter, self.vperm)
+
+    def with_(self, **kw):
+        return Config(**{**self.__dict__, **kw})
 
 
 # BASELINE.json configs[0..4]
@@ -135,8 +143,14 @@ CONFIGS = {
 }
 
 
-def kuhn_mesh(nx, ny, nz, seed=0, jitter=0.1):
-    """(elem_xyz (E,4,3) float64, elem_vid (E,4) int64) of the periodic jittered Kuhn mesh."""
+def kuhn_mesh(nx, ny, nz, seed=0, jitter=0.1, vperm=False):
+    """(elem_xyz (E,4,3) float64, elem_vid (E,4) int64) of the periodic jittered Kuhn mesh.
+
+    vperm: reorder each element's 4 vertices by a seeded random even permutation (det J
+    keeps its sign).  The Kuhn order alone produces only 6 of the 48 (face i, neighbour
+    face j, orientation h) cases of the neighbour relation; with vperm every case
+    occurs on meshes of a few hundred elements, as on the paper's reproducer with random
+    neighbour relations."""
     nv = nx * ny * nz
     jit = uniform_range(seed, STREAM_JITTER, 0, 3 * nv, -jitter, jitter).reshape(nv, 3)
     # cube corners in element order
@@ -162,7 +176,19 @@ def kuhn_mesh(nx, ny, nz, seed=0, jitter=0.1):
     w = pos % np.array([nx, ny, nz])
     vid = w[..., 0] + nx * (w[..., 1] + ny * w[..., 2])
     xyz = pos.astype(np.float64) + jit[vid]
-    return xyz, vid.astype(np.int64)
+    vid = vid.astype(np.int64)
+    if vperm:
+        E = xyz.shape[0]
+        u = uniform(seed, STREAM_VPERM, np.arange(E, dtype=np.uint64), 0.0, 12.0)
+        perm = np.asarray(EVEN_PERMS4, dtype=np.int64)[np.minimum(u.astype(np.int64), 11)]
+        xyz = np.take_along_axis(xyz, perm[:, :, None], axis=1)
+        vid = np.take_along_axis(vid, perm, axis=1)
+    return xyz, vid
+
+
+def mesh(cfg: "Config"):
+    """kuhn_mesh of a config (its seed, jitter and vertex-permutation flag)."""
+    return kuhn_mesh(cfg.nx, cfg.ny, cfg.nz, seed=cfg.seed, jitter=cfg.jitter, vperm=cfg.vperm)
 
 
 def material(cfg: Config, first=0, count=None):

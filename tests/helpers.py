@@ -6,7 +6,7 @@ from oracle import step as ostep
 
 
 def make_inputs(cfg):
-    xyz, vid = synth.kuhn_mesh(cfg.nx, cfg.ny, cfg.nz, seed=cfg.seed, jitter=cfg.jitter)
+    xyz, vid = synth.mesh(cfg)
     mat = synth.material(cfg)
     Q = synth.dofs(cfg)
     an = None
@@ -53,3 +53,31 @@ def rel_err(got, ref):
         if r.size and np.abs(r).max() > 0:
             out[g] = d[:, s].max() / np.abs(r).max()
     return out
+
+
+# BASELINE north_star tolerances; reading R21: the bound is applied to EVERY quantity group
+# (stress, velocity, memory variables) separately, since after one step the stresses
+# (~1e6-1e7) dwarf the O(1) velocities and a global max|dQ|/max|Q| would not see them.
+TOL = {8: 1e-12, 4: 2e-5}
+# fp64 per-group bound: the groups are normalised by their own max|Q|; velocities carry
+# the cancellation of stress divergences ~1e7 / rho, so 1e-11 (c0 has asserted it since
+# round 1)
+GROUP_TOL = {8: 1e-11, 4: 2e-5}
+
+
+def check_parity(err, precision, label=""):
+    """Assert max|dQ|/max|Q| overall and per quantity group; print all of them."""
+    print(f"parity {label}: " + " ".join(f"{k}={v:.3e}" for k, v in err.items()))
+    assert err["all"] <= TOL[precision], (label, err)
+    for g in ("stress", "velocity", "memory"):
+        if g in err:
+            assert err[g] <= GROUP_TOL[precision], (label, g, err)
+
+
+def face_cases(elem_vid):
+    """Set of (face i, neighbour face j, orientation h) occurring in the mesh (oracle tables)."""
+    import numpy as np
+    from oracle import mesh as omesh
+    nb, j, h = omesh.neighbour_table(elem_vid)
+    i = np.broadcast_to(np.arange(4), j.shape)
+    return set(zip(i.ravel().tolist(), j.ravel().tolist(), h.ravel().tolist()))

@@ -12,11 +12,9 @@ import pytest
 
 import synth
 from oracle import step as ostep
-from tests.helpers import rel_err
+from tests.helpers import check_parity, rel_err
 
 pytestmark = pytest.mark.gpu
-
-TOL = {8: 1e-12, 4: 2e-5}
 
 
 def _samples(cfg, blocks=4, width=48, seed=7):
@@ -65,8 +63,7 @@ def test_fullsize_sampled_one_step(name):
     got = gpu_rows(sel)
     ref = _oracle_one_step(cfg, xyz, vid, mat, an, sel, Q0[sel].astype(np.float64),
                            lambda ids: Q0[ids].astype(np.float64))
-    err = rel_err(got, ref)
-    assert err["all"] <= TOL[cfg.precision], err
+    check_parity(rel_err(got, ref), cfg.precision, f"{name} n=0")
     if name == "c1":  # last step of the benchmarked run: n = steps-1 -> steps
         ydg.ydg_step(h, cfg.dt, cfg.steps - 2)
         nb = ostep.setup(cfg.N, xyz, vid, mat, elements=sel).nb
@@ -76,6 +73,5 @@ def test_fullsize_sampled_one_step(name):
         got = gpu_rows(sel)
         ref = _oracle_one_step(cfg, xyz, vid, mat, an, sel, np.stack([Qn[e] for e in sel]),
                                lambda ids: np.stack([Qn[e] for e in ids]))
-        err = rel_err(got, ref)
-        assert err["all"] <= TOL[cfg.precision], err
+        check_parity(rel_err(got, ref), cfg.precision, f"{name} last step")
     ydg.ydg_destroy(h)

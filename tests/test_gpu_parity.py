@@ -8,11 +8,9 @@ import pytest
 
 import synth
 from oracle import mesh as omesh
-from tests.helpers import LAST_PATH, make_inputs, rel_err, run_gpu, run_oracle
+from tests.helpers import LAST_PATH, TOL, check_parity, face_cases, make_inputs, rel_err, run_gpu, run_oracle
 
 pytestmark = pytest.mark.gpu
-
-TOL = {8: 1e-12, 4: 2e-5}
 
 
 def _cfg(name, **kw):
@@ -20,11 +18,13 @@ def _cfg(name, **kw):
     return base.__class__(**{**base.__dict__, **kw})
 
 
-def _parity(cfg, nsteps=None, dt=None):
+def _parity(cfg, nsteps=None, dt=None, check=True):
     xyz, vid, mat, Q, an = make_inputs(cfg)
     got, nbt = run_gpu(cfg, xyz, vid, mat, Q, an, nsteps=nsteps, dt=dt)
     ref = run_oracle(cfg, xyz, vid, mat, Q, an, nsteps=nsteps, dt=dt)
     err = rel_err(got, ref)
+    if check:
+        check_parity(err, cfg.precision, cfg.name)
     return err, nbt, vid
 
 
@@ -32,8 +32,6 @@ def test_c0_parity_and_tables():
     """BASELINE configs[0]: full mesh, 1 step, fp64."""
     cfg = synth.CONFIGS["c0"]
     err, (nb, j, h), vid = _parity(cfg)
-    assert err["all"] <= TOL[8], err
-    assert err["velocity"] <= 1e-11, err  # the small group is checked too (reading R21)
     onb, oj, oh = omesh.neighbour_table(vid)
     assert np.array_equal(nb, onb) and np.array_equal(j, oj) and np.array_equal(h, oh)
 
@@ -43,28 +41,79 @@ def test_orders_fp64_ragged(N):
     """3x3x3 cubes = 162 elements: 5 full tiles of 32 and a ragged tail of 2."""
     cfg = _cfg("c0", N=N, nx=3, ny=3, nz=3)
     err, *_ = _parity(cfg, nsteps=2)
-    assert err["all"] <= TOL[8], err
 
 
 def test_c1_replica_fp64():
-    """configs[1] at 8x8x8 cubes (3072 elements), N=5, fp64, 3 steps (several CTA waves)."""
-    cfg = synth.CONFIGS["c1"].replica(8, steps=3)
+    """configs[1] at 8x8x8 cubes (3072 elements), N=5, fp64, its 10 steps (SURVEY §8(c)
+    parity protocol 2)."""
+    cfg = synth.CONFIGS["c1"].replica(8)
     err, *_ = _parity(cfg)
-    assert err["all"] <= TOL[8], err
 
 
 def test_c2_replica_fp32():
-    """configs[2] at 6x6x4 cubes, N=6, fp32, two-layer material, 2 steps."""
-    cfg = synth.CONFIGS["c2"].replica(6, 6, 4, steps=2)
+    """configs[2] at 8x8x8 cubes, N=6, fp32, two-layer material, 6 of its 10 steps: the
+    config's dt (0.2 h / vp_max, reading R13) is 2-6x the ADER-DG CFL bound, so max|Q| grows
+    ~700x per step (oracle: 3.9e9 after 1 step, 2.7e23 after 6, 8.8e34 after 10) and the
+    fp32 intermediates of steps 9-10 reach FLT_MAX; 6 steps is the longest run whose fp32
+    values are all far from overflow."""
+    cfg = synth.CONFIGS["c2"].replica(8, steps=6)
     err, *_ = _parity(cfg)
-    assert err["all"] <= TOL[4], err
+
+
+# ---- unstructured neighbour relations: every (face i, neighbour face j, orientation h)
+# case of Neigh/Face/Rot (P:1342).  The Kuhn order alone yields 6 of the 48 cases; a
+# per-element random even vertex permutation (synth vperm) yields all of them, as the
+# paper's reproducer's random neighbour relations (P:1697-1700) do.
+
+def _perm_parity(cfg, nsteps=None, dt=None):
+    err, (nb, j, h), vid = _parity(cfg, nsteps=nsteps, dt=dt)
+    assert len(face_cases(vid)) == 48
+    onb, oj, oh = omesh.neighbour_table(vid)
+    assert np.array_equal(nb, onb) and np.array_equal(j, oj) and np.array_equal(h, oh)
+    return err
+
+
+def test_vperm_c0_fp64():
+    _perm_parity(synth.CONFIGS["c0"].with_(vperm=True, name="c0-vperm"))
+
+
+@pytest.mark.parametrize("N", [1, 3, 4])
+def test_vperm_orders_fp64(N):
+    _perm_parity(synth.CONFIGS["c0"].with_(N=N, nx=3, ny=3, nz=3, vperm=True, name=f"N{N}-vperm"), nsteps=2)
+
+
+def test_vperm_c1_replica_fp64():
+    _perm_parity(synth.CONFIGS["c1"].replica(6, steps=3).with_(vperm=True, name="c1-vperm"))
+
+
+def test_vperm_c2_replica_fp32():
+    _perm_parity(synth.CONFIGS["c2"].replica(6, 6, 4, steps=2).with_(vperm=True, name="c2-vperm"))
+
+
+def test_vperm_c3_viscoelastic():
+    _perm_parity(synth.CONFIGS["c3"].replica(4, 4, 3, steps=2).with_(vperm=True, name="c3-vperm"))
+    assert LAST_PATH["path"] == 2
+
+
+def test_vperm_generic(monkeypatch):
+    monkeypatch.setenv("YDG_GENERIC", "1")
+    _perm_parity(synth.CONFIGS["c0"].with_(vperm=True, name="generic-vperm"), nsteps=2)
+
+
+def test_vperm_order6_fp64_generic():
+    _perm_parity(synth.CONFIGS["c1"].with_(N=6, nx=3, ny=3, nz=3, steps=1, vperm=True, name="N6-vperm"))
+
+
+def test_vperm_visco_generic(monkeypatch):
+    monkeypatch.setenv("YDG_VISCO_GENERIC", "1")
+    _perm_parity(synth.CONFIGS["c3"].replica(3, steps=1).with_(vperm=True, name="c3csr-vperm"))
+    assert LAST_PATH["path"] == 3
 
 
 def test_fp32_at_stable_dt():
     """fp32 at a stable time step (reading R13) so growth cannot hide precision loss."""
     cfg = _cfg("c0", precision=4, N=4, nx=3, ny=3, nz=3)
     err, *_ = _parity(cfg, nsteps=5, dt=0.02 / 6000.0)
-    assert err["all"] <= TOL[4], err
 
 
 def test_constant_state_is_steady_on_gpu():
@@ -120,8 +169,6 @@ def test_c3_viscoelastic_replica():
     cfg = synth.CONFIGS["c3"].replica(3, steps=2)
     err, *_ = _parity(cfg)
     assert LAST_PATH["path"] == 2  # the viscoelastic tensor-core kernels ran
-    assert err["all"] <= TOL[8], err
-    assert err["memory"] <= 1e-11, err
 
 
 @pytest.mark.parametrize("N", [1, 2, 3])
@@ -131,8 +178,6 @@ def test_viscoelastic_orders(N):
     cfg = _cfg("c3", N=N, nx=3, ny=3, nz=2, steps=2)
     err, *_ = _parity(cfg)
     assert LAST_PATH["path"] == 2
-    assert err["all"] <= TOL[8], err
-    assert err["memory"] <= 1e-11, err
 
 
 def test_viscoelastic_csr_kernel(monkeypatch):
@@ -141,17 +186,14 @@ def test_viscoelastic_csr_kernel(monkeypatch):
     cfg = synth.CONFIGS["c3"].replica(3, steps=1)
     err, *_ = _parity(cfg)
     assert LAST_PATH["path"] == 3
-    assert err["all"] <= TOL[8], err
 
 
 def test_generic_path_elastic(monkeypatch):
     """The generic (CSR) kernels on the elastic c0 problem agree with the oracle too."""
     monkeypatch.setenv("YDG_GENERIC", "1")
     err, *_ = _parity(synth.CONFIGS["c0"], nsteps=2)
-    assert err["all"] <= TOL[8], err
 
 
 def test_order6_fp64_generic():
     cfg = _cfg("c1", N=6, nx=3, ny=3, nz=3, steps=1)
     err, *_ = _parity(cfg)
-    assert err["all"] <= TOL[8], err
