@@ -9,9 +9,12 @@ north_star), i.e. one ``ydg_step(dt, 1)`` call = two kernel launches.  Metric: e
 updates/s (plus nonzero GFLOP/s and the roofline fraction of the dominant kernel).
 
 Workload (BASELINE.json configs[1], "c1"): elastic, N = 5, fp64, 64^3 Kuhn-split cubes =
-1,572,864 tetrahedra, synthetic seeded inputs (synth/).  With --gpus N > 1 (torchrun, one
-process per GPU) the mesh is extended to 64 x 64 x 64N cubes and rank r owns the z-slab of
-c1's size (weak scaling; the halo of face traces goes over NCCL inside ydg_step).
+1,572,864 tetrahedra, synthetic seeded inputs (synth/).  With --gpus N > 1 (one process per
+GPU; launched under torchrun by the driver, or re-executed under torchrun by this script
+when WORLD_SIZE is unset) the mesh is extended to 64 x 64 x 64N cubes and rank r owns the
+z-slab of c1's size (weak scaling; the halo of shared-face traces goes over NCCL inside
+ydg_step).  --config c4 (BASELINE configs[4]) is strong scaling: the fixed 128^3-cube mesh
+(12,582,912 tetrahedra) split into N z-slabs of 128/N cube layers.
 
 Timing: W untimed warm-up steps, then K steps bracketed by barrier + synchronize, CUDA
 events on the launching stream, max over ranks.  The inputs (6.3 GB of DOFs per GPU) are
@@ -73,16 +76,35 @@ def parse():
     ap.add_argument("--e2e-reps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=8, help="cubes per axis of the oracle sample")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="time ydg_step_graph (one CUDA graph per step); auto: on below 100k elements "
+                         "(c0: launch-latency bound), 1 GPU only")
     return ap.parse_args()
+
+
+STRONG = ("c4",)  # configs with a fixed global mesh (strong scaling over z-slabs)
 
 
 def workload(args, world):
     cfg = synth.CONFIGS[args.config]
     if args.replica:
         cfg = cfg.replica(args.replica)
-    if world > 1:
+    if world > 1 and args.config not in STRONG:
         cfg = cfg.__class__(**{**cfg.__dict__, "nz": cfg.nz * world, "name": f"{cfg.name}-zslab-x{world}"})
     return cfg
+
+
+def relaunch_under_torchrun(args):
+    """--gpus N > 1 without a torchrun environment: run this script as N ranks (one per GPU)
+    under torch.distributed.run on 127.0.0.1 and pass its exit code through."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 class Clocks:
@@ -169,8 +191,19 @@ def allmax(x, world):
 # ------------------------------------------------------------------ oracle (CPU)
 
 
-def oracle_rate(cfg, cubes, steps, warmup=0):
-    """Element-updates/s of the CPU oracle on a periodic cubes^3 sample of cfg (setup untimed)."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def oracle_rate(cfg, cubes, steps, warmup=0, threads=None):
+    """Element-updates/s of the CPU oracle on a periodic cubes^3 sample of cfg (setup untimed),
+    BLAS/OpenMP pools limited to `threads` (None: every host core)."""
     from oracle import step as ostep
     import threadpoolctl
     sample = cfg.replica(cubes, cubes, cubes)
@@ -181,15 +214,36 @@ def oracle_rate(cfg, cubes, steps, warmup=0):
         omega, Y = synth.anelastic(sample, mat)
     prob = ostep.setup(cfg.N, xyz, vid, mat, P=cfg.P, omega=omega, Y=Y)
     Q = ostep.to_internal(synth.dofs(sample))
-    for _ in range(warmup):
-        Q = ostep.step(prob, Q, cfg.dt, 1)
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        Q = ostep.step(prob, Q, cfg.dt, 1)
-        times.append(time.perf_counter() - t0)
-    threads = max([p.get("num_threads", 1) for p in threadpoolctl.threadpool_info()] + [1])
-    return sample.n_elements / statistics.mean(times), threads, sample, times
+    nthreads = threads or os.cpu_count() or 1
+    with threadpoolctl.threadpool_limits(nthreads):
+        for _ in range(warmup):
+            Q = ostep.step(prob, Q, cfg.dt, 1)
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            Q = ostep.step(prob, Q, cfg.dt, 1)
+            times.append(time.perf_counter() - t0)
+        used = max([p.get("num_threads", 1) for p in threadpoolctl.threadpool_info()] + [1])
+    return sample.n_elements / statistics.mean(times), used, sample, times
+
+
+def cpu_baseline(cfg, cubes, steps=5):
+    """The oracle on all host cores (cubes^3 sample) and on one core (a 4^3 sample): min and
+    median of `steps` timed steps after one warm-up step each."""
+    _, used, sample, times = oracle_rate(cfg, cubes, steps, 1)
+    _, _, sample1, times1 = oracle_rate(cfg, 4, steps, 1, threads=1)
+    rate = sample.n_elements / statistics.median(times)
+    return {
+        "value": rate, "unit": UNIT, "cores": used, "kind": "oracle",
+        "sample": (f"oracle (numpy fp64) on {cfg.name} parameters (N={cfg.N}, P={cfg.P}) over a periodic "
+                   f"{sample.nx}^3-cube sample ({sample.n_elements} elements); value = median of {steps} "
+                   f"steps after 1 warm-up, setup untimed"),
+        "all_cores": {"median": rate, "best": sample.n_elements / min(times), "threads": used,
+                      "elements": sample.n_elements, "steps": steps},
+        "single_core": {"median": sample1.n_elements / statistics.median(times1),
+                        "best": sample1.n_elements / min(times1), "elements": sample1.n_elements, "steps": steps},
+        "host_cores": os.cpu_count(), "cpu_model": cpu_model(),
+    }
 
 
 def run_reference(args):
@@ -200,14 +254,16 @@ def run_reference(args):
     cfg = workload(args, world)
     rate, threads, sample, times = oracle_rate(cfg, args.cpu_sample, args.steps, args.warmup)
     desc = (f"oracle (numpy fp64) on {cfg.name} parameters (N={cfg.N}, P={cfg.P}) over a periodic "
-            f"{sample.nx}^3-cube sample ({sample.n_elements} elements), one step per timed step")
+            f"{sample.nx}^3-cube sample ({sample.n_elements} elements), one step per timed step, "
+            f"{threads} threads on {os.cpu_count()} host cores ({cpu_model()})")
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg.name, "order": cfg.N, "quantities": cfg.P, "sample_elements": sample.n_elements},
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc,
+                         "best": sample.n_elements / min(times), "median": sample.n_elements / statistics.median(times)},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -269,27 +325,50 @@ def run_ydg(args):
     sptr = stream.cuda_stream
     assert sptr != 0
 
+    qbytes = nloc * cfg.P * cfg.B * (8 if cfg.precision == 8 else 4)
+    # inputs smaller than L2 (126 MB): a 512 MB buffer is rewritten between timed steps
+    flush = torch.zeros(64 << 20, dtype=torch.float64, device="cuda") if 4 * qbytes < 126e6 else None
+    use_graph = world == 1 and (args.graph == "on" or (args.graph == "auto" and cfg.n_elements < 100000))
+    step_fn = ydg.ydg_step_graph if use_graph else ydg.ydg_step
+
     # warm-up
     for _ in range(args.warmup):
-        ydg.ydg_step(h, cfg.dt, 1, stream=sptr)
+        step_fn(h, cfg.dt, 1, stream=sptr)
     torch.cuda.synchronize()
     barrier(world)
 
-    # timed region
-    ydg.ydg_profile(h, True)
+    # timed region (per-kernel events inside it, except on the graph path: there the same
+    # steps are replayed once more with the events, after the timed region)
+    if not use_graph:
+        ydg.ydg_profile(h, True)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         torch.cuda.synchronize()
         barrier(world)
-        e0.record(stream)
-        for _ in range(args.steps):
-            ydg.ydg_step(h, cfg.dt, 1, stream=sptr)
-        e1.record(stream)
+        if flush is None:
+            e0.record(stream)
+            for _ in range(args.steps):
+                step_fn(h, cfg.dt, 1, stream=sptr)
+            e1.record(stream)
+        else:  # L2-resident workload: flush L2 between steps, time each step on its own
+            evs = []
+            for _ in range(args.steps):
+                flush.add_(1)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                step_fn(h, cfg.dt, 1, stream=sptr)
+                b.record(stream)
+                evs.append((a, b))
         torch.cuda.synchronize()
         barrier(world)
-    ms = e0.elapsed_time(e1)
+    ms = e0.elapsed_time(e1) if flush is None else sum(a.elapsed_time(b) for a, b in evs)
     clocks = clk.summary()
+    if use_graph:
+        ydg.ydg_profile(h, True)
+        for _ in range(args.steps):
+            ydg.ydg_step(h, cfg.dt, 1, stream=sptr)
+        torch.cuda.synchronize()
     t_local = ydg.ydg_query(h, ydg.YDG_Q_PROF_LOCAL_MS)
     t_neigh = ydg.ydg_query(h, ydg.YDG_Q_PROF_NEIGH_MS)
     launches = int(ydg.ydg_query(h, ydg.YDG_Q_PROF_LAUNCHES))
@@ -313,11 +392,10 @@ def run_ydg(args):
         barrier(world)
         t0 = time.perf_counter()
         ydg.ydg_upload_dofs(h, first, Qh)
-        ydg.ydg_step(h, cfg.dt, cfg.steps)
+        step_fn(h, cfg.dt, cfg.steps)
         ydg.ydg_download_dofs(h, first, nloc, out=Qh)
         e2e_ms.append(1e3 * (time.perf_counter() - t0))
     e2e_best = allmax(min(e2e_ms), world)
-    qbytes = nloc * cfg.P * cfg.B * (8 if cfg.precision == 8 else 4)
 
     if rank != 0:
         ydg.ydg_destroy(h)
@@ -361,20 +439,20 @@ def run_ydg(args):
     step_roof = peak * 1e12 / nz  # element-updates/s if the whole step ran at the FP64 peak
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        rate, threads, sample, times = oracle_rate(cfg, args.cpu_sample, 2, 0)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": f"oracle (numpy fp64) on {cfg.name} parameters over a periodic {sample.nx}^3-cube "
-                         f"sample ({sample.n_elements} elements), mean of 2 steps, setup untimed"}
+        cpu = cpu_baseline(cfg, args.cpu_sample)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if cfg.precision == 8 else "f32",
+        "scaling": "strong" if args.config in STRONG else "weak", "vs_baseline": None,
+        "dtype": "f64" if cfg.precision == 8 else "f32",
         "data": "synthetic",
         "config": {"workload": cfg.name, "model": "ADER-DG elastic tetrahedra" if cfg.P == 9 else "ADER-DG viscoelastic",
                    "order": cfg.N, "quantities": cfg.P, "elements": ne_total, "elements_per_gpu": nloc,
                    "mesh": f"{cfg.nx}x{cfg.ny}x{cfg.nz} Kuhn cubes, periodic", "dt": cfg.dt,
                    "parallelism": f"zslab{world}" if world > 1 else "single",
-                   "l2": "inputs larger than L2 (DOFs %.1f GB/GPU), no flush" % (qbytes / 1e9)},
+                   "device_bytes_per_gpu": int(ydg.ydg_query(h, ydg.YDG_Q_DEVICE_BYTES)),
+                   "l2": ("inputs larger than L2 (DOFs %.1f GB/GPU), no flush" % (qbytes / 1e9)) if flush is None
+                         else "L2 flushed (512 MB rewrite) before every timed step; steps timed one by one"},
         "nz_gflops": value * nz / 1e9, "nz_flops_per_element": nz,
         "dof_updates_per_s": value * cfg.B * cfg.P,
         "step_roofline_frac": value / world / step_roof,
@@ -383,8 +461,9 @@ def run_ydg(args):
         "e2e": {"value": ne_total * cfg.steps / (e2e_best / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": qbytes * world / cfg.steps, "d2h_bytes_per_step": qbytes * world / cfg.steps,
                 "steps_per_call": cfg.steps,
-                "call": "ydg_upload_dofs(pinned host) + ydg_step(dt, %d) + ydg_download_dofs(pinned host)" % cfg.steps},
-        "gpu_launches": args.steps * per_step_launch,
+                "call": "ydg_upload_dofs(pinned host) + %s(dt, %d) + ydg_download_dofs(pinned host)"
+                        % ("ydg_step_graph" if use_graph else "ydg_step", cfg.steps)},
+        "gpu_launches": args.steps * per_step_launch, "cuda_graph": use_graph,
         "clocks": clocks, "finite": finite, "setup_s": round(setup_s, 1),
     }
     print(json.dumps(line), flush=True)
@@ -394,6 +473,12 @@ def run_ydg(args):
 
 def main():
     args = parse()
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1:
+        return relaunch_under_torchrun(args)
+    if world_env is not None and int(world_env) != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world_env}"}), flush=True)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     return run_ydg(args)

@@ -117,6 +117,13 @@ int ydg_download_dofs_device(ydg_solver* h, int64_t first, int64_t count, void* 
  * Collective over the ranks of ydg_set_comm: all must call with the same dt, nsteps. */
 int ydg_step(ydg_solver* h, double dt, int nsteps, void* cuda_stream);
 
+/* Same as ydg_step, launched as one CUDA graph: the 2 * nsteps kernel launches of (dt,
+ * nsteps) are captured on first use (and again whenever dt or nsteps change or a mesh is
+ * uploaded) and replayed with one cudaGraphLaunch on cuda_stream -- for small meshes whose
+ * steps are launch-latency bound (BASELINE configs[0]: 384 elements).  One rank only
+ * (YDG_ERR_UNSUPPORTED otherwise); profiling must be off (YDG_ERR_STATE). */
+int ydg_step_graph(ydg_solver* h, double dt, int nsteps, void* cuda_stream);
+
 /* Block until all work of the handle has finished. */
 int ydg_synchronize(ydg_solver* h);
 
@@ -137,15 +144,23 @@ int ydg_get_neighbours(ydg_solver* h, int64_t first, int64_t count, int64_t* nb,
 int ydg_profile(ydg_solver* h, int enable);
 
 /* Host-only helper (no device needed): the z-slab halo plan ydg_set_comm + ydg_upload_mesh
- * would build for `rank` of `nranks` on the mesh given by elem_vid [ne][4].
- *  counts[3] <- (number of peers, number of ghost elements, number of sent elements).
+ * would build for `rank` of `nranks` on the mesh given by elem_vid [ne][4].  The halo
+ * moves one face block (the time-integrated trace of one side of a face, Bt x P values)
+ * per face whose two elements live on different ranks (the neighbour flux reads
+ * the neighbour's trace on the shared face only).
+ *  counts[3] <- (number of peers np, number of ghost elements ng, number of face blocks nb
+ *              sent = received).
  *  If the array arguments are non-NULL they must hold counts[] entries and receive:
- *  peers[np] (ascending), recv_cnt[np], send_cnt[np], ghost_of[ng] (global ids of the
- *  ghost slots, grouped by peer, ascending within a peer) and send_elem[ns] (global ids
- *  sent, grouped by peer, ascending) -- a peer's send list equals our ghost list from it. */
+ *  peers[np] (ascending), recv_cnt[np], send_cnt[np] (face blocks per peer, equal),
+ *  ghost_of[ng] (global ids of the ghost slots, grouped by peer, ascending within a peer),
+ *  send_elem[nb] / send_face[nb] (global id and local face of every block sent, grouped by
+ *  peer, ordered by (id, face)) and recv_elem[nb] / recv_face[nb] (the sending element's
+ *  global id and local face of every block received, same order) -- a peer's send list
+ *  equals our receive list from it. */
 int ydg_halo_plan(int64_t n_elements, const int64_t* elem_vid, int rank, int nranks,
                   int64_t* counts, int32_t* peers, int64_t* recv_cnt, int64_t* send_cnt,
-                  int64_t* ghost_of, int64_t* send_elem);
+                  int64_t* ghost_of, int64_t* send_elem, int8_t* send_face, int64_t* recv_elem,
+                  int8_t* recv_face);
 
 /* Query a scalar (see YDG_Q_*). */
 int ydg_query(ydg_solver* h, int what, double* value);

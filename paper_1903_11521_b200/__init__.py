@@ -30,7 +30,7 @@ YDG_OK, YDG_ERR_ARG, YDG_ERR_STATE, YDG_ERR_CUDA, YDG_ERR_NCCL, YDG_ERR_MESH, YD
  YDG_Q_PROF_LAUNCHES, YDG_Q_KERNEL_PATH) = range(17)
 
 EXPORTS = ("ydg_create", "ydg_last_error", "ydg_set_comm", "ydg_upload_mesh", "ydg_upload_dofs",
-           "ydg_upload_dofs_device", "ydg_download_dofs_device", "ydg_step", "ydg_synchronize",
+           "ydg_upload_dofs_device", "ydg_download_dofs_device", "ydg_step", "ydg_step_graph", "ydg_synchronize",
            "ydg_download_dofs", "ydg_get_neighbours", "ydg_halo_plan", "ydg_profile", "ydg_query",
            "ydg_error_string", "ydg_destroy")
 
@@ -60,11 +60,12 @@ def lib():
         L.ydg_upload_dofs_device.argtypes = [vp, i64, i64, vp, vp]
         L.ydg_download_dofs_device.argtypes = [vp, i64, i64, vp, vp]
         L.ydg_step.argtypes = [vp, dbl, i32, vp]
+        L.ydg_step_graph.argtypes = [vp, dbl, i32, vp]
         L.ydg_synchronize.argtypes = [vp]
         L.ydg_download_dofs.argtypes = [vp, i64, i64, vp]
         L.ydg_get_neighbours.argtypes = [vp, i64, i64, vp, vp, vp]
         L.ydg_profile.argtypes = [vp, i32]
-        L.ydg_halo_plan.argtypes = [i64, vp, i32, i32, vp, vp, vp, vp, vp, vp]
+        L.ydg_halo_plan.argtypes = [i64, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.ydg_query.argtypes = [vp, i32, ctypes.POINTER(dbl)]
         L.ydg_error_string.argtypes = [vp]
         L.ydg_error_string.restype = ctypes.c_char_p
@@ -113,8 +114,14 @@ def ydg_upload_mesh(h, elem_xyz, elem_vid, material, anelastic=None):
     xyz, pxyz = _c(elem_xyz, np.float64)
     vid, pvid = _c(elem_vid, np.int64)
     mat, pmat = _c(material, np.float64)
+    ne = xyz.shape[0] if xyz.ndim else 0
+    if xyz.shape != (ne, 4, 3) or vid.shape != (ne, 4) or mat.shape != (ne, 3):
+        raise ValueError(f"mesh shapes: xyz {xyz.shape} (want (ne,4,3)), vid {vid.shape} (ne,4), "
+                         f"material {mat.shape} (ne,3)")
     if anelastic is not None:
         an, pan = _c(anelastic, np.float64)
+        if an.size != 3 + 6 * ne:
+            raise ValueError(f"anelastic: {an.size} values, want 3 + 6 ne = {3 + 6 * ne}")
     else:
         an, pan = None, None
     _check(h, lib().ydg_upload_mesh(h.ptr, xyz.shape[0], pxyz, pvid, pmat, pan))
@@ -122,6 +129,8 @@ def ydg_upload_mesh(h, elem_xyz, elem_vid, material, anelastic=None):
 
 def ydg_upload_dofs(h, first, Q):
     q, pq = _c(Q, h.dtype)
+    if q.ndim != 3 or q.shape[1:] != (h.P, h.B):
+        raise ValueError(f"Q shape {q.shape}, want (count, P={h.P}, B={h.B})")
     _check(h, lib().ydg_upload_dofs(h.ptr, first, q.shape[0], pq))
 
 
@@ -135,6 +144,10 @@ def ydg_download_dofs_device(h, first, count, ptr, stream=None):
 
 def ydg_step(h, dt, nsteps=1, stream=None):
     _check(h, lib().ydg_step(h.ptr, float(dt), int(nsteps), ctypes.c_void_p(stream)))
+
+
+def ydg_step_graph(h, dt, nsteps=1, stream=None):
+    _check(h, lib().ydg_step_graph(h.ptr, float(dt), int(nsteps), ctypes.c_void_p(stream)))
 
 
 def ydg_synchronize(h):
@@ -164,7 +177,7 @@ def ydg_halo_plan(elem_vid, rank, nranks):
     counts = np.zeros(3, dtype=np.int64)
     P = ctypes.c_void_p
     rc = lib().ydg_halo_plan(vid.shape[0], pvid, rank, nranks, counts.ctypes.data_as(P), None, None, None,
-                             None, None)
+                             None, None, None, None, None)
     if rc != YDG_OK:
         raise YdgError(rc, lib().ydg_last_error().decode())
     npeer, ng, ns = (int(x) for x in counts)
@@ -173,12 +186,17 @@ def ydg_halo_plan(elem_vid, rank, nranks):
     scnt = np.zeros(npeer, dtype=np.int64)
     ghost = np.zeros(ng, dtype=np.int64)
     send = np.zeros(ns, dtype=np.int64)
+    sface = np.zeros(ns, dtype=np.int8)
+    recv = np.zeros(ns, dtype=np.int64)
+    rface = np.zeros(ns, dtype=np.int8)
     rc = lib().ydg_halo_plan(vid.shape[0], pvid, rank, nranks, counts.ctypes.data_as(P), peers.ctypes.data_as(P),
                              rcnt.ctypes.data_as(P), scnt.ctypes.data_as(P), ghost.ctypes.data_as(P),
-                             send.ctypes.data_as(P))
+                             send.ctypes.data_as(P), sface.ctypes.data_as(P), recv.ctypes.data_as(P),
+                             rface.ctypes.data_as(P))
     if rc != YDG_OK:
         raise YdgError(rc, lib().ydg_last_error().decode())
-    return {"peers": peers, "recv_cnt": rcnt, "send_cnt": scnt, "ghost_of": ghost, "send_elem": send}
+    return {"peers": peers, "recv_cnt": rcnt, "send_cnt": scnt, "ghost_of": ghost, "send_elem": send,
+            "send_face": sface, "recv_elem": recv, "recv_face": rface}
 
 
 def ydg_profile(h, enable=True):

@@ -65,6 +65,11 @@ struct ydg_solver {
   std::vector<Ev> pending;
   double prof_ms[2] = {0, 0};
   int64_t prof_launches = 0;
+  // ydg_step_graph: the launch sequence of (dt, nsteps) captured once into a CUDA graph
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  double g_dt = 0;
+  int g_n = -1;
 };
 
 namespace {
@@ -101,6 +106,9 @@ void free_mesh(ydg_solver* h) {
   }
   h->device_bytes = 0;
   h->have_mesh = false;
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);  // captured the old buffers
+  h->gexec = nullptr;
+  h->g_n = -1;
 }
 
 int dalloc(ydg_solver* h, void** p, size_t bytes) {
@@ -511,6 +519,10 @@ int ydg_create(int order, int quantities, int precision, int cuda_device, ydg_so
     g_last_error = "the generic (viscoelastic) path is fp64 only";
     return YDG_ERR_UNSUPPORTED;
   }
+  if (generic && gen_local_te((order + 1) * (order + 2) * (order + 3) / 6, (order + 1) * (order + 2) / 2, quantities) == 0) {
+    g_last_error = "the generic kernel's work arrays exceed the shared memory of a CTA";
+    return YDG_ERR_UNSUPPORTED;
+  }
   std::unique_ptr<ydg_solver> h(new ydg_solver);
   h->N = order;
   h->P = quantities;
@@ -761,6 +773,40 @@ int ydg_step(ydg_solver* h, double dt, int nsteps, void* cuda_stream) {
   return h->prec == 8 ? do_step<double>(h, dt, nsteps, s) : do_step<float>(h, dt, nsteps, s);
 }
 
+int ydg_step_graph(ydg_solver* h, double dt, int nsteps, void* cuda_stream) {
+  int rc = check(h);
+  if (rc) return rc;
+  if (!h->have_mesh) return fail(h, YDG_ERR_STATE, "upload the mesh first");
+  if (!(dt > 0) || !std::isfinite(dt) || nsteps < 0) return fail(h, YDG_ERR_ARG, "bad dt or nsteps");
+  if (h->nranks > 1) return fail(h, YDG_ERR_UNSUPPORTED, "ydg_step_graph runs on one rank (the halo has host barriers)");
+  if (h->profiling) return fail(h, YDG_ERR_STATE, "disable ydg_profile before ydg_step_graph");
+  if (nsteps == 0) return YDG_OK;
+  cudaStream_t s = pick_stream(h, cuda_stream);
+  if (!h->gexec || h->g_dt != dt || h->g_n != nsteps) {
+    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+    if (!h->cap_stream) CUDA_OR_FAIL(h, cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    CUDA_OR_FAIL(h, cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeRelaxed));
+    rc = h->generic ? generic_step(h, dt, nsteps, h->cap_stream)
+                    : (h->prec == 8 ? do_step<double>(h, dt, nsteps, h->cap_stream)
+                                    : do_step<float>(h, dt, nsteps, h->cap_stream));
+    cudaGraph_t g = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(h->cap_stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    CUDA_OR_FAIL(h, ec);
+    const cudaError_t ei = cudaGraphInstantiate(&h->gexec, g, 0);
+    cudaGraphDestroy(g);
+    CUDA_OR_FAIL(h, ei);
+    h->g_dt = dt;
+    h->g_n = nsteps;
+  }
+  CUDA_OR_FAIL(h, cudaGraphLaunch(h->gexec, s));
+  return YDG_OK;
+}
+
 int ydg_synchronize(ydg_solver* h) {
   int rc = check(h);
   if (rc) return rc;
@@ -783,7 +829,7 @@ int ydg_get_neighbours(ydg_solver* h, int64_t first, int64_t count, int64_t* nb,
 
 int ydg_halo_plan(int64_t ne, const int64_t* vid, int rank, int nranks, int64_t* counts,
                   int32_t* peers, int64_t* recv_cnt, int64_t* send_cnt, int64_t* ghost_of,
-                  int64_t* send_elem) {
+                  int64_t* send_elem, int8_t* send_face, int64_t* recv_elem, int8_t* recv_face) {
   if (ne <= 0 || !vid || !counts || nranks < 1 || rank < 0 || rank >= nranks) return YDG_ERR_ARG;
   Neighbours nbr;
   std::string err;
@@ -807,8 +853,14 @@ int ydg_halo_plan(int64_t ne, const int64_t* vid, int rank, int nranks, int64_t*
       send_cnt[k] = plan.send_cnt[k];
     }
   if (ghost_of) std::copy(plan.ghost_of.begin(), plan.ghost_of.end(), ghost_of);
-  if (send_elem)
-    for (size_t k = 0; k < plan.send_slots.size(); ++k) send_elem[k] = first + plan.send_slots[k];
+  for (size_t k = 0; k < plan.send_slots.size(); ++k) {
+    if (send_elem) send_elem[k] = first + plan.send_slots[k];
+    if (send_face) send_face[k] = plan.send_face[k];
+  }
+  for (size_t k = 0; k < plan.recv_ghost.size(); ++k) {
+    if (recv_elem) recv_elem[k] = plan.ghost_of[plan.recv_ghost[k]];
+    if (recv_face) recv_face[k] = plan.recv_face[k];
+  }
   return YDG_OK;
 }
 
@@ -869,6 +921,7 @@ void ydg_destroy(ydg_solver* h) {
   free_mesh(h);
   for (void* p : h->csr) cudaFree(p);
   h->halo.destroy();
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }

@@ -26,7 +26,8 @@ struct GenParams {
                         // wratio[l] x those of mechanism 0 (checked at upload; visco.cu)
 };
 
-size_t gen_local_smem(int B, int Bt, int P);
+size_t gen_local_smem(int B, int Bt, int P, int te);
+int gen_local_te(int B, int Bt, int P);
 size_t gen_neigh_smem(int Bt, int P);
 cudaError_t gen_configure(int B, int Bt, int P, const int (*ecols)[9], const int (*scols)[3]);
 cudaError_t gen_launch(const GenParams& p, bool local, cudaStream_t s);

@@ -65,29 +65,32 @@ __device__ __forceinline__ int64_t tiled_index(int64_t s, int v, int Bt, int P, 
   return (((s >> 5) * 4 + F) * Bt + m) * (int64_t)(P * 32) + q * 32 + (s & 31);
 }
 
+// One face block (Bt x P values) per entry; sf = slot << 2 | face.
 template <typename W>
-__global__ void pack_kernel(const W* __restrict__ traces, const int64_t* __restrict__ slots,
+__global__ void pack_kernel(const W* __restrict__ traces, const int64_t* __restrict__ sf,
                             W* __restrict__ out, int64_t n, int Bt, int P, int TS, int L) {
-  const int vals = 4 * Bt * P;
+  const int vals = Bt * P;
   const int64_t total = n * vals;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = i / vals;
-    const int v = static_cast<int>(i - s * vals);
-    out[i] = traces[tiled_index(slots[s], v, Bt, P, TS, L)];
+    const int64_t k = i / vals;
+    const int v = static_cast<int>(i - k * vals);
+    const int64_t w = sf[k];
+    out[i] = traces[tiled_index(w >> 2, static_cast<int>(w & 3) * vals + v, Bt, P, TS, L)];
   }
 }
 
 template <typename W>
-__global__ void unpack_kernel(const W* __restrict__ in, W* __restrict__ traces, int64_t first_slot,
+__global__ void unpack_kernel(const W* __restrict__ in, W* __restrict__ traces, const int64_t* __restrict__ sf,
                               int64_t n, int Bt, int P, int TS, int L) {
-  const int vals = 4 * Bt * P;
+  const int vals = Bt * P;
   const int64_t total = n * vals;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t g = i / vals;
-    const int v = static_cast<int>(i - g * vals);
-    traces[tiled_index(first_slot + g, v, Bt, P, TS, L)] = in[i];
+    const int64_t k = i / vals;
+    const int v = static_cast<int>(i - k * vals);
+    const int64_t w = sf[k];
+    traces[tiled_index(w >> 2, static_cast<int>(w & 3) * vals + v, Bt, P, TS, L)] = in[i];
   }
 }
 
@@ -104,54 +107,49 @@ int64_t owner(int64_t g, int64_t ne, int nranks) {
 bool plan_halo(const Neighbours& nbr, int64_t ne, int rank, int nranks, HaloPlan* out,
                std::string* err) {
   const int64_t first = ne * rank / nranks, last = ne * (rank + 1) / nranks;
+  struct Blk { int64_t peer, gid; int face; int64_t ref; };  // ref: local slot / ghost gid
+  std::vector<Blk> sends, recvs;
   std::vector<std::pair<int64_t, int64_t>> ghosts;  // (owner, gid)
-  std::vector<std::pair<int64_t, int64_t>> sends;   // (peer, local slot)
-  for (int64_t e = first; e < last; ++e) {
-    std::vector<int64_t> peers_of_e;
+  for (int64_t e = first; e < last; ++e)
     for (int i = 0; i < 4; ++i) {
       const int64_t n = nbr.nb[e * 4 + i];
       if (n < 0 || n >= ne) { *err = "bad neighbour id"; return false; }
       if (n >= first && n < last) continue;
       const int64_t o = owner(n, ne, nranks);
       ghosts.emplace_back(o, n);
-      peers_of_e.push_back(o);
+      sends.push_back({o, e, i, e - first});                   // my side of the face
+      recvs.push_back({o, n, static_cast<int>(nbr.j[e * 4 + i]), n});  // the peer's side
     }
-    std::sort(peers_of_e.begin(), peers_of_e.end());
-    peers_of_e.erase(std::unique(peers_of_e.begin(), peers_of_e.end()), peers_of_e.end());
-    for (int64_t o : peers_of_e) sends.emplace_back(o, e - first);
-  }
+  auto key = [](const Blk& x, const Blk& y) {
+    return x.peer != y.peer ? x.peer < y.peer : (x.gid != y.gid ? x.gid < y.gid : x.face < y.face);
+  };
   std::sort(ghosts.begin(), ghosts.end());
   ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
-  std::sort(sends.begin(), sends.end());
-  out->ghost_of.clear();
-  out->peers.clear();
-  out->recv_off.clear();
-  out->recv_cnt.clear();
-  out->send_slots.clear();
-  out->send_off.clear();
-  out->send_cnt.clear();
+  std::sort(sends.begin(), sends.end(), key);
+  std::sort(recvs.begin(), recvs.end(), key);
+  *out = HaloPlan();
   for (size_t g = 0; g < ghosts.size(); ++g) {
-    if (out->peers.empty() || out->peers.back() != ghosts[g].first) {
-      out->peers.push_back(static_cast<int>(ghosts[g].first));
-      out->recv_off.push_back(static_cast<int64_t>(g));
-      out->recv_cnt.push_back(0);
-    }
-    out->recv_cnt.back()++;
+    if (out->peers.empty() || out->peers.back() != ghosts[g].first) out->peers.push_back(static_cast<int>(ghosts[g].first));
     out->ghost_of.push_back(ghosts[g].second);
   }
   for (int peer : out->peers) {
     out->send_off.push_back(static_cast<int64_t>(out->send_slots.size()));
-    int64_t c = 0;
-    for (auto& s : sends)
-      if (s.first == peer) { out->send_slots.push_back(s.second); ++c; }
-    out->send_cnt.push_back(c);
+    out->recv_off.push_back(static_cast<int64_t>(out->recv_ghost.size()));
+    int64_t cs = 0, cr = 0;
+    for (const Blk& b : sends)
+      if (b.peer == peer) { out->send_slots.push_back(b.ref); out->send_face.push_back(static_cast<int8_t>(b.face)); ++cs; }
+    for (const Blk& b : recvs)
+      if (b.peer == peer) {
+        const auto it = std::lower_bound(ghosts.begin(), ghosts.end(), std::make_pair(b.peer, b.gid));
+        out->recv_ghost.push_back(static_cast<int64_t>(it - ghosts.begin()));
+        out->recv_face.push_back(static_cast<int8_t>(b.face));
+        ++cr;
+      }
+    // a face has one side per rank: the blocks a peer sends are the faces it shares with us
+    if (cs != cr) { *err = "asymmetric halo"; return false; }
+    out->send_cnt.push_back(cs);
+    out->recv_cnt.push_back(cr);
   }
-  // every peer we send to must also be a peer we receive from (face adjacency symmetric)
-  for (auto& s : sends)
-    if (std::find(out->peers.begin(), out->peers.end(), static_cast<int>(s.first)) == out->peers.end()) {
-      *err = "asymmetric halo";
-      return false;
-    }
   return true;
 }
 
@@ -237,15 +235,19 @@ int Halo::bind(void* traces, int Bt, int P, int TS, int L, int elem_bytes, int64
   TS_ = TS;
   L_ = L;
   P_ = P;
-  vals_ = 4 * Bt * P;
+  vals_ = Bt * P;  // one face block per message entry
   eb_ = elem_bytes;
   owned_slots_ = owned_slots;
-  const size_t ns = plan_.send_slots.size(), ng = plan_.ghost_of.size();
+  const size_t ns = plan_.send_slots.size(), nr = plan_.recv_ghost.size();
+  std::vector<int64_t> sf(ns), rf(nr);
+  for (size_t k = 0; k < ns; ++k) sf[k] = plan_.send_slots[k] << 2 | plan_.send_face[k];
+  for (size_t k = 0; k < nr; ++k) rf[k] = (owned_slots + plan_.recv_ghost[k]) << 2 | plan_.recv_face[k];
   cudaError_t e = cudaMalloc(&d_send_slots_, std::max<size_t>(1, ns) * sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMalloc(&d_recv_slots_, std::max<size_t>(1, nr) * sizeof(int64_t));
   if (e == cudaSuccess) e = cudaMalloc(&d_send_buf_, std::max<size_t>(1, ns) * vals_ * eb_);
-  if (e == cudaSuccess) e = cudaMalloc(&d_recv_buf_, std::max<size_t>(1, ng) * vals_ * eb_);
-  if (e == cudaSuccess && ns)
-    e = cudaMemcpy(d_send_slots_, plan_.send_slots.data(), ns * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&d_recv_buf_, std::max<size_t>(1, nr) * vals_ * eb_);
+  if (e == cudaSuccess && ns) e = cudaMemcpy(d_send_slots_, sf.data(), ns * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && nr) e = cudaMemcpy(d_recv_slots_, rf.data(), nr * sizeof(int64_t), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
   return 0;
 }
@@ -254,7 +256,7 @@ int Halo::exchange(cudaStream_t s, void* traces, int elem_bytes, std::string* er
   cudaError_t e = cudaEventRecord(ready_, s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(cstream_, ready_, 0);
   const int64_t ns = static_cast<int64_t>(plan_.send_slots.size());
-  const int64_t ng = static_cast<int64_t>(plan_.ghost_of.size());
+  const int64_t ng = static_cast<int64_t>(plan_.recv_ghost.size());
   if (e == cudaSuccess && ns) {
     if (elem_bytes == 8)
       pack_kernel<unsigned long long><<<148 * 4, 256, 0, cstream_>>>(
@@ -302,10 +304,10 @@ int Halo::exchange(cudaStream_t s, void* traces, int elem_bytes, std::string* er
     if (elem_bytes == 8)
       unpack_kernel<unsigned long long><<<148 * 4, 256, 0, cstream_>>>(
           static_cast<const unsigned long long*>(d_recv_buf_), static_cast<unsigned long long*>(traces),
-          owned_slots_, ng, Bt_, P_, TS_, L_);
+          d_recv_slots_, ng, Bt_, P_, TS_, L_);
     else
       unpack_kernel<unsigned int><<<148 * 4, 256, 0, cstream_>>>(
-          static_cast<const unsigned int*>(d_recv_buf_), static_cast<unsigned int*>(traces), owned_slots_,
+          static_cast<const unsigned int*>(d_recv_buf_), static_cast<unsigned int*>(traces), d_recv_slots_,
           ng, Bt_, P_, TS_, L_);
     e = cudaGetLastError();
     if (e != cudaSuccess) { *err = cudaGetErrorString(e); return 3; }
@@ -323,6 +325,8 @@ int Halo::wait(cudaStream_t s, std::string* err) {
 
 void Halo::destroy() {
   if (d_send_slots_) cudaFree(d_send_slots_);
+  if (d_recv_slots_) cudaFree(d_recv_slots_);
+  d_recv_slots_ = nullptr;
   if (d_send_buf_) cudaFree(d_send_buf_);
   if (d_recv_buf_) cudaFree(d_recv_buf_);
   d_send_slots_ = nullptr;

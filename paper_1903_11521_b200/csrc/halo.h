@@ -16,13 +16,21 @@
 
 namespace ydg {
 
+// Messages carry one face block (Bt x P values of the time-integrated trace) per shared
+// face: for every face whose two elements live on different ranks, the owner of each side
+// sends its own side's trace; the receiver stores it in the ghost slot of the sending
+// element at that element's local face.  Both sides order a peer's blocks by (global id of
+// the sending element, its local face), so no index travels with the data.
 struct HaloPlan {
   // ghosts: global ids in slot order (sorted by owner rank, then global id)
   std::vector<int64_t> ghost_of;
   std::vector<int> peers;             // peer ranks (ascending)
-  std::vector<int64_t> recv_off;      // first ghost index per peer
-  std::vector<int64_t> recv_cnt;      // ghosts per peer
-  std::vector<int64_t> send_slots;    // local slots to pack, grouped by peer
+  std::vector<int64_t> recv_off;      // first received face block per peer
+  std::vector<int64_t> recv_cnt;      // face blocks per peer
+  std::vector<int64_t> recv_ghost;    // per received block: ghost index (slot - owned slots)
+  std::vector<int8_t> recv_face;      //   and the ghost element's local face
+  std::vector<int64_t> send_slots;    // per sent block: local slot, grouped by peer
+  std::vector<int8_t> send_face;      //   and the local face
   std::vector<int64_t> send_off, send_cnt;
 };
 
@@ -55,7 +63,8 @@ class Halo {
   cudaStream_t cstream_ = nullptr;
   cudaEvent_t ready_ = nullptr, done_ = nullptr;
   HaloPlan plan_;
-  int64_t* d_send_slots_ = nullptr;
+  int64_t* d_send_slots_ = nullptr;  // packed (slot << 2 | face) per sent block
+  int64_t* d_recv_slots_ = nullptr;  // packed (ghost slot << 2 | face) per received block
   void* d_send_buf_ = nullptr;
   void* d_recv_buf_ = nullptr;
   int vals_ = 0, eb_ = 0, Bt_ = 0, P_ = 0, TS_ = 0, L_ = 32;

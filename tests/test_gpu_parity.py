@@ -197,3 +197,55 @@ def test_generic_path_elastic(monkeypatch):
 def test_order6_fp64_generic():
     cfg = _cfg("c1", N=6, nx=3, ny=3, nz=3, steps=1)
     err, *_ = _parity(cfg)
+
+
+def test_viscoelastic_order5_generic():
+    """P = 27 at N = 5 runs the CSR kernels with 2-element CTAs (4 do not fit in 227 KB)."""
+    cfg = _cfg("c3", N=5, nx=3, ny=3, nz=2, steps=1, vperm=True, name="c3-N5")
+    _parity(cfg)
+    assert LAST_PATH["path"] == 3
+
+
+def test_generic_handles_of_both_quantity_counts_coexist(monkeypatch):
+    """A P = 9 and a P = 27 generic handle alive in one process, steps interleaved: each keeps
+    its own star / source column patterns."""
+    import paper_1903_11521_b200 as ydg
+    monkeypatch.setenv("YDG_GENERIC", "1")
+    monkeypatch.setenv("YDG_VISCO_GENERIC", "1")
+    c9 = _cfg("c0", nx=3, ny=3, nz=3, name="coexist-9")
+    c27 = _cfg("c3", N=2, nx=3, ny=3, nz=3, steps=1, name="coexist-27")
+    ins = {c.name: make_inputs(c) for c in (c9, c27)}
+    hs = {}
+    for c in (c9, c27):  # P = 9 first: the later P = 27 configuration must not clobber it
+        xyz, vid, mat, Q, an = ins[c.name]
+        h = ydg.ydg_create(c.N, c.P, c.precision)
+        ydg.ydg_upload_mesh(h, xyz, vid, mat, an)
+        ydg.ydg_upload_dofs(h, 0, Q)
+        hs[c.name] = h
+    for c in (c9, c27, c9):
+        ydg.ydg_step(hs[c.name], c.dt, 1)
+    for c, n in ((c9, 2), (c27, 1)):
+        got = ydg.ydg_download_dofs(hs[c.name], 0, c.n_elements)
+        ref = run_oracle(c, *ins[c.name], nsteps=n)
+        check_parity(rel_err(got, ref), 8, c.name)
+        ydg.ydg_destroy(hs[c.name])
+
+
+def test_step_graph_matches_step():
+    """ydg_step_graph (the nsteps launch sequence as one CUDA graph) is bitwise ydg_step, and
+    is re-captured when dt changes."""
+    import paper_1903_11521_b200 as ydg
+    cfg = synth.CONFIGS["c0"]
+    xyz, vid, mat, Q, _ = make_inputs(cfg)
+    outs = []
+    for graph in (False, True):
+        h = ydg.ydg_create(cfg.N, 9, 8)
+        ydg.ydg_upload_mesh(h, xyz, vid, mat)
+        ydg.ydg_upload_dofs(h, 0, Q)
+        f = ydg.ydg_step_graph if graph else ydg.ydg_step
+        f(h, cfg.dt, 3)
+        f(h, cfg.dt, 3)
+        f(h, 0.5 * cfg.dt, 3)
+        outs.append(ydg.ydg_download_dofs(h, 0, cfg.n_elements))
+        ydg.ydg_destroy(h)
+    assert np.array_equal(outs[0], outs[1])

@@ -1,11 +1,13 @@
 """Multi-rank host logic of the z-slab decomposition, world size 2 (and 3) over gloo on CPU.
 
 Each rank builds its halo plan with the library's host-only ``ydg_halo_plan`` (the same
-code ``ydg_set_comm`` + ``ydg_upload_mesh`` run), fills the send buffer with per-element
-"traces" (a function of the global element id), exchanges them with gloo send/recv exactly
-as the NCCL group in ``Halo::exchange`` does (one message per peer), and checks that every
-ghost slot received the right element's data and that every off-rank neighbour of an owned
-element is a ghost.  No GPU kernels are involved (those ranks cannot be emulated on one GPU).
+code ``ydg_set_comm`` + ``ydg_upload_mesh`` run), fills the send buffer with per-face-block
+"traces" (a function of the sending element's global id and local face), exchanges them
+with gloo send/recv exactly as the NCCL group in ``Halo::exchange`` does (one message per
+peer), and checks that every received block is the one the plan says (element, face), that
+these are exactly the shared faces every owned element's neighbour flux reads (nb, j of
+P:1342 from the oracle's brute-force table) and that every off-rank neighbour is a ghost.
+No GPU kernels are involved (those ranks cannot be emulated on one GPU).
 """
 import os
 import socket
@@ -20,8 +22,8 @@ import synth
 VALS = 5  # values per element "trace" in this test
 
 
-def _fake_trace(gids):
-    g = np.asarray(gids, dtype=np.float64)[:, None]
+def _fake_trace(gids, faces):
+    g = np.asarray(gids, dtype=np.float64)[:, None] * 4 + np.asarray(faces, dtype=np.float64)[:, None]
     return g * 10.0 + np.arange(VALS)[None, :]
 
 
@@ -32,13 +34,13 @@ def _worker(rank, world, port, nx, nz, out):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        xyz, vid = synth.kuhn_mesh(nx, nx, nz)
+        xyz, vid = synth.kuhn_mesh(nx, nx, nz, vperm=True)
         ne = vid.shape[0]
         plan = ydg.ydg_halo_plan(vid, rank, world)
         first, last = ne * rank // world, ne * (rank + 1) // world
         assert (plan["send_elem"] >= first).all() and (plan["send_elem"] < last).all()
-        send = torch.from_numpy(_fake_trace(plan["send_elem"]))
-        recv = torch.zeros((len(plan["ghost_of"]), VALS), dtype=torch.float64)
+        send = torch.from_numpy(_fake_trace(plan["send_elem"], plan["send_face"]))
+        recv = torch.zeros((len(plan["recv_elem"]), VALS), dtype=torch.float64)
         reqs = []
         so = ro = 0
         for k, peer in enumerate(plan["peers"]):
@@ -54,13 +56,20 @@ def _worker(rank, world, port, nx, nz, out):
                 recv[r[2]:r[2] + r[1].shape[0]] = r[1]
             else:
                 r.wait()
-        ok_data = bool(np.array_equal(recv.numpy(), _fake_trace(plan["ghost_of"])))
-        # completeness: every off-rank neighbour of an owned element is a ghost
+        ok_data = bool(np.array_equal(recv.numpy(), _fake_trace(plan["recv_elem"], plan["recv_face"])))
+        # completeness: the received blocks are exactly the (Neigh, Face) pairs of the owned
+        # elements' off-rank faces, each once; every off-rank neighbour is a ghost
         from oracle import mesh as omesh
-        nb = omesh.match_faces(vid)
-        off = {int(n) for e in range(first, last) for n in nb[e] if not (first <= n < last)}
-        ok_cover = off == set(int(g) for g in plan["ghost_of"])
-        out[rank] = (ok_data, ok_cover, len(plan["ghost_of"]))
+        nb, j, _ = omesh.neighbour_table(vid)
+        need = sorted((int(nb[e, i]), int(j[e, i])) for e in range(first, last) for i in range(4)
+                      if not (first <= nb[e, i] < last))
+        got = sorted(zip(plan["recv_elem"].tolist(), plan["recv_face"].tolist()))
+        off = {n for n, _ in need}
+        ok_cover = need == got and off == set(int(g) for g in plan["ghost_of"])
+        # blocks sent: our side of every off-rank face, once
+        mine = sorted((e, i) for e in range(first, last) for i in range(4) if not (first <= nb[e, i] < last))
+        ok_send = mine == sorted(zip(plan["send_elem"].tolist(), plan["send_face"].tolist()))
+        out[rank] = (ok_data, ok_cover and ok_send, len(plan["ghost_of"]))
     finally:
         dist.destroy_process_group()
 
