@@ -201,7 +201,7 @@ def test_order6_fp64_generic():
 
 def test_viscoelastic_order5_generic():
     """P = 27 at N = 5 runs the CSR kernels with 2-element CTAs (4 do not fit in 227 KB)."""
-    cfg = _cfg("c3", N=5, nx=3, ny=3, nz=2, steps=1, vperm=True, name="c3-N5")
+    cfg = synth.CONFIGS["c3"].with_(N=5, nx=3, ny=3, nz=2, steps=1, vperm=True, name="c3-N5")
     _parity(cfg)
     assert LAST_PATH["path"] == 3
 
@@ -212,8 +212,8 @@ def test_generic_handles_of_both_quantity_counts_coexist(monkeypatch):
     import paper_1903_11521_b200 as ydg
     monkeypatch.setenv("YDG_GENERIC", "1")
     monkeypatch.setenv("YDG_VISCO_GENERIC", "1")
-    c9 = _cfg("c0", nx=3, ny=3, nz=3, name="coexist-9")
-    c27 = _cfg("c3", N=2, nx=3, ny=3, nz=3, steps=1, name="coexist-27")
+    c9 = synth.CONFIGS["c0"].with_(nx=3, ny=3, nz=3, name="coexist-9")
+    c27 = synth.CONFIGS["c3"].with_(N=2, nx=3, ny=3, nz=3, steps=1, name="coexist-27")
     ins = {c.name: make_inputs(c) for c in (c9, c27)}
     hs = {}
     for c in (c9, c27):  # P = 9 first: the later P = 27 configuration must not clobber it
