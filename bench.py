@@ -76,6 +76,8 @@ def parse():
     ap.add_argument("--e2e-reps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=8, help="cubes per axis of the oracle sample")
+    ap.add_argument("--sims", type=int, default=1,
+                    help="fused simulations S (NEXT-1, P:1306-1308): element-simulations = elements x S")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="time ydg_step_graph (one CUDA graph per step); auto: on below 100k elements "
                          "(c0: launch-latency bound), 1 GPU only")
@@ -297,6 +299,8 @@ def run_ydg(args):
         omega, Y = synth.anelastic(cfg, mat)
         an = np.concatenate([omega, Y.ravel()])
     h = ydg.ydg_create(cfg.N, cfg.P, cfg.precision, device=local)
+    if args.sims > 1:
+        ydg.ydg_set_simulations(h, args.sims)
     if world > 1:
         import torch.distributed as dist
         uid = [torch.cuda.nccl.unique_id() if rank == 0 else None]
@@ -401,7 +405,7 @@ def run_ydg(args):
         ydg.ydg_destroy(h)
         return 0
 
-    ne_total = cfg.n_elements
+    ne_total = cfg.n_elements * args.sims  # element-simulations with fused simulations
     value = ne_total * args.steps / (ms_max / 1e3)
     n_launch = args.steps  # launches per kernel kind (single rank: 1 local + 1 neighbour per step)
     if world > 1:
@@ -446,7 +450,8 @@ def run_ydg(args):
         "scaling": "strong" if args.config in STRONG else "weak", "vs_baseline": None,
         "dtype": "f64" if cfg.precision == 8 else "f32",
         "data": "synthetic",
-        "config": {"workload": cfg.name, "model": "ADER-DG elastic tetrahedra" if cfg.P == 9 else "ADER-DG viscoelastic",
+        "config": {"workload": cfg.name + (f"-S{args.sims}" if args.sims > 1 else ""), "simulations": args.sims,
+                   "model": "ADER-DG elastic tetrahedra" if cfg.P == 9 else "ADER-DG viscoelastic",
                    "order": cfg.N, "quantities": cfg.P, "elements": ne_total, "elements_per_gpu": nloc,
                    "mesh": f"{cfg.nx}x{cfg.ny}x{cfg.nz} Kuhn cubes, periodic", "dt": cfg.dt,
                    "parallelism": f"zslab{world}" if world > 1 else "single",

@@ -59,9 +59,10 @@ enum {
   YDG_Q_PROF_LOCAL_MS = 13,    /* profiling: summed device time of local-kernel launches   */
   YDG_Q_PROF_NEIGH_MS = 14,    /* profiling: summed device time of neighbour launches      */
   YDG_Q_PROF_LAUNCHES = 15,    /* profiling: number of timed kernel launches               */
-  YDG_Q_KERNEL_PATH = 16       /* kernels a step runs: 0 fp64 elastic tensor-core (dm_local/
+  YDG_Q_KERNEL_PATH = 16,      /* kernels a step runs: 0 fp64 elastic tensor-core (dm_local/
                                   dm_flux), 1 fp32 sparse FFMA (ader_*), 2 viscoelastic
                                   tensor-core (vm_local/vm_neigh), 3 generic CSR (gen_*)    */
+  YDG_Q_SIMULATIONS = 17       /* fused simulations S (ydg_set_simulations)                 */
 };
 
 typedef struct ydg_solver ydg_solver; /* opaque, owned by the library */
@@ -86,6 +87,17 @@ int ydg_set_comm(ydg_solver* h, int rank, int nranks, const void* nccl_unique_id
  *  NCCL: the ranks are handles of one process (one host thread each) on one GPU, the halo
  *  goes device-to-device at host barriers -- for checking partition invariance on a single
  *  GPU; same plan, pack and unpack as the NCCL path. */
+
+/* Optional, before ydg_upload_mesh: S >= 1 fused simulations (an extra index
+ * s on the degrees of freedom, Q_skp; the mesh, material, star matrices and flux solvers
+ * are shared).  The S simulations of element e are the "element-simulations" v = e*S + s:
+ * after ydg_upload_mesh every element id of the DOF calls, ydg_get_neighbours and the
+ * YDG_Q_N_ELEMENTS / FIRST_LOCAL / N_LOCAL queries counts element-simulations, so the
+ * canonical DOF layout becomes [element][simulation][quantity][basis] and the neighbour of
+ * v across face i is Neigh(e, i) * S + s.  On the GPU the simulations of an element are
+ * adjacent lanes of a tile (the batch dimension every kernel already vectorises over).
+ * S in [1, 64]; YDG_ERR_STATE after ydg_upload_mesh. */
+int ydg_set_simulations(ydg_solver* h, int S);
 
 /* Upload the (global) mesh and material; builds geometry, star matrices, flux solvers and
  * the neighbour relation (Neigh, Face, Rot of P:1342) on the host in fp64.

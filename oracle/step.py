@@ -198,3 +198,50 @@ def literal_update(prob: Problem, Q, dt, nbtab):
     Inb = I[nb]           # (E, 4, B, P)
     out = out - np.einsum("ei,ikm,eimn,eiln,eilq,eipq->ekp", prob.s, R, fh, Rj, Inb, prob.Aminus)
     return out
+
+
+# ---- multiple fused simulations: the scheme with an extra index s
+# on the degrees of freedom Q_skp, the derivatives D_skp and the time integral I_skp; every
+# matrix (global, star, flux) is shared by the S simulations.
+
+def time_integral_fused(prob: Problem, Q, dt):
+    """(I, [D^0..D^N]) for Q (S, E, B, P):  D^(d+1)_sekp = sum_c Kt^c_kl D^d_selq A*^c_epq."""
+    D = Q.copy()
+    Ds = [D]
+    I = dt * D
+    for d in range(prob.N):
+        Dn = np.zeros_like(D)
+        for c in range(3):
+            Dn += np.einsum("kl,selq,epq->sekp", prob.Kt[c], D, prob.Astar[:, c])
+        if prob.E_src is not None:
+            Dn += np.einsum("sekq,epq->sekp", D, prob.E_src)
+        D = Dn
+        Ds.append(D)
+        I = I + dt ** (d + 2) / factorial(d + 2) * D
+    return I, Ds
+
+
+def update_fused(prob: Problem, Q, I):
+    """Q^(n+1)_sekp (P:1334-1342 with the index s); Q, I: (S, E, B, P), full mesh."""
+    out = Q.copy()
+    for c in range(3):
+        out += np.einsum("kl,selq,epq->sekp", prob.Kh[c], I, prob.Astar[:, c])
+    if prob.E_src is not None:
+        out += np.einsum("sekq,epq->sekp", I, prob.E_src)
+    for i in range(4):
+        out -= np.einsum("e,kl,selq,epq->sekp", prob.s[:, i], prob.Fm[i], I, prob.Aplus[:, i])
+    E = Q.shape[1]
+    for i in range(4):
+        Inb = I[:, prob.nb[:, i]]
+        for e in range(E):
+            Fp = prob.fp_mats[prob.fp_key[4 * e + i]]
+            out[:, e] -= prob.s[e, i] * np.einsum("kl,slq,pq->skp", Fp, Inb[:, e], prob.Aminus[e, i])
+    return out
+
+
+def step_fused(prob: Problem, Q, dt, nsteps=1):
+    """nsteps global time steps of S fused simulations; Q (S, E, B, P) internal layout."""
+    for _ in range(nsteps):
+        I, _ = time_integral_fused(prob, Q, dt)
+        Q = update_fused(prob, Q, I)
+    return Q

@@ -27,9 +27,9 @@ YDG_OK, YDG_ERR_ARG, YDG_ERR_STATE, YDG_ERR_CUDA, YDG_ERR_NCCL, YDG_ERR_MESH, YD
 (YDG_Q_N_ELEMENTS, YDG_Q_FIRST_LOCAL, YDG_Q_N_LOCAL, YDG_Q_NZ_FLOPS, YDG_Q_ALG_BYTES, YDG_Q_B,
  YDG_Q_BTILDE, YDG_Q_DEVICE_BYTES, YDG_Q_LAUNCHES_PER_STEP, YDG_Q_LOCAL_BYTES, YDG_Q_NEIGH_BYTES,
  YDG_Q_LOCAL_FLOPS, YDG_Q_NEIGH_FLOPS, YDG_Q_PROF_LOCAL_MS, YDG_Q_PROF_NEIGH_MS,
- YDG_Q_PROF_LAUNCHES, YDG_Q_KERNEL_PATH) = range(17)
+ YDG_Q_PROF_LAUNCHES, YDG_Q_KERNEL_PATH, YDG_Q_SIMULATIONS) = range(18)
 
-EXPORTS = ("ydg_create", "ydg_last_error", "ydg_set_comm", "ydg_upload_mesh", "ydg_upload_dofs",
+EXPORTS = ("ydg_create", "ydg_last_error", "ydg_set_comm", "ydg_set_simulations", "ydg_upload_mesh", "ydg_upload_dofs",
            "ydg_upload_dofs_device", "ydg_download_dofs_device", "ydg_step", "ydg_step_graph", "ydg_synchronize",
            "ydg_download_dofs", "ydg_get_neighbours", "ydg_halo_plan", "ydg_profile", "ydg_query",
            "ydg_error_string", "ydg_destroy")
@@ -56,6 +56,7 @@ def lib():
         L.ydg_last_error.restype = ctypes.c_char_p
         L.ydg_set_comm.argtypes = [vp, i32, i32, ctypes.c_char_p]
         L.ydg_upload_mesh.argtypes = [vp, i64, vp, vp, vp, vp]
+        L.ydg_set_simulations.argtypes = [vp, i32]
         L.ydg_upload_dofs.argtypes = [vp, i64, i64, vp]
         L.ydg_upload_dofs_device.argtypes = [vp, i64, i64, vp, vp]
         L.ydg_download_dofs_device.argtypes = [vp, i64, i64, vp, vp]
@@ -108,6 +109,10 @@ def ydg_create(order, quantities=9, precision=8, device=0):
 
 def ydg_set_comm(h, rank, nranks, nccl_unique_id: bytes):
     _check(h, lib().ydg_set_comm(h.ptr, rank, nranks, nccl_unique_id))
+
+
+def ydg_set_simulations(h, S):
+    _check(h, lib().ydg_set_simulations(h.ptr, int(S)))
 
 
 def ydg_upload_mesh(h, elem_xyz, elem_vid, material, anelastic=None):

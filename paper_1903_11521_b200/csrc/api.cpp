@@ -18,6 +18,7 @@
 #include "generated/ydg_matrices.h"
 #include "generic.h"
 #include "halo.h"
+#include <cstdio>
 #include "kernels.cuh"
 #include "setup.h"
 
@@ -68,6 +69,7 @@ struct ydg_solver {
   // ydg_step_graph: the launch sequence of (dt, nsteps) captured once into a CUDA graph
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t gexec = nullptr;
+  int sims = 1;  // fused simulations (element-simulations v = e * sims + s)
   double g_dt = 0;
   int g_n = -1;
 };
@@ -576,11 +578,48 @@ int ydg_set_comm(ydg_solver* h, int rank, int nranks, const void* nccl_unique_id
   return YDG_OK;
 }
 
+int ydg_set_simulations(ydg_solver* h, int S) {
+  int rc = check(h);
+  if (rc) return rc;
+  if (h->have_mesh) return fail(h, YDG_ERR_STATE, "ydg_set_simulations must precede ydg_upload_mesh");
+  if (S < 1 || S > 64) return fail(h, YDG_ERR_ARG, "simulations must be in [1, 64]");
+  h->sims = S;
+  return YDG_OK;
+}
+
+static int upload_mesh_impl(ydg_solver* h, int64_t ne, const double* xyz, const int64_t* vid,
+                            const double* material, const double* anelastic);
+
 int ydg_upload_mesh(ydg_solver* h, int64_t ne, const double* xyz, const int64_t* vid,
                     const double* material, const double* anelastic) {
   int rc = check(h);
   if (rc) return rc;
   if (ne <= 0 || !xyz || !vid || !material) return fail(h, YDG_ERR_ARG, "null mesh input or ne <= 0");
+  if (h->sims == 1) return upload_mesh_impl(h, ne, xyz, vid, material, anelastic);
+  // fused simulations: element-simulation v = e * S + s carries element e's geometry and
+  // material; the vertex ids of simulation s are shifted by s * (max id + 1), so faces match
+  // within a simulation only and Neigh(v, i) = Neigh(e, i) * S + s
+  const int64_t S = h->sims, nv = ne * S;
+  int64_t vmax = 0;
+  for (int64_t i = 0; i < ne * 4; ++i) vmax = std::max(vmax, vid[i]);
+  std::vector<double> xyz_v(static_cast<size_t>(nv) * 12), mat_v(static_cast<size_t>(nv) * 3);
+  std::vector<int64_t> vid_v(static_cast<size_t>(nv) * 4);
+  std::vector<double> an_v;
+  if (anelastic) an_v.assign(anelastic, anelastic + 3), an_v.resize(3 + static_cast<size_t>(nv) * 6);
+  for (int64_t e = 0; e < ne; ++e)
+    for (int64_t sm = 0; sm < S; ++sm) {
+      const int64_t v = e * S + sm;
+      std::copy(xyz + e * 12, xyz + e * 12 + 12, xyz_v.begin() + v * 12);
+      std::copy(material + e * 3, material + e * 3 + 3, mat_v.begin() + v * 3);
+      for (int k = 0; k < 4; ++k) vid_v[v * 4 + k] = vid[e * 4 + k] + sm * (vmax + 1);
+      if (anelastic) std::copy(anelastic + 3 + e * 6, anelastic + 9 + e * 6, an_v.begin() + 3 + v * 6);
+    }
+  return upload_mesh_impl(h, nv, xyz_v.data(), vid_v.data(), mat_v.data(), anelastic ? an_v.data() : nullptr);
+}
+
+static int upload_mesh_impl(ydg_solver* h, int64_t ne, const double* xyz, const int64_t* vid,
+                            const double* material, const double* anelastic) {
+  int rc = 0;
   if (h->P == 27 && !anelastic) return fail(h, YDG_ERR_ARG, "viscoelastic solver needs anelastic data");
   for (int64_t e = 0; e < ne; ++e) {
     const double* m = material + e * 3;
@@ -885,6 +924,7 @@ int ydg_query(ydg_solver* h, int what, double* v) {
     case YDG_Q_PROF_LOCAL_MS: *v = h->prof_ms[0]; break;
     case YDG_Q_PROF_NEIGH_MS: *v = h->prof_ms[1]; break;
     case YDG_Q_PROF_LAUNCHES: *v = static_cast<double>(h->prof_launches); break;
+    case YDG_Q_SIMULATIONS: *v = static_cast<double>(h->sims); break;
     case YDG_Q_N_ELEMENTS: *v = static_cast<double>(h->ne); break;
     case YDG_Q_FIRST_LOCAL: *v = static_cast<double>(h->first); break;
     case YDG_Q_N_LOCAL: *v = static_cast<double>(h->nlocal); break;

@@ -134,6 +134,27 @@ __device__ __forceinline__ double afrag_l(const Ctx& x, int g, int r) {
   return (kLocalFs && r < kLocalFsCap) ? afrag_s(x, r) : afrag_g(x, g);
 }
 __device__ __forceinline__ double afrag_f(const Ctx& x, int g, int r) { return kFluxFs ? afrag_s(x, r) : afrag_g(x, g); }
+// L2 eviction hints on the streaming stores (bit mask, build flag): 1 = trace bulk stores of
+// the local kernel, 2 = its Q stores, 4 = the flux kernel's Q stores -- evict_first, so that
+// the Q^n rows a tile re-reads stay in L2
+#ifndef YDG_L2HINT
+#define YDG_L2HINT 0
+#endif
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+template <int BIT>
+__device__ __forceinline__ void st_q2(double* p, double2 v) {
+  if constexpr ((YDG_L2HINT & BIT) != 0) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
+                 "l"(evict_first_policy())
+                 : "memory");
+  } else {
+    *reinterpret_cast<double2*>(p) = v;
+  }
+}
 __device__ __forceinline__ double ld_stream(const double* p) {
   double v;
   asm("ld.global.nc.L1::evict_first.f64 %0, [%1];" : "=d"(v) : "l"(p));
@@ -307,8 +328,8 @@ __device__ __forceinline__ void add_q(const Ctx& x, double* Qt, double (&acc)[MT
       if (row == 0xff) continue;
 #pragma unroll
       for (int k = 0; k < kU; ++k)
-        *reinterpret_cast<double2*>(Qt + row * kRS + ccol(x, k)) =
-            make_double2(acc[m0 + k2][k][0] + vc[k2][k].x, acc[m0 + k2][k][1] + vc[k2][k].y);
+        st_q2<2>(Qt + row * kRS + ccol(x, k),
+                 make_double2(acc[m0 + k2][k][0] + vc[k2][k].x, acc[m0 + k2][k][1] + vc[k2][k].y));
     }
     if (m0 + 2 < MT) {
 #pragma unroll
@@ -395,8 +416,7 @@ __device__ __forceinline__ void store_qf(const Ctx& x, double* Qt, unsigned long
     if (row == 0xff) continue;
 #pragma unroll
     for (int k = 0; k < kU; ++k)
-      *reinterpret_cast<double2*>(Qt + row * kRS + qcolf(x, k)) =
-          make_double2(q[k2][k].x + acc[k2][k][0], q[k2][k].y + acc[k2][k][1]);
+      st_q2<4>(Qt + row * kRS + qcolf(x, k), make_double2(q[k2][k].x + acc[k2][k][0], q[k2][k].y + acc[k2][k][1]));
   }
 }
 
@@ -561,9 +581,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
-               "r"(bytes)
-               : "memory");
+  if constexpr ((YDG_L2HINT & 1) != 0) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+                 "r"(smem_addr(src)), "r"(bytes), "l"(evict_first_policy())
+                 : "memory");
+  } else {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+                 "r"(bytes)
+                 : "memory");
+  }
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 template <int K>

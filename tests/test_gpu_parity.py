@@ -249,3 +249,35 @@ def test_step_graph_matches_step():
         outs.append(ydg.ydg_download_dofs(h, 0, cfg.n_elements))
         ydg.ydg_destroy(h)
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("S,prec", [(4, 8), (16, 8), (8, 4)])
+def test_fused_simulations(S, prec):
+    """NEXT-1: S fused simulations (element-simulations v = e*S + s, adjacent
+    lanes of a tile) against the oracle's scheme with the index s; neighbours Neigh(e,i)*S+s."""
+    import paper_1903_11521_b200 as ydg
+    from oracle import step as ostep
+    cfg = synth.CONFIGS["c0"].with_(vperm=True, precision=prec, name=f"fused-S{S}")
+    xyz, vid, mat, _, _ = make_inputs(cfg)
+    E = cfg.n_elements
+    Qs = synth.uniform(cfg.seed + 1, synth.STREAM_DOFS, np.arange(S * E * 9 * cfg.B, dtype=np.uint64), -1, 1)
+    Qs = Qs.reshape(S, E, 9, cfg.B)  # [s][e][p][k]
+    h = ydg.ydg_create(cfg.N, 9, prec)
+    ydg.ydg_set_simulations(h, S)
+    ydg.ydg_upload_mesh(h, xyz, vid, mat)
+    assert ydg.ydg_query(h, ydg.YDG_Q_N_ELEMENTS) == S * E
+    assert ydg.ydg_query(h, ydg.YDG_Q_SIMULATIONS) == S
+    dt_np = np.float64 if prec == 8 else np.float32
+    ydg.ydg_upload_dofs(h, 0, np.ascontiguousarray(Qs.transpose(1, 0, 2, 3)).reshape(E * S, 9, cfg.B).astype(dt_np))
+    ydg.ydg_step(h, cfg.dt, 2)
+    got = ydg.ydg_download_dofs(h, 0, E * S).reshape(E, S, 9, cfg.B).transpose(1, 0, 2, 3).astype(np.float64)
+    nb, j, hr = ydg.ydg_get_neighbours(h, 0, E * S)
+    ydg.ydg_destroy(h)
+    onb, oj, oh = omesh.neighbour_table(vid)
+    v = np.arange(E * S)
+    assert np.array_equal(nb, onb[v // S] * S + (v % S)[:, None])
+    assert np.array_equal(j, oj[v // S]) and np.array_equal(hr, oh[v // S])
+    prob = ostep.setup(cfg.N, xyz, vid, mat)
+    ref = ostep.step_fused(prob, np.ascontiguousarray(Qs.transpose(0, 1, 3, 2)), cfg.dt, 2).transpose(0, 1, 3, 2)
+    for s in range(S):
+        check_parity(rel_err(got[s], ref[s]), prec, f"fused S={S} s={s}")

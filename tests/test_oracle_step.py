@@ -160,3 +160,19 @@ def test_visco_constant_state_is_truncated_exponential():
         want = q0 @ S
         assert np.abs(out[e, 0] - want).max() < 1e-12 * np.abs(want).max() + 1e-9
         assert np.abs(out[e, 1:]).max() < 1e-9 * np.abs(want).max()
+
+
+def test_fused_simulations_equal_independent_runs():
+    """S fused simulations (extra index s on Q, D, I; all matrices shared) are S
+    independent runs of the single-simulation scheme."""
+    prob, *_ = _problem(SMALL)
+    rng = np.random.default_rng(5)
+    S = 3
+    Qs = rng.uniform(-1, 1, (S, SMALL.n_elements, comb(SMALL.N + 3, 3), 9))
+    fused = step.step_fused(prob, Qs, SMALL.dt, 2)
+    for s in range(S):
+        single = step.step(prob, Qs[s], SMALL.dt, 2)
+        assert np.abs(fused[s] - single).max() <= 1e-13 * np.abs(single).max()
+    # the simulations do not mix: a zero simulation stays zero
+    Qs[1] = 0.0
+    assert not step.step_fused(prob, Qs, SMALL.dt, 1)[1].any()
