@@ -38,7 +38,9 @@ struct ydg_solver {
   int64_t nslots = 0;   // local element slots incl. ghosts (multiple of lanes)
   int lanes = 32;       // elements per tile: kDmLanes (fp64 tensor-core kernels) or 32 (fp32)
   int64_t ntiles = 0;   // owned tiles
-  Neighbours nbr;       // global tables (for ydg_get_neighbours)
+  Neighbours nbr;       // global tables in internal element numbering
+  Neighbours nbr_ext;   // ... in the caller's numbering when the elements are reordered
+  int32_t* slot_of = nullptr;  // device: owned external local index -> internal slot (or null)
   // device buffers
   void* Q = nullptr;
   void* traces = nullptr;
@@ -101,6 +103,7 @@ int trace_block(const ydg_solver* h) { return h->prec == 8 ? (h->Bt * h->P + 1) 
 
 void free_mesh(ydg_solver* h) {
   for (void** p : {&h->Q, &h->traces, &h->star, &h->aplus, &h->aminus, &h->staging, &h->src,
+                   reinterpret_cast<void**>(&h->slot_of),
                    reinterpret_cast<void**>(&h->nb), reinterpret_cast<void**>(&h->jh),
                    reinterpret_cast<void**>(&h->nb64), reinterpret_cast<void**>(&h->jh_e)}) {
     if (*p) cudaFree(*p);
@@ -589,6 +592,7 @@ int ydg_set_simulations(ydg_solver* h, int S) {
 
 static int upload_mesh_impl(ydg_solver* h, int64_t ne, const double* xyz, const int64_t* vid,
                             const double* material, const double* anelastic);
+static int upload_tiled(ydg_solver* h, const double* xyz, const double* material, const double* anelastic);
 
 int ydg_upload_mesh(ydg_solver* h, int64_t ne, const double* xyz, const int64_t* vid,
                     const double* material, const double* anelastic) {
@@ -617,6 +621,60 @@ int ydg_upload_mesh(ydg_solver* h, int64_t ne, const double* xyz, const int64_t*
   return upload_mesh_impl(h, nv, xyz_v.data(), vid_v.data(), mat_v.data(), anelastic ? an_v.data() : nullptr);
 }
 
+// Internal element order of the tiled paths (see upload_mesh_impl): ext_of[i] = caller id of
+// internal element i.  Each rank range [r ne / R, (r+1) ne / R) is permuted within itself
+// (so every rank derives the same global numbering): elements with a neighbour in another
+// range first, then ascending Morton code of the centroid (21 bits per axis over the bounding
+// box of all centroids), ties by caller id.
+static std::vector<int64_t> locality_order(int64_t ne, const double* xyz, const Neighbours& nbr, int nranks) {
+  std::vector<double> c(static_cast<size_t>(ne) * 3);
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int64_t e = 0; e < ne; ++e)
+    for (int d = 0; d < 3; ++d) {
+      const double* x = xyz + e * 12;
+      const double v = 0.25 * (x[d] + x[3 + d] + x[6 + d] + x[9 + d]);
+      c[e * 3 + d] = v;
+      lo[d] = std::min(lo[d], v);
+      hi[d] = std::max(hi[d], v);
+    }
+  auto spread = [](uint64_t v) {  // 21 bits -> every third bit
+    v &= 0x1fffff;
+    v = (v | v << 32) & 0x1f00000000ffffULL;
+    v = (v | v << 16) & 0x1f0000ff0000ffULL;
+    v = (v | v << 8) & 0x100f00f00f00f00fULL;
+    v = (v | v << 4) & 0x10c30c30c30c30c3ULL;
+    v = (v | v << 2) & 0x1249249249249249ULL;
+    return v;
+  };
+  std::vector<uint64_t> key(static_cast<size_t>(ne));
+  for (int64_t e = 0; e < ne; ++e) {
+    uint64_t m = 0;
+    for (int d = 0; d < 3; ++d) {
+      const double span = hi[d] > lo[d] ? hi[d] - lo[d] : 1.0;
+      const uint64_t q = static_cast<uint64_t>((c[e * 3 + d] - lo[d]) / span * 2097151.0);
+      m |= spread(q) << d;
+    }
+    key[e] = m;
+  }
+  std::vector<int64_t> ext_of(static_cast<size_t>(ne));
+  for (int r = 0; r < nranks; ++r) {
+    const int64_t a = ne * r / nranks, b = ne * (r + 1) / nranks;
+    std::vector<std::pair<std::pair<int, uint64_t>, int64_t>> k;
+    k.reserve(static_cast<size_t>(b - a));
+    for (int64_t e = a; e < b; ++e) {
+      int bnd = 0;
+      for (int i = 0; i < 4; ++i) {
+        const int64_t n = nbr.nb[e * 4 + i];
+        bnd |= (n < a || n >= b);
+      }
+      k.push_back({{bnd ? 0 : 1, key[e]}, e});
+    }
+    std::sort(k.begin(), k.end());
+    for (int64_t i = a; i < b; ++i) ext_of[i] = k[i - a].second;
+  }
+  return ext_of;
+}
+
 static int upload_mesh_impl(ydg_solver* h, int64_t ne, const double* xyz, const int64_t* vid,
                             const double* material, const double* anelastic) {
   int rc = 0;
@@ -630,10 +688,40 @@ static int upload_mesh_impl(ydg_solver* h, int64_t ne, const double* xyz, const 
   std::string err;
   if (!match_faces(ne, vid, &nbr, &err)) return fail(h, YDG_ERR_MESH, err);
   free_mesh(h);
-  h->nbr = std::move(nbr);
   h->ne = ne;
   h->first = ne * h->rank / h->nranks;
   h->nlocal = ne * (h->rank + 1) / h->nranks - h->first;
+  // Optional locality reordering of the tiled (fp64 / fp32 elastic) paths (YDG_REORDER=1):
+  // within every rank's element range, elements with an off-rank neighbour first (they are
+  // launched before the halo), then by the Morton code of their centroid, so that the
+  // neighbour traces a flux tile gathers were written by nearby tiles.  Internal numbering
+  // only: the DOF calls, ydg_get_neighbours and the rank ranges use the caller's ids.
+  // Measured on c1 / c2: flux 7.90 -> 7.87 ms, fp32 ader_neigh 23.9 -> 25.6 ms,
+  // so it is off by default (the kernels are latency-, not DRAM-bound).
+  std::vector<int64_t> ext_of;
+  const char* ro = std::getenv("YDG_REORDER");
+  if (!h->generic && ro && ro[0] == '1') {
+    ext_of = locality_order(ne, xyz, nbr, h->nranks);
+    std::vector<double> xyz_i(static_cast<size_t>(ne) * 12), mat_i(static_cast<size_t>(ne) * 3);
+    std::vector<int64_t> vid_i(static_cast<size_t>(ne) * 4);
+    for (int64_t i = 0; i < ne; ++i) {
+      const int64_t e = ext_of[i];
+      std::copy(xyz + e * 12, xyz + e * 12 + 12, xyz_i.begin() + i * 12);
+      std::copy(material + e * 3, material + e * 3 + 3, mat_i.begin() + i * 3);
+      std::copy(vid + e * 4, vid + e * 4 + 4, vid_i.begin() + i * 4);
+    }
+    Neighbours nbr_i;
+    if (!match_faces(ne, vid_i.data(), &nbr_i, &err)) return fail(h, YDG_ERR_MESH, err);
+    h->nbr_ext = std::move(nbr);
+    h->nbr = std::move(nbr_i);
+    std::vector<int32_t> slot(static_cast<size_t>(h->nlocal));
+    for (int64_t i = h->first; i < h->first + h->nlocal; ++i) slot[ext_of[i] - h->first] = static_cast<int32_t>(i - h->first);
+    if ((rc = dalloc(h, reinterpret_cast<void**>(&h->slot_of), slot.size() * sizeof(int32_t)))) { free_mesh(h); return rc; }
+    CUDA_OR_FAIL(h, cudaMemcpy(h->slot_of, slot.data(), slot.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    return upload_tiled(h, xyz_i.data(), mat_i.data(), anelastic);
+  }
+  h->nbr = std::move(nbr);
+  h->nbr_ext = Neighbours();
   if (h->generic) {
     if (h->nranks > 1) return fail(h, YDG_ERR_UNSUPPORTED, "the generic (viscoelastic) path runs on one rank");
     rc = generic_upload_mesh(h, xyz, material, anelastic);
@@ -641,6 +729,12 @@ static int upload_mesh_impl(ydg_solver* h, int64_t ne, const double* xyz, const 
     h->have_mesh = true;
     return YDG_OK;
   }
+  return upload_tiled(h, xyz, material, anelastic);
+}
+
+// Device layout of the tiled paths, for the elements in internal numbering (h->nbr).
+static int upload_tiled(ydg_solver* h, const double* xyz, const double* material, const double* anelastic) {
+  int rc = 0;
   h->lanes = h->prec == 8 ? kDmLanes : 32;
   const int kLanes = h->lanes;
   h->ntiles = (h->nlocal + kLanes - 1) / kLanes;
@@ -693,9 +787,10 @@ static int upload_mesh_impl(ydg_solver* h, int64_t ne, const double* xyz, const 
     // cover every tile with a ghost (for other orders these ranges simply grow).
     h->bnd_lo = h->bnd_hi = 0;
     const int64_t half = h->ntiles / 2;
+    const bool reordered = !h->nbr_ext.nb.empty();  // locality order: boundary elements first
     for (int64_t t = 0; t < h->ntiles; ++t)
       if (is_boundary[t]) {
-        if (t < half) h->bnd_lo = std::max(h->bnd_lo, t + 1);
+        if (t < half || reordered) h->bnd_lo = std::max(h->bnd_lo, t + 1);
         else h->bnd_hi = std::max(h->bnd_hi, h->ntiles - t);
       }
   }
@@ -766,14 +861,14 @@ static int xfer_dofs(ydg_solver* h, int64_t first, int64_t count, const void* sr
         CUDA_OR_FAIL(h, cudaMemcpyAsync(buf, static_cast<const char*>(src_host) + c0 * per * eb, n * per * eb,
                                         cudaMemcpyHostToDevice, s));
       }
-      cudaError_t e = eb == 8 ? launch_to_tiled<double>(h->P, h->B, h->lanes, static_cast<const double*>(buf), static_cast<double*>(h->Q), lfirst, n, s)
-                              : launch_to_tiled<float>(h->P, h->B, h->lanes, static_cast<const float*>(buf), static_cast<float*>(h->Q), lfirst, n, s);
+      cudaError_t e = eb == 8 ? launch_to_tiled<double>(h->P, h->B, h->lanes, static_cast<const double*>(buf), static_cast<double*>(h->Q), lfirst, n, h->slot_of, s)
+                              : launch_to_tiled<float>(h->P, h->B, h->lanes, static_cast<const float*>(buf), static_cast<float*>(h->Q), lfirst, n, h->slot_of, s);
       CUDA_OR_FAIL(h, e);
       if (!dev_side) CUDA_OR_FAIL(h, cudaStreamSynchronize(s));
     } else {
       if (dev_side) buf = static_cast<char*>(dst_dev) + c0 * per * eb;
-      cudaError_t e = eb == 8 ? launch_to_canonical<double>(h->P, h->B, h->lanes, static_cast<const double*>(h->Q), static_cast<double*>(buf), lfirst, n, s)
-                              : launch_to_canonical<float>(h->P, h->B, h->lanes, static_cast<const float*>(h->Q), static_cast<float*>(buf), lfirst, n, s);
+      cudaError_t e = eb == 8 ? launch_to_canonical<double>(h->P, h->B, h->lanes, static_cast<const double*>(h->Q), static_cast<double*>(buf), lfirst, n, h->slot_of, s)
+                              : launch_to_canonical<float>(h->P, h->B, h->lanes, static_cast<const float*>(h->Q), static_cast<float*>(buf), lfirst, n, h->slot_of, s);
       CUDA_OR_FAIL(h, e);
       if (!dev_side) {
         CUDA_OR_FAIL(h, cudaMemcpyAsync(static_cast<char*>(dst_host) + c0 * per * eb, buf, n * per * eb,
@@ -860,9 +955,10 @@ int ydg_get_neighbours(ydg_solver* h, int64_t first, int64_t count, int64_t* nb,
   if (!h->have_mesh) return fail(h, YDG_ERR_STATE, "upload the mesh first");
   if (!nb || !j || !hr || count < 0 || first < 0 || first + count > h->ne)
     return fail(h, YDG_ERR_ARG, "bad neighbour query");
-  std::memcpy(nb, h->nbr.nb.data() + first * 4, count * 4 * sizeof(int64_t));
-  std::memcpy(j, h->nbr.j.data() + first * 4, count * 4);
-  std::memcpy(hr, h->nbr.h.data() + first * 4, count * 4);
+  const Neighbours& t = h->nbr_ext.nb.empty() ? h->nbr : h->nbr_ext;
+  std::memcpy(nb, t.nb.data() + first * 4, count * 4 * sizeof(int64_t));
+  std::memcpy(j, t.j.data() + first * 4, count * 4);
+  std::memcpy(hr, t.h.data() + first * 4, count * 4);
   return YDG_OK;
 }
 

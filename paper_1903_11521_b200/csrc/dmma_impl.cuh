@@ -138,7 +138,7 @@ __device__ __forceinline__ double afrag_f(const Ctx& x, int g, int r) { return k
 // the local kernel, 2 = its Q stores, 4 = the flux kernel's Q stores -- evict_first, so that
 // the Q^n rows a tile re-reads stay in L2
 #ifndef YDG_L2HINT
-#define YDG_L2HINT 0
+#define YDG_L2HINT 3  // measured: local 15.31 -> 14.77-14.95 ms (c1); 7 (also flux Q stores) slows the flux kernel
 #endif
 __device__ __forceinline__ unsigned long long evict_first_policy() {
   unsigned long long pol;

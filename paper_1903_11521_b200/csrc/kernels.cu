@@ -48,27 +48,27 @@ constexpr int kRS = kP * kLanes;
 // canonical [e][p][k] <-> tiled [tile][k][p][L] (L = 16 for fp64, 32 for fp32)
 template <typename T>
 __global__ void to_tiled_kernel(int P, int B, int L, const T* __restrict__ canon, T* __restrict__ tiled,
-                                int64_t first, int64_t count) {
+                                int64_t first, int64_t count, const int32_t* __restrict__ slot_of) {
   const int64_t n = count * P * B;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t el = i / (P * B);
     const int r = static_cast<int>(i - el * P * B);
     const int p = r / B, k = r - p * B;
-    const int64_t e = first + el;
+    const int64_t e = slot_of ? slot_of[first + el] : first + el;
     tiled[((e / L) * B + k) * P * L + p * L + (e % L)] = canon[i];
   }
 }
 template <typename T>
 __global__ void to_canonical_kernel(int P, int B, int L, const T* __restrict__ tiled, T* __restrict__ canon,
-                                    int64_t first, int64_t count) {
+                                    int64_t first, int64_t count, const int32_t* __restrict__ slot_of) {
   const int64_t n = count * P * B;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t el = i / (P * B);
     const int r = static_cast<int>(i - el * P * B);
     const int p = r / B, k = r - p * B;
-    const int64_t e = first + el;
+    const int64_t e = slot_of ? slot_of[first + el] : first + el;
     canon[i] = tiled[((e / L) * B + k) * P * L + p * L + (e % L)];
   }
 }
@@ -166,16 +166,16 @@ cudaError_t launch_neigh(int N, const StepParams<T>& p, int grid, cudaStream_t s
 }
 template <typename T>
 cudaError_t launch_to_tiled(int P, int B, int L, const T* canon, T* tiled, int64_t first, int64_t count,
-                            cudaStream_t s) {
+                            const int32_t* slot_of, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  to_tiled_kernel<T><<<148 * 8, 256, 0, s>>>(P, B, L, canon, tiled, first, count);
+  to_tiled_kernel<T><<<148 * 8, 256, 0, s>>>(P, B, L, canon, tiled, first, count, slot_of);
   return cudaGetLastError();
 }
 template <typename T>
 cudaError_t launch_to_canonical(int P, int B, int L, const T* tiled, T* canon, int64_t first,
-                                int64_t count, cudaStream_t s) {
+                                int64_t count, const int32_t* slot_of, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  to_canonical_kernel<T><<<148 * 8, 256, 0, s>>>(P, B, L, tiled, canon, first, count);
+  to_canonical_kernel<T><<<148 * 8, 256, 0, s>>>(P, B, L, tiled, canon, first, count, slot_of);
   return cudaGetLastError();
 }
 
@@ -183,9 +183,9 @@ template cudaError_t launch_local<double>(int, const StepParams<double>&, int, c
 template cudaError_t launch_local<float>(int, const StepParams<float>&, int, cudaStream_t);
 template cudaError_t launch_neigh<double>(int, const StepParams<double>&, int, cudaStream_t);
 template cudaError_t launch_neigh<float>(int, const StepParams<float>&, int, cudaStream_t);
-template cudaError_t launch_to_tiled<double>(int, int, int, const double*, double*, int64_t, int64_t, cudaStream_t);
-template cudaError_t launch_to_tiled<float>(int, int, int, const float*, float*, int64_t, int64_t, cudaStream_t);
-template cudaError_t launch_to_canonical<double>(int, int, int, const double*, double*, int64_t, int64_t, cudaStream_t);
-template cudaError_t launch_to_canonical<float>(int, int, int, const float*, float*, int64_t, int64_t, cudaStream_t);
+template cudaError_t launch_to_tiled<double>(int, int, int, const double*, double*, int64_t, int64_t, const int32_t*, cudaStream_t);
+template cudaError_t launch_to_tiled<float>(int, int, int, const float*, float*, int64_t, int64_t, const int32_t*, cudaStream_t);
+template cudaError_t launch_to_canonical<double>(int, int, int, const double*, double*, int64_t, int64_t, const int32_t*, cudaStream_t);
+template cudaError_t launch_to_canonical<float>(int, int, int, const float*, float*, int64_t, int64_t, const int32_t*, cudaStream_t);
 
 }  // namespace ydg

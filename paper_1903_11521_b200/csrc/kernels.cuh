@@ -53,10 +53,10 @@ template <typename T>
 cudaError_t launch_neigh(int N, const StepParams<T>& p, int grid, cudaStream_t s);
 template <typename T>
 cudaError_t launch_to_tiled(int P, int B, int L, const T* canon, T* tiled, int64_t first, int64_t count,
-                            cudaStream_t s);
+                            const int32_t* slot_of, cudaStream_t s);
 template <typename T>
 cudaError_t launch_to_canonical(int P, int B, int L, const T* tiled, T* canon, int64_t first,
-                                int64_t count, cudaStream_t s);
+                                int64_t count, const int32_t* slot_of, cudaStream_t s);
 size_t local_smem_bytes(int N, int elem_bytes);
 size_t sparse_local_smem(int N, int elem_bytes);
 size_t sparse_neigh_smem(int N, int elem_bytes);

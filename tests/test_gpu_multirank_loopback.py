@@ -61,3 +61,23 @@ def test_zslab_partition_fp32():
     ref = _run(cfg, 1, cfg.steps)
     got = _run(cfg, 2, cfg.steps)
     assert np.array_equal(got, ref), np.abs(got - ref).max()
+
+
+def test_c4_replica_eight_ranks():
+    """BASELINE configs[4] shape (N = 5 fp64, strong scaling over z-slabs) on an 8x8x16-cube
+    replica split into 8 slabs of 2 cube layers (every element touches a slab boundary side),
+    random neighbour relations (vperm): bitwise the 1-rank result."""
+    cfg = synth.CONFIGS["c4"].replica(8, 8, 16, steps=2).with_(vperm=True)
+    ref = _run(cfg, 1, cfg.steps)
+    got = _run(cfg, 8, cfg.steps)
+    assert np.array_equal(got, ref), np.abs(got - ref).max()
+
+
+def test_reordered_elements_are_bitwise_invariant(monkeypatch):
+    """YDG_REORDER=1 (Morton / boundary-first internal order) changes no result bit, on one
+    rank and on 3 ranks."""
+    cfg = synth.CONFIGS["c1"].replica(6, steps=2).with_(vperm=True)
+    ref = _run(cfg, 1, cfg.steps)
+    monkeypatch.setenv("YDG_REORDER", "1")
+    assert np.array_equal(_run(cfg, 1, cfg.steps), ref)
+    assert np.array_equal(_run(cfg, 3, cfg.steps), ref)
