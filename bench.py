@@ -476,6 +476,92 @@ def run_ydg(args):
     return 0
 
 
+def run_lina(args):
+    """LinA workload (NEXT-3): ADER-DG-SEM acoustics, order 8, 64^3 cuboids."""
+    import torch
+    import paper_1903_11521_b200 as ydg
+    rank, world, local = dist_setup(args)
+    if world > 1:
+        if rank == 0:
+            print(json.dumps({"error": "the LinA workload runs on one GPU"}), flush=True)
+        return 0
+    cfg = synth.LINA_CONFIGS[args.config]
+    if args.replica:
+        cfg = cfg.with_(nx=args.replica, ny=args.replica, nz=args.replica)
+    mat = synth.lina_material(cfg)
+    h = ydg.lina_create(cfg.N, 8, local)
+    ydg.lina_upload_grid(h, cfg.nx, cfg.ny, cfg.nz, np.array(cfg.h), mat)
+    n = cfg.N + 1
+    E = cfg.n_elements
+    host = torch.empty((E, 4, n, n, n), dtype=torch.float64, pin_memory=True)
+    Qh = host.numpy()
+    Qh[...] = synth.lina_dofs(cfg)
+    ydg.lina_upload_dofs(h, 0, Qh)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    sptr = stream.cuda_stream
+    for _ in range(args.warmup):
+        ydg.lina_step(h, cfg.dt, 1, stream=sptr)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            ydg.lina_step(h, cfg.dt, 1, stream=sptr)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clocks = clk.summary()
+    flops = ydg.lina_query(h, ydg.LINA_Q_NZ_FLOPS)
+    abytes = ydg.lina_query(h, ydg.LINA_Q_ALG_BYTES)
+    probe = ydg.lina_download_dofs(h, 0, min(E, 16))
+    e2e = []
+    for _ in range(max(1, args.e2e_reps)):
+        t0 = time.perf_counter()
+        ydg.lina_upload_dofs(h, 0, Qh)
+        ydg.lina_step(h, cfg.dt, cfg.steps)
+        Qh[...] = ydg.lina_download_dofs(h, 0, E)
+        e2e.append(1e3 * (time.perf_counter() - t0))
+    value = E * args.steps / (ms / 1e3)
+    ach = value * flops / 1e12
+    qbytes = E * 4 * n ** 3 * 8
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import lina as olina
+        small = cfg.with_(nx=4, ny=4, nz=4)
+        g = olina.setup(small.N, small.nx, small.ny, small.nz, small.h, synth.lina_material(small))
+        Qs = np.ascontiguousarray(synth.lina_dofs(small).transpose(0, 2, 3, 4, 1))
+        olina.step(g, Qs, small.dt, 1)
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            olina.step(g, Qs, small.dt, 1)
+            ts.append(time.perf_counter() - t0)
+        cpu = {"value": small.n_elements / statistics.median(ts), "unit": UNIT, "cores": os.cpu_count(),
+               "kind": "oracle", "sample": f"oracle/lina.py on a 4^3-element grid at N={small.N}, median of 3 steps"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "model": "LinA ADER-DG-SEM acoustics (NEXT-3)", "order": cfg.N + 1,
+                   "elements": E, "grid": f"{cfg.nx}x{cfg.ny}x{cfg.nz} periodic cuboids", "dt": cfg.dt,
+                   "l2": "inputs larger than L2 (DOFs %.1f GB), no flush" % (qbytes / 1e9)},
+        "nz_flops_per_element": flops, "nz_gflops": value * flops / 1e9,
+        "roofline": {"bound": "alu", "achieved": round(ach, 3), "peak": round(FP64_PEAK_TFLOPS, 2),
+                     "unit": "TFLOP/s", "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": None,
+                     "kernel": "lina_local+lina_flux (whole step)", "peak_source": PEAK_SOURCE,
+                     "alg_hbm_gbs": round(value * abytes / 1e9, 1), "alg_bytes_per_element": abytes},
+        "cpu_baseline": cpu,
+        "e2e": {"value": E * cfg.steps / (min(e2e) / 1e3), "unit": UNIT, "h2d_bytes_per_step": qbytes / cfg.steps,
+                "d2h_bytes_per_step": qbytes / cfg.steps, "steps_per_call": cfg.steps},
+        "gpu_launches": 2 * args.steps, "clocks": clocks, "finite": bool(np.isfinite(probe).all()),
+    }
+    print(json.dumps(line), flush=True)
+    ydg.lina_destroy(h)
+    return 0
+
+
 def main():
     args = parse()
     world_env = os.environ.get("WORLD_SIZE")
@@ -484,6 +570,11 @@ def main():
     if world_env is not None and int(world_env) != args.gpus:
         print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world_env}"}), flush=True)
         return 2
+    if args.config.startswith("lina"):
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "the reference arm times the c-configs"}))
+            return 0
+        return run_lina(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ydg(args)

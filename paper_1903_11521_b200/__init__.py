@@ -32,7 +32,10 @@ YDG_OK, YDG_ERR_ARG, YDG_ERR_STATE, YDG_ERR_CUDA, YDG_ERR_NCCL, YDG_ERR_MESH, YD
 EXPORTS = ("ydg_create", "ydg_last_error", "ydg_set_comm", "ydg_set_simulations", "ydg_upload_mesh", "ydg_upload_dofs",
            "ydg_upload_dofs_device", "ydg_download_dofs_device", "ydg_step", "ydg_step_graph", "ydg_synchronize",
            "ydg_download_dofs", "ydg_get_neighbours", "ydg_halo_plan", "ydg_profile", "ydg_query",
-           "ydg_error_string", "ydg_destroy")
+           "ydg_error_string", "ydg_destroy",
+           # LinA workload (include/ydg_lina.h)
+           "ydg_lina_create", "ydg_lina_upload_grid", "ydg_lina_upload_dofs", "ydg_lina_download_dofs",
+           "ydg_lina_step", "ydg_lina_query", "ydg_lina_error_string", "ydg_lina_destroy")
 
 
 class YdgError(RuntimeError):
@@ -72,6 +75,16 @@ def lib():
         L.ydg_error_string.restype = ctypes.c_char_p
         L.ydg_destroy.argtypes = [vp]
         L.ydg_destroy.restype = None
+        L.ydg_lina_create.argtypes = [i32, i32, i32, ctypes.POINTER(vp)]
+        L.ydg_lina_upload_grid.argtypes = [vp, i32, i32, i32, vp, vp]
+        L.ydg_lina_upload_dofs.argtypes = [vp, i64, i64, vp]
+        L.ydg_lina_download_dofs.argtypes = [vp, i64, i64, vp]
+        L.ydg_lina_step.argtypes = [vp, dbl, i32, vp]
+        L.ydg_lina_query.argtypes = [vp, i32, ctypes.POINTER(dbl)]
+        L.ydg_lina_error_string.argtypes = [vp]
+        L.ydg_lina_error_string.restype = ctypes.c_char_p
+        L.ydg_lina_destroy.argtypes = [vp]
+        L.ydg_lina_destroy.restype = None
         _lib = L
     return _lib
 
@@ -217,4 +230,75 @@ def ydg_query(h, what):
 def ydg_destroy(h):
     if h.ptr:
         lib().ydg_destroy(h.ptr)
+        h.ptr = None
+
+
+# ---------------------------------------------------------------- LinA (include/ydg_lina.h)
+
+LINA_Q_ELEMENTS, LINA_Q_NZ_FLOPS, LINA_Q_ALG_BYTES, LINA_Q_DEVICE_BYTES, LINA_Q_LAUNCHES = range(5)
+
+
+class LinaHandle:
+    """Owns a ydg_lina*: ADER-DG-SEM acoustics on a uniform periodic cuboid grid."""
+
+    def __init__(self, ptr, order):
+        self.ptr, self.N = ptr, order
+        self.n = order + 1
+        self.E = 0
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            lina_destroy(self)
+
+
+def _lcheck(h, rc):
+    if rc != YDG_OK:
+        raise YdgError(rc, lib().ydg_lina_error_string(h.ptr).decode())
+
+
+def lina_create(order, precision=8, device=0):
+    out = ctypes.c_void_p()
+    rc = lib().ydg_lina_create(order, precision, device, ctypes.byref(out))
+    if rc != YDG_OK:
+        raise YdgError(rc, "ydg_lina_create")
+    return LinaHandle(out.value, order)
+
+
+def lina_upload_grid(h, nx, ny, nz, hxyz, material):
+    hh, ph = _c(hxyz, np.float64)
+    m, pm = _c(material, np.float64)
+    if hh.shape != (3,) or m.shape != (nx * ny * nz, 2):
+        raise ValueError(f"h {hh.shape} (want (3,)), material {m.shape} (want ({nx * ny * nz}, 2))")
+    _lcheck(h, lib().ydg_lina_upload_grid(h.ptr, nx, ny, nz, ph, pm))
+    h.E = nx * ny * nz
+
+
+def lina_upload_dofs(h, first, Q):
+    q, pq = _c(Q, np.float64)
+    n = h.n
+    if q.ndim != 5 or q.shape[1:] != (4, n, n, n):
+        raise ValueError(f"Q shape {q.shape}, want (count, 4, {n}, {n}, {n})")
+    _lcheck(h, lib().ydg_lina_upload_dofs(h.ptr, first, q.shape[0], pq))
+
+
+def lina_download_dofs(h, first, count):
+    n = h.n
+    out = np.empty((count, 4, n, n, n), dtype=np.float64)
+    _lcheck(h, lib().ydg_lina_download_dofs(h.ptr, first, count, out.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
+def lina_step(h, dt, nsteps=1, stream=None):
+    _lcheck(h, lib().ydg_lina_step(h.ptr, float(dt), int(nsteps), ctypes.c_void_p(stream)))
+
+
+def lina_query(h, what):
+    v = ctypes.c_double()
+    _lcheck(h, lib().ydg_lina_query(h.ptr, what, ctypes.byref(v)))
+    return v.value
+
+
+def lina_destroy(h):
+    if h.ptr:
+        lib().ydg_lina_destroy(h.ptr)
         h.ptr = None

@@ -29,7 +29,7 @@ CXXFLAGS += [f for f in os.environ.get("YDG_NVFLAGS", "").split() if f.startswit
 
 
 def sources():
-    cu = [os.path.join(CSRC, f) for f in ("kernels.cu", "halo.cu", "generic.cu", "visco.cu")]
+    cu = [os.path.join(CSRC, f) for f in ("kernels.cu", "halo.cu", "generic.cu", "visco.cu", "lina.cu")]
     cu += [os.path.join(CSRC, "generated", f"kernels_N{n}.cu") for n in range(1, 7)]
     cpp = [os.path.join(CSRC, f) for f in ("setup.cpp", "api.cpp")]
     return cu, cpp

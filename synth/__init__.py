@@ -230,3 +230,61 @@ def dofs(cfg: Config, first=0, count=None, out=None, threads=None):
     flat = uniform_range(cfg.seed, STREAM_DOFS, first * cfg.P * cfg.B, n, -1.0, 1.0,
                          out=None if out is None else out.reshape(-1), threads=threads)
     return flat.reshape(E, cfg.P, cfg.B)
+
+
+# ---- LinA (NEXT-3): ADER-DG-SEM acoustics on a uniform periodic grid of cuboids
+STREAM_LINA_MAT = 5
+STREAM_LINA_DOFS = 6
+
+
+@dataclass(frozen=True)
+class LinaConfig:
+    name: str
+    N: int            # polynomial degree per axis (order N+1 <= 8)
+    nx: int
+    ny: int
+    nz: int
+    steps: int
+    h: tuple = (1.0, 1.0, 1.0)
+    seed: int = 0
+
+    @property
+    def n_elements(self):
+        return self.nx * self.ny * self.nz
+
+    @property
+    def c_max(self):
+        return math.sqrt(1e10 / 1000.0)
+
+    @property
+    def dt(self):
+        # well inside the ADER-DG-SEM stability bound ~ h / (c (2N+1) d)
+        return 0.2 * min(self.h) / (self.c_max * (2 * self.N + 1) * 3)
+
+    def with_(self, **kw):
+        return LinaConfig(**{**self.__dict__, **kw})
+
+
+# LinA's paper runs orders 8-32 in 2D/3D; here 3D order 8 on 64^3 elements
+LINA_CONFIGS = {
+    "lina": LinaConfig("lina", 7, 64, 64, 64, 10),
+    "lina-small": LinaConfig("lina-small", 3, 4, 3, 5, 2),
+}
+
+
+def lina_material(cfg: LinaConfig):
+    """(E, 2) = (rho ~ U[1000, 3000], K ~ U[1e9, 1e10]) per element."""
+    e = np.arange(cfg.n_elements, dtype=np.uint64)
+    rho = uniform(cfg.seed, STREAM_LINA_MAT, 2 * e, 1000.0, 3000.0)
+    K = uniform(cfg.seed, STREAM_LINA_MAT, 2 * e + np.uint64(1), 1e9, 1e10)
+    return np.stack([rho, K], axis=1)
+
+
+def lina_dofs(cfg: LinaConfig, first=0, count=None):
+    """Q in the ABI layout (count, 4, n, n, n): p ~ U[-1e6, 1e6] (Pa), velocities U[-1, 1]."""
+    E = cfg.n_elements if count is None else count
+    n = cfg.N + 1
+    flat = uniform_range(cfg.seed, STREAM_LINA_DOFS, first * 4 * n ** 3, E * 4 * n ** 3, -1.0, 1.0)
+    Q = flat.reshape(E, 4, n, n, n)
+    Q[:, 0] *= 1e6
+    return Q
