@@ -13,7 +13,7 @@
 // nonzeros per axis (p <- u_a, u_a <- p), so a derivative needs six directional derivative
 // fields (d_a p, d_a u_a), each written straight into its output quantity.
 // Shared layout: quantity-major, node (x, y, z) at x*XS + y*YS + z with YS = N+2,
-// XS = (N+1) YS + 1 (conflict-light pencils along every axis).
+// XS = (N+1) YS (conflict-free y- and z-pencils at N+1 = 8).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -51,7 +51,9 @@ struct Params {
 template <int N>
 struct Lay {
   static constexpr int n = N + 1, NN = n * n * n;
-  static constexpr int YS = n + 1, XS = n * YS + 1, NNP = n * XS;  // padded node space
+  // padded node space: YS odd and XS = 8 (mod 16) make the z- and y-pencil loads of a
+  // half-warp hit 16 distinct double banks at n = 8
+  static constexpr int YS = n + 1, XS = n * YS, NNP = n * XS;
   static constexpr int BUF = 4 * NNP;                               // one 4-quantity tensor
   static constexpr int SMEM = 3 * BUF;                              // D, Dn, I (doubles)
   __device__ static int node(int x, int y, int z) { return x * XS + y * YS + z; }
@@ -59,9 +61,20 @@ struct Lay {
 
 // Out_{target} (=|+=) coef * sum_l M[k][l] S_{src}(pencil along axis a), for the pencil
 // task t in [0, n^2): (u, v) = the other two axes.  ACC: add instead of store.
-template <int N, int AXIS, bool ACC>
-__device__ __forceinline__ void pencil(const double* __restrict__ S, double* __restrict__ Out, const double* M,
-                                       int t, double coef) {
+template <int N, int MAT>
+__device__ __forceinline__ double mat(int k, int l) {
+  // constant-cache load at the use (volatile: fewer matrix entries are kept live across the
+  // element loop than with plain __constant__ reads: 76 vs 328 bytes of spills at N = 7)
+  const double* p = (MAT == 0 ? c_kt[N] : c_kh[N]) + k * (N + 1) + l;
+  unsigned long long a;
+  asm("cvta.to.const.u64 %0, %1;" : "=l"(a) : "l"(p));
+  double v;
+  asm volatile("ld.const.f64 %0, [%1];" : "=d"(v) : "l"(a));
+  return v;
+}
+template <int N, int AXIS, bool ACC, int MAT>
+__device__ __forceinline__ void pencil(const double* __restrict__ S, double* __restrict__ Out, int t, double coef,
+                                       double* __restrict__ Iacc = nullptr, double f = 0.0) {
   using L = Lay<N>;
   constexpr int n = L::n;
   const int u = t / n, v = t % n;
@@ -76,10 +89,11 @@ __device__ __forceinline__ void pencil(const double* __restrict__ S, double* __r
   for (int k = 0; k < n; ++k) {
     double s = 0.0;
 #pragma unroll
-    for (int l = 0; l < n; ++l) s = fma(M[k * n + l], in[l], s);
+    for (int l = 0; l < n; ++l) s = fma(mat<N, MAT>(k, l), in[l], s);
     double* o = Out + base + k * stride;
-    if (ACC) *o = fma(coef, s, *o);
-    else *o = coef * s;
+    const double r = ACC ? fma(coef, s, *o) : coef * s;
+    *o = r;
+    if (Iacc) Iacc[base + k * stride] = fma(f, r, Iacc[base + k * stride]);  // final value: I += f D
   }
 }
 
@@ -87,32 +101,34 @@ __device__ __forceinline__ void pencil(const double* __restrict__ S, double* __r
 //   Out_p = sum_a A*_a[0][1+a] (M_a S_{u_a}),   Out_{u_a} = A*_a[1+a][0] (M_a S_p).
 // Three phases (one per axis); 2 n^2 pencil tasks per phase; barriers between phases
 // (Out_p is accumulated).
-template <int N>
-__device__ __forceinline__ void apply3(const double* S, double* Out, const double* M, const double (&c)[3][2],
-                                       int tid) {
+template <int N, int MAT>
+__device__ __forceinline__ void apply3(const double* S, double* Out, const double (&c)[3][2], int tid,
+                                       double* I = nullptr, double f = 0.0) {
   using L = Lay<N>;
   constexpr int n2 = L::n * L::n;
   const double* Sp = S;
   double* Op = Out;
+  // I != nullptr: also I += f Out for every value once it is final (u after x, v after y,
+  // p and w after z)
   for (int t = tid; t < 2 * n2; t += kT) {  // axis x: d_x p -> u, d_x u -> p (store)
-    if (t < n2) pencil<N, 0, false>(Sp, Out + 1 * L::NNP, M, t, c[0][1]);
-    else pencil<N, 0, false>(S + 1 * L::NNP, Op, M, t - n2, c[0][0]);
+    if (t < n2) pencil<N, 0, false, MAT>(Sp, Out + 1 * L::NNP, t, c[0][1], I ? I + 1 * L::NNP : nullptr, f);
+    else pencil<N, 0, false, MAT>(S + 1 * L::NNP, Op, t - n2, c[0][0]);
   }
   __syncthreads();
   for (int t = tid; t < 2 * n2; t += kT) {  // axis y: d_y p -> v, d_y v -> p (+=)
-    if (t < n2) pencil<N, 1, false>(Sp, Out + 2 * L::NNP, M, t, c[1][1]);
-    else pencil<N, 1, true>(S + 2 * L::NNP, Op, M, t - n2, c[1][0]);
+    if (t < n2) pencil<N, 1, false, MAT>(Sp, Out + 2 * L::NNP, t, c[1][1], I ? I + 2 * L::NNP : nullptr, f);
+    else pencil<N, 1, true, MAT>(S + 2 * L::NNP, Op, t - n2, c[1][0]);
   }
   __syncthreads();
   for (int t = tid; t < 2 * n2; t += kT) {  // axis z: d_z p -> w, d_z w -> p (+=)
-    if (t < n2) pencil<N, 2, false>(Sp, Out + 3 * L::NNP, M, t, c[2][1]);
-    else pencil<N, 2, true>(S + 3 * L::NNP, Op, M, t - n2, c[2][0]);
+    if (t < n2) pencil<N, 2, false, MAT>(Sp, Out + 3 * L::NNP, t, c[2][1], I ? I + 3 * L::NNP : nullptr, f);
+    else pencil<N, 2, true, MAT>(S + 3 * L::NNP, Op, t - n2, c[2][0], I, f);
   }
   __syncthreads();
 }
 
 template <int N>
-__global__ void __launch_bounds__(kT) lina_local(const __grid_constant__ Params prm) {
+__global__ void __launch_bounds__(kT, 3) lina_local(const __grid_constant__ Params prm) {
   using L = Lay<N>;
   constexpr int n = L::n, NN = L::NN;
   extern __shared__ __align__(16) double sm[];
@@ -120,8 +136,6 @@ __global__ void __launch_bounds__(kT) lina_local(const __grid_constant__ Params 
   double* Dn = sm + L::BUF;
   double* I = sm + 2 * L::BUF;
   const int tid = threadIdx.x;
-  const double* Kt = c_kt[N];
-  const double* Kh = c_kh[N];
   for (int64_t e = blockIdx.x; e < prm.ne; e += gridDim.x) {
     const double* Qe = prm.Q + e * 4 * NN;
     for (int i = tid; i < 4 * NN; i += kT) {
@@ -140,20 +154,12 @@ __global__ void __launch_bounds__(kT) lina_local(const __grid_constant__ Params 
     double* cur = D;
     double* nxt = Dn;
     for (int d = 0; d < N; ++d) {  // CK recursion and time integral
-      apply3<N>(cur, nxt, Kt, c, tid);
-      const double f = prm.tfac[d];
-      for (int i = tid; i < 4 * NN; i += kT) {
-        const int q = i / NN, r = i % NN, s = q * L::NNP + L::node(r / (n * n), (r / n) % n, r % n);
-        I[s] = fma(f, nxt[s], I[s]);
-      }
+      apply3<N, 0>(cur, nxt, c, tid, I, prm.tfac[d]);
       double* t = cur;
       cur = nxt;
       nxt = t;
-      // (no barrier needed: the next apply3 only reads cur after its own loads, and the
-      // I update reads nxt == the buffer apply3 wrote before its final barrier)
     }
-    __syncthreads();
-    apply3<N>(I, nxt, Kh, c, tid);  // volume into nxt
+    apply3<N, 1>(I, nxt, c, tid);  // volume into nxt
     // Q* = Q + volume; sides of I -> traces
     double* Qw = prm.Q + e * 4 * NN;
     for (int i = tid; i < 4 * NN; i += kT) {
@@ -232,7 +238,7 @@ struct ydg_lina {
   double* aflux = nullptr;
   int32_t* nb = nullptr;
   size_t bytes = 0;
-  int grid = 0;
+  int grid = 0, grid_flux = 0;
 };
 
 namespace {
@@ -470,10 +476,13 @@ int ydg_lina_upload_grid(ydg_lina* h, int nx, int ny, int nz, const double* hxyz
   LCUDA(h, cudaMemcpy(h->aflux, aflux.data(), aflux.size() * sizeof(double), cudaMemcpyHostToDevice));
   LCUDA(h, cudaMemcpy(h->nb, nb.data(), nb.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   LCUDA(h, cudaFuncSetAttribute(local_fn(h->N), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_of(h->N))));
-  int sms = 148, occ = 1;
+  LCUDA(h, cudaFuncSetAttribute(local_fn(h->N), cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  int sms = 148, occ = 1, occf = 1;
   LCUDA(h, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->dev));
   LCUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, local_fn(h->N), ydg::lina::kT, smem_of(h->N)));
+  LCUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, flux_fn(h->N), ydg::lina::kT, 0));
   h->grid = sms * std::max(1, occ);
+  h->grid_flux = sms * std::max(1, occf);  // the flux kernel is latency-bound: every resident CTA
   h->ne = E;
   return YDG_OK;
 }
@@ -508,9 +517,10 @@ int ydg_lina_step(ydg_lina* h, double dt, int nsteps, void* cuda_stream) {
   }
   void* args[] = {&p};
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(h->grid, h->ne));
+  const unsigned gridf = static_cast<unsigned>(std::min<int64_t>(h->grid_flux, h->ne));
   for (int k = 0; k < nsteps; ++k) {
     LCUDA(h, cudaLaunchKernel(local_fn(h->N), dim3(grid), dim3(ydg::lina::kT), args, smem_of(h->N), s));
-    LCUDA(h, cudaLaunchKernel(flux_fn(h->N), dim3(grid), dim3(ydg::lina::kT), args, 0, s));
+    LCUDA(h, cudaLaunchKernel(flux_fn(h->N), dim3(gridf), dim3(ydg::lina::kT), args, 0, s));
   }
   return YDG_OK;
 }
