@@ -55,7 +55,7 @@ struct Lay {
   // half-warp hit 16 distinct double banks at n = 8
   static constexpr int YS = n + 1, XS = n * YS, NNP = n * XS;
   static constexpr int BUF = 4 * NNP;                               // one 4-quantity tensor
-  static constexpr int SMEM = 3 * BUF;                              // D, Dn, I (doubles)
+  static constexpr int SMEM = 3 * BUF + 4 * NN;                     // D, Dn, I, next Q (doubles)
   __device__ static int node(int x, int y, int z) { return x * XS + y * YS + z; }
 };
 
@@ -82,17 +82,24 @@ __device__ __forceinline__ void pencil(const double* __restrict__ S, double* __r
   if (AXIS == 0) { base = u * L::YS + v; stride = L::XS; }
   else if (AXIS == 1) { base = u * L::XS + v; stride = L::YS; }
   else { base = u * L::XS + v * L::YS; stride = 1; }
-  double in[n];
+  double in[n], acc[n];
 #pragma unroll
   for (int l = 0; l < n; ++l) in[l] = S[base + l * stride];
+  // n independent accumulator chains (l outer): no dependent-FMA waits
+#pragma unroll
+  for (int k = 0; k < n; ++k) acc[k] = mat<N, MAT>(k, 0) * in[0];
+#pragma unroll
+  for (int l = 1; l < n; ++l)
+#pragma unroll
+    for (int k = 0; k < n; ++k) acc[k] = fma(mat<N, MAT>(k, l), in[l], acc[k]);
+  double old[n];
+  if (ACC)
+#pragma unroll
+    for (int k = 0; k < n; ++k) old[k] = Out[base + k * stride];
 #pragma unroll
   for (int k = 0; k < n; ++k) {
-    double s = 0.0;
-#pragma unroll
-    for (int l = 0; l < n; ++l) s = fma(mat<N, MAT>(k, l), in[l], s);
-    double* o = Out + base + k * stride;
-    const double r = ACC ? fma(coef, s, *o) : coef * s;
-    *o = r;
+    const double r = ACC ? fma(coef, acc[k], old[k]) : coef * acc[k];
+    Out[base + k * stride] = r;
     if (Iacc) Iacc[base + k * stride] = fma(f, r, Iacc[base + k * stride]);  // final value: I += f D
   }
 }
@@ -135,15 +142,29 @@ __global__ void __launch_bounds__(kT, 3) lina_local(const __grid_constant__ Para
   double* D = sm;
   double* Dn = sm + L::BUF;
   double* I = sm + 2 * L::BUF;
+  double* R = sm + 3 * L::BUF;  // Q of the next element, canonical order (cp.async prefetch)
   const int tid = threadIdx.x;
+  auto prefetch = [&](int64_t e) {  // 16-byte cp.async chunks of element e's Q into R
+    const double* src = prm.Q + e * 4 * NN;
+    for (int c = tid; c < 2 * NN; c += kT)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(R + 2 * c))),
+                   "l"(src + 2 * c)
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (blockIdx.x < prm.ne) prefetch(blockIdx.x);
   for (int64_t e = blockIdx.x; e < prm.ne; e += gridDim.x) {
-    const double* Qe = prm.Q + e * 4 * NN;
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // R holds Q of element e
+#pragma unroll 4
     for (int i = tid; i < 4 * NN; i += kT) {
       const int q = i / NN, r = i % NN, x = r / (n * n), y = (r / n) % n, z = r % n;
-      const double v = Qe[i];
+      const double v = R[i];
       D[q * L::NNP + L::node(x, y, z)] = v;
       I[q * L::NNP + L::node(x, y, z)] = prm.dt * v;
     }
+    __syncthreads();  // R is free: the next element's Q streams in during this one
+    if (e + gridDim.x < prm.ne) prefetch(e + gridDim.x);
     double c[3][2];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -162,9 +183,22 @@ __global__ void __launch_bounds__(kT, 3) lina_local(const __grid_constant__ Para
     apply3<N, 1>(I, nxt, c, tid);  // volume into nxt
     // Q* = Q + volume; sides of I -> traces
     double* Qw = prm.Q + e * 4 * NN;
-    for (int i = tid; i < 4 * NN; i += kT) {
-      const int q = i / NN, r = i % NN, s = q * L::NNP + L::node(r / (n * n), (r / n) % n, r % n);
-      Qw[i] += nxt[s];
+    constexpr int QIT = (4 * NN + kT - 1) / kT;
+    {  // Q* = Q + volume: all of the thread's Q loads in flight at once
+      double qv[QIT];
+#pragma unroll
+      for (int j = 0; j < QIT; ++j) {
+        const int i = tid + j * kT;
+        qv[j] = i < 4 * NN ? Qw[i] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < QIT; ++j) {
+        const int i = tid + j * kT;
+        if (i < 4 * NN) {
+          const int q = i / NN, r = i % NN, s = q * L::NNP + L::node(r / (n * n), (r / n) % n, r % n);
+          Qw[i] = qv[j] + nxt[s];
+        }
+      }
     }
     double* Te = prm.traces + e * 6 * 4 * n * n;
     for (int i = tid; i < 6 * 4 * n * n; i += kT) {
