@@ -62,7 +62,8 @@ enum {
   YDG_Q_KERNEL_PATH = 16,      /* kernels a step runs: 0 fp64 elastic tensor-core (dm_local/
                                   dm_flux), 1 fp32 sparse FFMA (ader_*), 2 viscoelastic
                                   tensor-core (vm_local/vm_neigh), 3 generic CSR (gen_*)    */
-  YDG_Q_SIMULATIONS = 17       /* fused simulations S (ydg_set_simulations)                 */
+  YDG_Q_SIMULATIONS = 17,      /* fused simulations S (ydg_set_simulations)                 */
+  YDG_Q_TILE_ELEMENTS = 18     /* elements per tile of the tiled kernels (16 fp64, 32 fp32) */
 };
 
 typedef struct ydg_solver ydg_solver; /* opaque, owned by the library */
@@ -135,6 +136,19 @@ int ydg_step(ydg_solver* h, double dt, int nsteps, void* cuda_stream);
  * steps are launch-latency bound (BASELINE configs[0]: 384 elements).  One rank only
  * (YDG_ERR_UNSUPPORTED otherwise); profiling must be off (YDG_ERR_STATE). */
 int ydg_step_graph(ydg_solver* h, double dt, int nsteps, void* cuda_stream);
+
+/* Optional, before ydg_upload_mesh: two-cluster local time stepping (the paper's LTS of
+ * Table loh1; scheme = reading R26 of DESIGN.md, rate 2).  cluster[n] per
+ * element (caller numbering): 0 advances by dt, 1 by 2 dt.  The number of 1s must be a
+ * multiple of YDG_Q_TILE_ELEMENTS (every launch covers whole tiles of one cluster).  fp64
+ * elastic tensor-core path on one rank (YDG_ERR_UNSUPPORTED otherwise, at upload). */
+int ydg_set_clusters(ydg_solver* h, const int8_t* cluster, int64_t n);
+
+/* One LTS cycle takes every element from t to t + 2 dt: coarse sub-interval traces, coarse
+ * local update (2 dt), two fine substeps (local + flux with the coarse neighbours' traces of
+ * the matching half interval), then the coarse flux with the sum of the fine substeps'
+ * traces.  ncycles cycles, enqueued on cuda_stream (NULL = the handle's stream). */
+int ydg_step_lts(ydg_solver* h, double dt, int ncycles, void* cuda_stream);
 
 /* Block until all work of the handle has finished. */
 int ydg_synchronize(ydg_solver* h);

@@ -27,10 +27,10 @@ YDG_OK, YDG_ERR_ARG, YDG_ERR_STATE, YDG_ERR_CUDA, YDG_ERR_NCCL, YDG_ERR_MESH, YD
 (YDG_Q_N_ELEMENTS, YDG_Q_FIRST_LOCAL, YDG_Q_N_LOCAL, YDG_Q_NZ_FLOPS, YDG_Q_ALG_BYTES, YDG_Q_B,
  YDG_Q_BTILDE, YDG_Q_DEVICE_BYTES, YDG_Q_LAUNCHES_PER_STEP, YDG_Q_LOCAL_BYTES, YDG_Q_NEIGH_BYTES,
  YDG_Q_LOCAL_FLOPS, YDG_Q_NEIGH_FLOPS, YDG_Q_PROF_LOCAL_MS, YDG_Q_PROF_NEIGH_MS,
- YDG_Q_PROF_LAUNCHES, YDG_Q_KERNEL_PATH, YDG_Q_SIMULATIONS) = range(18)
+ YDG_Q_PROF_LAUNCHES, YDG_Q_KERNEL_PATH, YDG_Q_SIMULATIONS, YDG_Q_TILE_ELEMENTS) = range(19)
 
 EXPORTS = ("ydg_create", "ydg_last_error", "ydg_set_comm", "ydg_set_simulations", "ydg_upload_mesh", "ydg_upload_dofs",
-           "ydg_upload_dofs_device", "ydg_download_dofs_device", "ydg_step", "ydg_step_graph", "ydg_synchronize",
+           "ydg_upload_dofs_device", "ydg_download_dofs_device", "ydg_step", "ydg_step_graph", "ydg_set_clusters", "ydg_step_lts", "ydg_synchronize",
            "ydg_download_dofs", "ydg_get_neighbours", "ydg_halo_plan", "ydg_profile", "ydg_query",
            "ydg_error_string", "ydg_destroy",
            # LinA workload (include/ydg_lina.h)
@@ -65,6 +65,8 @@ def lib():
         L.ydg_download_dofs_device.argtypes = [vp, i64, i64, vp, vp]
         L.ydg_step.argtypes = [vp, dbl, i32, vp]
         L.ydg_step_graph.argtypes = [vp, dbl, i32, vp]
+        L.ydg_set_clusters.argtypes = [vp, vp, i64]
+        L.ydg_step_lts.argtypes = [vp, dbl, i32, vp]
         L.ydg_synchronize.argtypes = [vp]
         L.ydg_download_dofs.argtypes = [vp, i64, i64, vp]
         L.ydg_get_neighbours.argtypes = [vp, i64, i64, vp, vp, vp]
@@ -166,6 +168,15 @@ def ydg_step(h, dt, nsteps=1, stream=None):
 
 def ydg_step_graph(h, dt, nsteps=1, stream=None):
     _check(h, lib().ydg_step_graph(h.ptr, float(dt), int(nsteps), ctypes.c_void_p(stream)))
+
+
+def ydg_set_clusters(h, cluster):
+    c, pc = _c(cluster, np.int8)
+    _check(h, lib().ydg_set_clusters(h.ptr, pc, c.size))
+
+
+def ydg_step_lts(h, dt, ncycles=1, stream=None):
+    _check(h, lib().ydg_step_lts(h.ptr, float(dt), int(ncycles), ctypes.c_void_p(stream)))
 
 
 def ydg_synchronize(h):

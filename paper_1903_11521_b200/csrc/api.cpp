@@ -72,6 +72,14 @@ struct ydg_solver {
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t gexec = nullptr;
   int sims = 1;  // fused simulations (element-simulations v = e * sims + s)
+  // two-cluster local time stepping (ydg_set_clusters / ydg_step_lts, reading R26)
+  std::vector<int8_t> cluster_ext;  // caller numbering; empty = global time stepping
+  bool lts = false;
+  int64_t lts_nc = 0;          // coarse elements = internal [0, lts_nc), a multiple of the tile width
+  int64_t lts_ncb_tiles = 0;   // tiles covering the coarse elements with a fine neighbour
+  int32_t* nb_lts[3] = {nullptr, nullptr, nullptr};  // flux neighbour slots: fine sub 1, fine sub 2, coarse
+  int64_t* lts_lst[3] = {nullptr, nullptr, nullptr};  // combine lists: S1 = own, S2 = own - S1, B (=|+=) own
+  int64_t lts_n[3] = {0, 0, 0};
   double g_dt = 0;
   int g_n = -1;
 };
@@ -103,7 +111,10 @@ int trace_block(const ydg_solver* h) { return h->prec == 8 ? (h->Bt * h->P + 1) 
 
 void free_mesh(ydg_solver* h) {
   for (void** p : {&h->Q, &h->traces, &h->star, &h->aplus, &h->aminus, &h->staging, &h->src,
-                   reinterpret_cast<void**>(&h->slot_of),
+                   reinterpret_cast<void**>(&h->slot_of), reinterpret_cast<void**>(&h->nb_lts[0]),
+                   reinterpret_cast<void**>(&h->nb_lts[1]), reinterpret_cast<void**>(&h->nb_lts[2]),
+                   reinterpret_cast<void**>(&h->lts_lst[0]), reinterpret_cast<void**>(&h->lts_lst[1]),
+                   reinterpret_cast<void**>(&h->lts_lst[2]),
                    reinterpret_cast<void**>(&h->nb), reinterpret_cast<void**>(&h->jh),
                    reinterpret_cast<void**>(&h->nb64), reinterpret_cast<void**>(&h->jh_e)}) {
     if (*p) cudaFree(*p);
@@ -111,6 +122,7 @@ void free_mesh(ydg_solver* h) {
   }
   h->device_bytes = 0;
   h->have_mesh = false;
+  h->lts = false;
   if (h->gexec) cudaGraphExecDestroy(h->gexec);  // captured the old buffers
   h->gexec = nullptr;
   h->g_n = -1;
@@ -700,8 +712,32 @@ static int upload_mesh_impl(ydg_solver* h, int64_t ne, const double* xyz, const 
   // so it is off by default (the kernels are latency-, not DRAM-bound).
   std::vector<int64_t> ext_of;
   const char* ro = std::getenv("YDG_REORDER");
-  if (!h->generic && ro && ro[0] == '1') {
+  if (!h->cluster_ext.empty()) {
+    // LTS: coarse elements with a fine neighbour, the other coarse elements, then the fine
+    // ones (caller order within each class), so that every launch of a cycle covers one
+    // contiguous tile range
+    if (h->generic || h->prec != 8 || h->nranks > 1)
+      return fail(h, YDG_ERR_UNSUPPORTED, "local time stepping runs on the fp64 elastic tensor-core path, one rank");
+    if (static_cast<int64_t>(h->cluster_ext.size()) != ne) return fail(h, YDG_ERR_ARG, "cluster array size != elements");
+    std::vector<int64_t> cb, ci, fi;
+    for (int64_t e = 0; e < ne; ++e) {
+      if (h->cluster_ext[e] == 0) { fi.push_back(e); continue; }
+      bool bnd = false;
+      for (int i = 0; i < 4; ++i) bnd |= h->cluster_ext[nbr.nb[e * 4 + i]] == 0;
+      (bnd ? cb : ci).push_back(e);
+    }
+    const int64_t nc = static_cast<int64_t>(cb.size() + ci.size());
+    if (nc % kDmLanes) return fail(h, YDG_ERR_ARG, "the coarse cluster must hold a multiple of the tile width (YDG_Q_TILE_ELEMENTS)");
+    ext_of = cb;
+    ext_of.insert(ext_of.end(), ci.begin(), ci.end());
+    ext_of.insert(ext_of.end(), fi.begin(), fi.end());
+    h->lts = true;
+    h->lts_nc = nc;
+    h->lts_ncb_tiles = (static_cast<int64_t>(cb.size()) + kDmLanes - 1) / kDmLanes;
+  } else if (!h->generic && ro && ro[0] == '1') {
     ext_of = locality_order(ne, xyz, nbr, h->nranks);
+  }
+  if (!ext_of.empty()) {  // internal numbering = ext_of
     std::vector<double> xyz_i(static_cast<size_t>(ne) * 12), mat_i(static_cast<size_t>(ne) * 3);
     std::vector<int64_t> vid_i(static_cast<size_t>(ne) * 4);
     for (int64_t i = 0; i < ne; ++i) {
@@ -794,6 +830,44 @@ static int upload_tiled(ydg_solver* h, const double* xyz, const double* material
         else h->bnd_hi = std::max(h->bnd_hi, h->ntiles - t);
       }
   }
+  // LTS: extra trace slots after the owned ones -- S1, S2 (the coarse element's traces of
+  // I over [0, dt] and [dt, 2 dt]) per coarse element with a fine neighbour, B (the sum of
+  // the two fine substeps' traces) per fine element with a coarse neighbour -- and the
+  // neighbour-slot tables of the three flux launches of a cycle
+  std::vector<int32_t> nbt[3];
+  std::vector<int64_t> lst[3];
+  if (h->lts) {
+    const int64_t nc = h->lts_nc;
+    std::vector<int64_t> s1(h->nlocal, -1), bslot(h->nlocal, -1);
+    int64_t next = h->nslots;
+    for (int64_t e = 0; e < h->nlocal; ++e) {
+      bool cross = false;
+      for (int i = 0; i < 4; ++i) cross |= (h->nbr.nb[e * 4 + i] < nc) != (e < nc);
+      if (!cross) continue;
+      if (e < nc) { s1[e] = next; next += 2; }
+      else bslot[e] = next++;
+    }
+    for (int64_t e = 0; e < h->nlocal; ++e) {
+      if (s1[e] >= 0) {
+        lst[0].insert(lst[0].end(), {s1[e], e, 0});
+        lst[1].insert(lst[1].end(), {s1[e] + 1, e, s1[e]});
+      }
+      if (bslot[e] >= 0) lst[2].insert(lst[2].end(), {bslot[e], e, 0});
+    }
+    h->nslots = (next + kLanes - 1) / kLanes * kLanes;
+    for (int k = 0; k < 3; ++k) nbt[k] = nb_local;
+    for (int64_t l = 0; l < h->nlocal; ++l)
+      for (int i = 0; i < 4; ++i) {
+        const int64_t n = h->nbr.nb[l * 4 + i];
+        const size_t dst = ((l / kLanes) * 4 + i) * kLanes + l % kLanes;
+        if (l >= nc && n < nc) {  // fine element, coarse neighbour: its sub-interval traces
+          nbt[0][dst] = static_cast<int32_t>(s1[n]);
+          nbt[1][dst] = static_cast<int32_t>(s1[n] + 1);
+        } else if (l < nc && n >= nc) {  // coarse element, fine neighbour: the fine sum
+          nbt[2][dst] = static_cast<int32_t>(bslot[n]);
+        }
+      }
+  }
   const int eb = elem_bytes(h);
   const size_t q_n = static_cast<size_t>(h->ntiles) * kLanes * h->P * h->B;
   const size_t tr_n = static_cast<size_t>(h->nslots) * 4 * (trace_block(h) ? trace_block(h) : h->Bt * h->P);
@@ -805,6 +879,16 @@ static int upload_tiled(ydg_solver* h, const double* xyz, const double* material
   CUDA_OR_FAIL(h, cudaMemset(h->traces, 0, tr_n * eb));
   CUDA_OR_FAIL(h, cudaMemcpy(h->nb, nb_local.data(), nb_local.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   CUDA_OR_FAIL(h, cudaMemcpy(h->jh, jh_local.data(), jh_local.size(), cudaMemcpyHostToDevice));
+  if (h->lts) {
+    for (int k = 0; k < 3; ++k) {
+      if ((rc = dalloc(h, reinterpret_cast<void**>(&h->nb_lts[k]), nbt[k].size() * sizeof(int32_t)))) { free_mesh(h); return rc; }
+      CUDA_OR_FAIL(h, cudaMemcpy(h->nb_lts[k], nbt[k].data(), nbt[k].size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+      h->lts_n[k] = static_cast<int64_t>(lst[k].size() / 3);
+      if ((rc = dalloc(h, reinterpret_cast<void**>(&h->lts_lst[k]), std::max<size_t>(1, lst[k].size()) * sizeof(int64_t)))) { free_mesh(h); return rc; }
+      if (!lst[k].empty())
+        CUDA_OR_FAIL(h, cudaMemcpy(h->lts_lst[k], lst[k].data(), lst[k].size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    }
+  }
   rc = eb == 8 ? upload_coeffs<double>(h, xyz, material, anelastic) : upload_coeffs<float>(h, xyz, material, anelastic);
   if (rc) { free_mesh(h); return rc; }
   if (h->nranks > 1) {
@@ -941,6 +1025,79 @@ int ydg_step_graph(ydg_solver* h, double dt, int nsteps, void* cuda_stream) {
   return YDG_OK;
 }
 
+int ydg_set_clusters(ydg_solver* h, const int8_t* cluster, int64_t n) {
+  int rc = check(h);
+  if (rc) return rc;
+  if (h->have_mesh) return fail(h, YDG_ERR_STATE, "ydg_set_clusters must precede ydg_upload_mesh");
+  if (!cluster || n < 0) return fail(h, YDG_ERR_ARG, "null cluster array");
+  for (int64_t e = 0; e < n; ++e)
+    if (cluster[e] != 0 && cluster[e] != 1) return fail(h, YDG_ERR_ARG, "cluster ids must be 0 (dt) or 1 (2 dt)");
+  h->cluster_ext.assign(cluster, cluster + n);
+  return YDG_OK;
+}
+
+int ydg_step_lts(ydg_solver* h, double dt, int ncycles, void* cuda_stream) {
+  int rc = check(h);
+  if (rc) return rc;
+  if (!h->have_mesh) return fail(h, YDG_ERR_STATE, "upload the mesh first");
+  if (!h->lts) return fail(h, YDG_ERR_STATE, "no clusters: call ydg_set_clusters before ydg_upload_mesh");
+  if (!(dt > 0) || !std::isfinite(dt) || ncycles < 0) return fail(h, YDG_ERR_ARG, "bad dt or ncycles");
+  cudaStream_t s = pick_stream(h, cuda_stream);
+  StepParams<double> base{};
+  base.Q = static_cast<double*>(h->Q);
+  base.traces = static_cast<double*>(h->traces);
+  base.star = static_cast<const double*>(h->star);
+  base.aplus = static_cast<const double*>(h->aplus);
+  base.jh = h->jh;
+  auto with_dt = [&](double tau) {
+    StepParams<double> p = base;
+    p.dt = tau;
+    for (int d = 0; d < h->N; ++d) {
+      p.scal[d] = tau / (d + 1);
+      p.scal[h->N + d] = tau / (d + 2);
+    }
+    return p;
+  };
+  const int64_t ntc = h->lts_nc / h->lanes, ntf = h->ntiles - ntc;
+  const int TS = trace_block(h);
+  auto local = [&](StepParams<double> p, int64_t t0, int64_t nt, int tr_only) -> int {
+    if (nt <= 0) return YDG_OK;
+    p.nb = h->nb;
+    p.tile0 = t0;
+    p.ntiles = nt;
+    p.tr_only = tr_only;
+    CUDA_OR_FAIL(h, timed(h, 0, s, [&] { return launch_local<double>(h->N, p, static_cast<int>(std::min<int64_t>(h->grid_local, nt)), s); }));
+    return YDG_OK;
+  };
+  auto flux = [&](int table, int64_t t0, int64_t nt) -> int {
+    if (nt <= 0) return YDG_OK;
+    StepParams<double> p = base;
+    p.nb = h->nb_lts[table];
+    p.tile0 = t0;
+    p.ntiles = nt;
+    CUDA_OR_FAIL(h, timed(h, 1, s, [&] { return launch_neigh<double>(h->N, p, static_cast<int>(std::min<int64_t>(h->grid_neigh, nt * (h->lanes / 8))), s); }));
+    return YDG_OK;
+  };
+  auto combine = [&](int k, int mode) -> int {
+    CUDA_OR_FAIL(h, launch_trace_combine(static_cast<double*>(h->traces), h->lts_lst[k], h->lts_n[k], TS, h->lanes, mode, s));
+    return YDG_OK;
+  };
+  const StepParams<double> p1 = with_dt(dt), p2 = with_dt(2 * dt);
+  for (int c = 0; c < ncycles; ++c) {
+    // coarse elements next to fine ones: traces of I[0, dt] -> S1 (before their update)
+    if ((rc = local(p1, 0, h->lts_ncb_tiles, 1)) || (rc = combine(0, 0))) return rc;
+    // coarse: traces of I[0, 2 dt], volume update; S2 = I[0, 2dt] - I[0, dt] traces
+    if ((rc = local(p2, 0, ntc, 0)) || (rc = combine(1, 1))) return rc;
+    // fine substep 1: local (dt), B = own traces, flux with the coarse S1
+    if ((rc = local(p1, ntc, ntf, 0)) || (rc = combine(2, 0)) || (rc = flux(0, ntc, ntf))) return rc;
+    // fine substep 2: local (dt) from the updated Q, B += own traces, flux with S2
+    if ((rc = local(p1, ntc, ntf, 0)) || (rc = combine(2, 2)) || (rc = flux(1, ntc, ntf))) return rc;
+    // coarse flux over 2 dt: coarse neighbours' full traces, fine neighbours' B
+    if ((rc = flux(2, 0, ntc))) return rc;
+  }
+  return YDG_OK;
+}
+
 int ydg_synchronize(ydg_solver* h) {
   int rc = check(h);
   if (rc) return rc;
@@ -1021,6 +1178,7 @@ int ydg_query(ydg_solver* h, int what, double* v) {
     case YDG_Q_PROF_NEIGH_MS: *v = h->prof_ms[1]; break;
     case YDG_Q_PROF_LAUNCHES: *v = static_cast<double>(h->prof_launches); break;
     case YDG_Q_SIMULATIONS: *v = static_cast<double>(h->sims); break;
+    case YDG_Q_TILE_ELEMENTS: *v = static_cast<double>(h->prec == 8 ? kDmLanes : kLanes); break;
     case YDG_Q_N_ELEMENTS: *v = static_cast<double>(h->ne); break;
     case YDG_Q_FIRST_LOCAL: *v = static_cast<double>(h->first); break;
     case YDG_Q_N_LOCAL: *v = static_cast<double>(h->nlocal); break;

@@ -762,6 +762,11 @@ __global__ void __launch_bounds__(kT * kLocalGroups, kLocalGroups == 1 ? kDmCtas
       if (x.tid == 0) bulk_s2g(gtr + F * Lay::FACE, stg, Lay::FACE * sizeof(double));
     }
     YDG_PHASE(8);
+    if (prm.tr_only) {  // LTS: the sub-interval traces of a coarse element, no update
+      if (x.tid == 0) bulk_wait_read<0>();
+      x.sync();
+      continue;
+    }
     if (x.tid == 0) bulk_wait_read<0>();
     x.sync();  // the staging blocks overlap the X buffers of the volume term
     if (x.tid == 0) {  // rows < IROWS of Q^n -> S (free now) for the volume's update

@@ -73,6 +73,23 @@ __global__ void to_canonical_kernel(int P, int B, int L, const T* __restrict__ t
   }
 }
 
+// LTS trace bookkeeping: for every entry k, over the 4 faces of element slots: mode 0:
+// dst = a; mode 1: dst = a - b; mode 2: dst += a.  Traces layout [tile][face][lane][TS].
+__global__ void trace_combine_kernel(double* __restrict__ tr, const int64_t* __restrict__ lst, int64_t n, int TS,
+                                     int L, int mode) {
+  const int64_t total = n * 4 * TS;
+  auto at = [&](int64_t s, int F, int v) { return (((s / L) * 4 + F) * L + (s % L)) * (int64_t)TS + v; };
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i / (4 * TS);
+    const int F = static_cast<int>((i / TS) % 4), v = static_cast<int>(i % TS);
+    const int64_t d = lst[3 * k], a = lst[3 * k + 1], b = lst[3 * k + 2];
+    const double va = tr[at(a, F, v)];
+    if (mode == 0) tr[at(d, F, v)] = va;
+    else if (mode == 1) tr[at(d, F, v)] = va - tr[at(b, F, v)];
+    else tr[at(d, F, v)] += va;
+  }
+}
+
 const void* pick_local(int N, int eb) {
   switch (N) {
     case 1: return local_fn_N1(eb);
@@ -163,6 +180,12 @@ cudaError_t launch_neigh(int N, const StepParams<T>& p, int grid, cudaStream_t s
   // fp64: grid counts 3-warp groups (virtual CTAs); kFluxGroups of them share one CTA
   const int ctas = sizeof(T) == 8 ? (grid + kFluxGroups - 1) / kFluxGroups : grid;
   return cudaLaunchKernel(f, dim3(ctas), dim3(flux_threads(sizeof(T))), args, neigh_smem_bytes(N, sizeof(T)), s);
+}
+cudaError_t launch_trace_combine(double* traces, const int64_t* lst, int64_t n, int TS, int L, int mode,
+                                 cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  trace_combine_kernel<<<148 * 4, 256, 0, s>>>(traces, lst, n, TS, L, mode);
+  return cudaGetLastError();
 }
 template <typename T>
 cudaError_t launch_to_tiled(int P, int B, int L, const T* canon, T* tiled, int64_t first, int64_t count,

@@ -44,6 +44,7 @@ struct StepParams {
   int64_t ntiles;        // number of tiles handled
   T scal[2 * kMaxN];     // dt/(d+1), d < N ; dt/(d+2), d < N
   T dt;
+  int tr_only;           // fp64 local kernel: traces of I only, no volume update (LTS)
 };
 
 // host launchers (kernels.cu)
@@ -57,6 +58,10 @@ cudaError_t launch_to_tiled(int P, int B, int L, const T* canon, T* tiled, int64
 template <typename T>
 cudaError_t launch_to_canonical(int P, int B, int L, const T* tiled, T* canon, int64_t first,
                                 int64_t count, const int32_t* slot_of, cudaStream_t s);
+// LTS: per entry (dst, a, b) element slots, all four faces: mode 0 dst = a, 1 dst = a - b,
+// 2 dst += a (fp64 trace layout [tile][face][lane][TS])
+cudaError_t launch_trace_combine(double* traces, const int64_t* lst, int64_t n, int TS, int L, int mode,
+                                 cudaStream_t s);
 size_t local_smem_bytes(int N, int elem_bytes);
 size_t sparse_local_smem(int N, int elem_bytes);
 size_t sparse_neigh_smem(int N, int elem_bytes);

@@ -281,3 +281,50 @@ def test_fused_simulations(S, prec):
     ref = ostep.step_fused(prob, np.ascontiguousarray(Qs.transpose(0, 1, 3, 2)), cfg.dt, 2).transpose(0, 1, 3, 2)
     for s in range(S):
         check_parity(rel_err(got[s], ref[s]), prec, f"fused S={S} s={s}")
+
+
+def _lts_clusters(cfg, xyz):
+    """Elements of the upper half (centroid z >= nz/2) coarse: whole z-layers of cubes, so
+    the coarse count is a multiple of the tile width."""
+    return (xyz[:, :, 2].mean(1) >= cfg.nz / 2).astype(np.int8)
+
+
+@pytest.mark.parametrize("N,vperm", [(2, False), (5, True), (3, True)])
+def test_local_time_stepping(N, vperm):
+    """NEXT-2 (reading R26): two-cluster LTS cycles on the GPU (ydg_step_lts) against the
+    oracle's LTS (oracle/lts.py), including the cluster interface in both directions."""
+    import paper_1903_11521_b200 as ydg
+    from oracle import lts as olts
+    from oracle import step as ostep
+    cfg = synth.CONFIGS["c0"].with_(N=N, nx=4, ny=4, nz=4, vperm=vperm, name=f"lts-N{N}")
+    xyz, vid, mat, Q, _ = make_inputs(cfg)
+    cl = _lts_clusters(cfg, xyz)
+    assert cl.sum() % 16 == 0 and 0 < cl.sum() < len(cl)
+    dt = cfg.dt / 4
+    h = ydg.ydg_create(cfg.N, 9, 8)
+    ydg.ydg_set_clusters(h, cl)
+    ydg.ydg_upload_mesh(h, xyz, vid, mat)
+    ydg.ydg_upload_dofs(h, 0, Q)
+    ydg.ydg_step_lts(h, dt, 2)
+    got = ydg.ydg_download_dofs(h, 0, cfg.n_elements)
+    nb, j, hr = ydg.ydg_get_neighbours(h, 0, cfg.n_elements)
+    ydg.ydg_destroy(h)
+    onb, oj, oh = omesh.neighbour_table(vid)
+    assert np.array_equal(nb, onb) and np.array_equal(j, oj) and np.array_equal(hr, oh)
+    prob = ostep.setup(cfg.N, xyz, vid, mat)
+    ref = ostep.to_canonical(olts.lts(prob, ostep.to_internal(Q), dt, cl, 2))
+    check_parity(rel_err(got, ref), 8, cfg.name)
+
+
+def test_lts_rejects_ragged_coarse_cluster():
+    import paper_1903_11521_b200 as ydg
+    cfg = synth.CONFIGS["c0"]
+    xyz, vid, mat, Q, _ = make_inputs(cfg)
+    cl = np.zeros(cfg.n_elements, np.int8)
+    cl[:5] = 1
+    h = ydg.ydg_create(cfg.N, 9, 8)
+    ydg.ydg_set_clusters(h, cl)
+    with pytest.raises(ydg.YdgError) as ei:
+        ydg.ydg_upload_mesh(h, xyz, vid, mat)
+    assert ei.value.code == ydg.YDG_ERR_ARG
+    ydg.ydg_destroy(h)
