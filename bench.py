@@ -78,6 +78,10 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=8, help="cubes per axis of the oracle sample")
     ap.add_argument("--sims", type=int, default=1,
                     help="fused simulations S (NEXT-1, P:1306-1308): element-simulations = elements x S")
+    ap.add_argument("--lts", action="store_true",
+                    help="NEXT-2: two-cluster local time stepping on the config's mesh with the two-layer "
+                         "material (upper half vp in [1500, 2500] advances by 2 dt); reports GTS-equivalent "
+                         "element-updates/s and the speed-up over global time stepping on the same mesh")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="time ydg_step_graph (one CUDA graph per step); auto: on below 100k elements "
                          "(c0: launch-latency bound), 1 GPU only")
@@ -562,6 +566,75 @@ def run_lina(args):
     return 0
 
 
+def run_lts(args):
+    """LTS (NEXT-2, reading R26) vs GTS on one handle: c1's mesh and order with the two-layer
+    material; a cycle advances every element by 2 dt (= two GTS steps of dt)."""
+    import torch
+    import paper_1903_11521_b200 as ydg
+    rank, world, local = dist_setup(args)
+    if world > 1:
+        if rank == 0:
+            print(json.dumps({"error": "LTS runs on one GPU"}), flush=True)
+        return 0
+    cfg = synth.CONFIGS[args.config].with_(material="two_layer", name=args.config + "-lts")
+    if args.replica:
+        cfg = cfg.replica(args.replica)
+    xyz, vid = synth.mesh(cfg)
+    mat = synth.material(cfg)
+    cl = (xyz[:, :, 2].mean(1) >= cfg.nz / 2).astype(np.int8)  # upper half: slow layer, 2 dt
+    vp_c, vp_f = mat[cl == 1, 1].max(), mat[cl == 0, 1].max()
+    assert 2 * vp_c <= vp_f, "coarse cluster must be CFL-admissible at 2 dt"
+    h = ydg.ydg_create(cfg.N, cfg.P, cfg.precision, device=local)
+    ydg.ydg_set_clusters(h, cl)
+    ydg.ydg_upload_mesh(h, xyz, vid, mat)
+    E = cfg.n_elements
+    del xyz, vid
+    ydg.ydg_upload_dofs(h, 0, synth.dofs(cfg))
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    sptr = stream.cuda_stream
+    dt = 0.5 * cfg.dt  # fine step: the GTS step of the fast layer
+    res = {}
+    for mode in ("lts", "gts"):
+        for _ in range(args.warmup):
+            if mode == "lts":
+                ydg.ydg_step_lts(h, dt, 1, stream=sptr)
+            else:
+                ydg.ydg_step(h, dt, 2, stream=sptr)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with Clocks(local) as clk:
+            e0.record(stream)
+            for _ in range(args.steps):  # one step = 2 dt of simulated time
+                if mode == "lts":
+                    ydg.ydg_step_lts(h, dt, 1, stream=sptr)
+                else:
+                    ydg.ydg_step(h, dt, 2, stream=sptr)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        res[mode] = (e0.elapsed_time(e1), clk.summary())
+    ms, clocks = res["lts"]
+    value = 2 * E * args.steps / (ms / 1e3)
+    gts_value = 2 * E * args.steps / (res["gts"][0] / 1e3)
+    nz = ydg.ydg_query(h, ydg.YDG_Q_NZ_FLOPS)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT + " (GTS-equivalent: element x dt advanced)",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "order": cfg.N, "elements": E, "coarse_elements": int(cl.sum()),
+                   "dt_fine": dt, "step": "one LTS cycle = 2 dt of simulated time",
+                   "material": "two-layer: upper half vp in [1500, 2500] (cluster 1, 2 dt), lower [4000, 6000]",
+                   "l2": "inputs larger than L2, no flush"},
+        "gts": {"value": gts_value, "ms_per_2dt": res["gts"][0] / args.steps},
+        "lts_speedup_vs_gts": value / gts_value,
+        "nz_gflops_equivalent": value * nz / 1e9, "clocks": clocks,
+        "gpu_launches": 10 * args.steps,
+    }
+    print(json.dumps(line), flush=True)
+    ydg.ydg_destroy(h)
+    return 0
+
+
 def main():
     args = parse()
     world_env = os.environ.get("WORLD_SIZE")
@@ -570,6 +643,8 @@ def main():
     if world_env is not None and int(world_env) != args.gpus:
         print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world_env}"}), flush=True)
         return 2
+    if args.lts:
+        return run_lts(args)
     if args.config.startswith("lina"):
         if args.impl == "reference":
             print(json.dumps({"impl": "reference", "unavailable": "the reference arm times the c-configs"}))
