@@ -1,7 +1,7 @@
 """Per-window summary of an ncu --page source --csv --print-source sass export:
     python tools/sass_windows.py KERNEL_INDEX WINDOW CSV"""
 import csv, collections, re, sys
-rows = list(csv.reader(open('sys.argv[3] if len(sys.argv) > 3 else "/tmp/src_sass.csv"')))
+rows = list(csv.reader(open(sys.argv[3] if len(sys.argv) > 3 else '/tmp/src_sass.csv')))
 kern = [i for i,r in enumerate(rows) if r and r[0]=='Kernel Name']
 which = int(sys.argv[1]) if len(sys.argv)>1 else 0
 W = int(sys.argv[2]) if len(sys.argv)>2 else 300
