@@ -31,6 +31,9 @@ namespace lina {
 
 constexpr int kMaxN = 7;
 constexpr int kT = 128;  // threads per CTA
+#ifndef LINA_MINB
+#define LINA_MINB 2  // CTAs per SM of lina_local: 2 with the register-resident I (12.6 ms) beat 3 (17.9, spills)
+#endif
 
 // Kt = -Dm (reading L4), Kh = W^-1 Dm^T W (L5), per order N (row-major n x n)
 __constant__ double c_kt[kMaxN + 1][64];
@@ -72,9 +75,9 @@ __device__ __forceinline__ double mat(int k, int l) {
   asm volatile("ld.const.f64 %0, [%1];" : "=d"(v) : "l"(a));
   return v;
 }
-template <int N, int AXIS, bool ACC, int MAT>
+template <int N, int AXIS, bool ACC, int MAT, bool IR>
 __device__ __forceinline__ void pencil(const double* __restrict__ S, double* __restrict__ Out, int t, double coef,
-                                       double* __restrict__ Iacc = nullptr, double f = 0.0) {
+                                       double (&ir)[N + 1], double f) {
   using L = Lay<N>;
   constexpr int n = L::n;
   const int u = t / n, v = t % n;
@@ -100,42 +103,76 @@ __device__ __forceinline__ void pencil(const double* __restrict__ S, double* __r
   for (int k = 0; k < n; ++k) {
     const double r = ACC ? fma(coef, acc[k], old[k]) : coef * acc[k];
     Out[base + k * stride] = r;
-    if (Iacc) Iacc[base + k * stride] = fma(f, r, Iacc[base + k * stride]);  // final value: I += f D
+    if (IR) ir[k] = fma(f, r, ir[k]);  // the value is final: I += f D (registers)
   }
+}
+
+// node offset of pencil task t of `axis` at position k along it (the pencil() addressing)
+template <int N, int AXIS>
+__device__ __forceinline__ int pencil_node(int t, int k) {
+  using L = Lay<N>;
+  const int u = t / L::n, v = t % L::n;
+  if (AXIS == 0) return u * L::YS + v + k * L::XS;
+  if (AXIS == 1) return u * L::XS + v + k * L::YS;
+  return u * L::XS + v * L::YS + k;
 }
 
 // Out = sum_a A*_a-mixing of (M along axis a) applied to S (P:1491-1496 / P:1506-1509):
 //   Out_p = sum_a A*_a[0][1+a] (M_a S_{u_a}),   Out_{u_a} = A*_a[1+a][0] (M_a S_p).
 // Three phases (one per axis); 2 n^2 pencil tasks per phase; barriers between phases
 // (Out_p is accumulated).
-template <int N, int MAT>
+template <int N, int MAT, bool IR>
 __device__ __forceinline__ void apply3(const double* S, double* Out, const double (&c)[3][2], int tid,
-                                       double* I = nullptr, double f = 0.0) {
+                                       double (&ir)[3][N + 1], double f) {
   using L = Lay<N>;
   constexpr int n2 = L::n * L::n;
   const double* Sp = S;
   double* Op = Out;
-  // I != nullptr: also I += f Out for every value once it is final (u after x, v after y,
-  // p and w after z)
+  // IR: the time integral of every value once it is final lives in the registers of the
+  // thread that finalises it (fixed task per thread: 2 n^2 <= 128 = kT): threads < n^2 hold
+  // I_u (x phase), I_v (y), I_w (z) pencils, threads >= n^2 the I_p pencil (z phase)
   for (int t = tid; t < 2 * n2; t += kT) {  // axis x: d_x p -> u, d_x u -> p (store)
-    if (t < n2) pencil<N, 0, false, MAT>(Sp, Out + 1 * L::NNP, t, c[0][1], I ? I + 1 * L::NNP : nullptr, f);
-    else pencil<N, 0, false, MAT>(S + 1 * L::NNP, Op, t - n2, c[0][0]);
+    if (t < n2) pencil<N, 0, false, MAT, IR>(Sp, Out + 1 * L::NNP, t, c[0][1], ir[0], f);
+    else pencil<N, 0, false, MAT, false>(S + 1 * L::NNP, Op, t - n2, c[0][0], ir[0], f);
   }
   __syncthreads();
   for (int t = tid; t < 2 * n2; t += kT) {  // axis y: d_y p -> v, d_y v -> p (+=)
-    if (t < n2) pencil<N, 1, false, MAT>(Sp, Out + 2 * L::NNP, t, c[1][1], I ? I + 2 * L::NNP : nullptr, f);
-    else pencil<N, 1, true, MAT>(S + 2 * L::NNP, Op, t - n2, c[1][0]);
+    if (t < n2) pencil<N, 1, false, MAT, IR>(Sp, Out + 2 * L::NNP, t, c[1][1], ir[1], f);
+    else pencil<N, 1, true, MAT, false>(S + 2 * L::NNP, Op, t - n2, c[1][0], ir[0], f);
   }
   __syncthreads();
   for (int t = tid; t < 2 * n2; t += kT) {  // axis z: d_z p -> w, d_z w -> p (+=)
-    if (t < n2) pencil<N, 2, false, MAT>(Sp, Out + 3 * L::NNP, t, c[2][1], I ? I + 3 * L::NNP : nullptr, f);
-    else pencil<N, 2, true, MAT>(S + 3 * L::NNP, Op, t - n2, c[2][0], I, f);
+    if (t < n2) pencil<N, 2, false, MAT, IR>(Sp, Out + 3 * L::NNP, t, c[2][1], ir[2], f);
+    else pencil<N, 2, true, MAT, IR>(S + 3 * L::NNP, Op, t - n2, c[2][0], ir[0], f);
   }
   __syncthreads();
 }
 
+// The thread's register pencils of I <-> the shared I tensor (see apply3).
+template <int N, bool TO_SHARED>
+__device__ __forceinline__ void ireg_io(double* I, double (&ir)[3][N + 1], int tid, double scale) {
+  using L = Lay<N>;
+  constexpr int n = L::n, n2 = n * n;
+  if (tid < n2) {
+#pragma unroll
+    for (int k = 0; k < n; ++k) {
+      const int a = 1 * L::NNP + pencil_node<N, 0>(tid, k), b = 2 * L::NNP + pencil_node<N, 1>(tid, k),
+                c = 3 * L::NNP + pencil_node<N, 2>(tid, k);
+      if (TO_SHARED) { I[a] = ir[0][k]; I[b] = ir[1][k]; I[c] = ir[2][k]; }
+      else { ir[0][k] = scale * I[a]; ir[1][k] = scale * I[b]; ir[2][k] = scale * I[c]; }
+    }
+  } else if (tid < 2 * n2) {
+#pragma unroll
+    for (int k = 0; k < n; ++k) {
+      const int a = pencil_node<N, 2>(tid - n2, k);
+      if (TO_SHARED) I[a] = ir[0][k];
+      else ir[0][k] = scale * I[a];
+    }
+  }
+}
+
 template <int N>
-__global__ void __launch_bounds__(kT, 3) lina_local(const __grid_constant__ Params prm) {
+__global__ void __launch_bounds__(kT, LINA_MINB) lina_local(const __grid_constant__ Params prm) {
   using L = Lay<N>;
   constexpr int n = L::n, NN = L::NN;
   extern __shared__ __align__(16) double sm[];
@@ -159,9 +196,7 @@ __global__ void __launch_bounds__(kT, 3) lina_local(const __grid_constant__ Para
 #pragma unroll 4
     for (int i = tid; i < 4 * NN; i += kT) {
       const int q = i / NN, r = i % NN, x = r / (n * n), y = (r / n) % n, z = r % n;
-      const double v = R[i];
-      D[q * L::NNP + L::node(x, y, z)] = v;
-      I[q * L::NNP + L::node(x, y, z)] = prm.dt * v;
+      D[q * L::NNP + L::node(x, y, z)] = R[i];
     }
     __syncthreads();  // R is free: the next element's Q streams in during this one
     if (e + gridDim.x < prm.ne) prefetch(e + gridDim.x);
@@ -172,15 +207,19 @@ __global__ void __launch_bounds__(kT, 3) lina_local(const __grid_constant__ Para
       c[a][1] = prm.astar[(e * 3 + a) * 2 + 1];
     }
     __syncthreads();
+    double ir[3][n];
+    ireg_io<N, false>(D, ir, tid, prm.dt);  // I = dt D^0, in registers
     double* cur = D;
     double* nxt = Dn;
     for (int d = 0; d < N; ++d) {  // CK recursion and time integral
-      apply3<N, 0>(cur, nxt, c, tid, I, prm.tfac[d]);
+      apply3<N, 0, true>(cur, nxt, c, tid, ir, prm.tfac[d]);
       double* t = cur;
       cur = nxt;
       nxt = t;
     }
-    apply3<N, 1>(I, nxt, c, tid);  // volume into nxt
+    ireg_io<N, true>(I, ir, tid, 1.0);
+    __syncthreads();
+    apply3<N, 1, false>(I, nxt, c, tid, ir, 0.0);  // volume into nxt
     // Q* = Q + volume; sides of I -> traces
     double* Qw = prm.Q + e * 4 * NN;
     constexpr int QIT = (4 * NN + kT - 1) / kT;
