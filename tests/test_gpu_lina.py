@@ -45,3 +45,43 @@ def test_lina_order8_more_elements_than_ctas():
     cfg = synth.LINA_CONFIGS["lina"].with_(nx=12, ny=11, nz=10, steps=3)
     got, ref = _run(cfg, 3)
     _check(got, ref, "N=7 1320 elements")
+
+
+def test_lina_fullsize_sampled():
+    """The bench workload itself (order 8, 64^3 cuboids, the bench's launch configuration):
+    one GPU step, checked on sampled elements against the oracle on the samples and their six
+    neighbours (the update of an element reads only its neighbours' side tensors)."""
+    import paper_1903_11521_b200 as ydg
+    cfg = synth.LINA_CONFIGS["lina"]
+    mat = synth.lina_material(cfg)
+    Q = synth.lina_dofs(cfg)
+    h = ydg.lina_create(cfg.N)
+    ydg.lina_upload_grid(h, cfg.nx, cfg.ny, cfg.nz, np.array(cfg.h), mat)
+    ydg.lina_upload_dofs(h, 0, Q)
+    ydg.lina_step(h, cfg.dt, 1)
+    rng = np.random.default_rng(3)
+    sel = np.unique(np.concatenate([rng.integers(0, cfg.n_elements, 40), [0, cfg.n_elements - 1]]))
+    got = np.stack([ydg.lina_download_dofs(h, int(e), 1)[0] for e in sel])
+    ydg.lina_destroy(h)
+    nb = olina.neighbours(cfg.nx, cfg.ny, cfg.nz)
+    union = np.unique(np.concatenate([sel, nb[sel].ravel()]))
+    pos = {int(e): i for i, e in enumerate(union)}
+    nodes, w, Kt, Kh, Fh = olina.matrices(cfg.N)
+    U = len(union)
+    Astar = np.zeros((U, 3, 4, 4))
+    Ap = np.zeros((U, 6, 4, 4))
+    Am = np.zeros((U, 6, 4, 4))
+    nbs = np.zeros((U, 6), dtype=np.int64)
+    for u, e in enumerate(union):
+        J = olina.jacobians(*mat[e])
+        for a in range(3):
+            Astar[u, a] = J[a] / cfg.h[a]
+        for s, (a, end) in enumerate(olina.SIDES):
+            p, m = olina.flux_solvers(a, 1.0 if end else -1.0, mat[e], mat[nb[e, s]])
+            Ap[u, s], Am[u, s] = p / cfg.h[a], m / cfg.h[a]
+            nbs[u, s] = pos.get(int(nb[e, s]), u)  # only the samples' rows are used
+    g = olina.Grid(cfg.N, cfg.nx, cfg.ny, cfg.nz, cfg.h, Kt, Kh, Fh, w, nodes, Astar, Ap, Am, nbs)
+    Qu = np.ascontiguousarray(Q[union].transpose(0, 2, 3, 4, 1))
+    I, _ = olina.time_integral(g, Qu, cfg.dt)
+    ref = olina.update(g, Qu, I).transpose(0, 4, 1, 2, 3)[[pos[int(e)] for e in sel]]
+    _check(got, ref, "order 8 64^3 sampled")
