@@ -386,6 +386,7 @@ def run_ydg(args):
     kpath = int(ydg.ydg_query(h, ydg.YDG_Q_KERNEL_PATH))
     fl_local = ydg.ydg_query(h, ydg.YDG_Q_LOCAL_FLOPS)
     fl_neigh = ydg.ydg_query(h, ydg.YDG_Q_NEIGH_FLOPS)
+    fl_neigh_exec = ydg.ydg_query(h, ydg.YDG_Q_NEIGH_FLOPS_EXEC)
     by_local = ydg.ydg_query(h, ydg.YDG_Q_LOCAL_BYTES)
     by_neigh = ydg.ydg_query(h, ydg.YDG_Q_NEIGH_BYTES)
     per_step_launch = int(ydg.ydg_query(h, ydg.YDG_Q_LAUNCHES_PER_STEP))
@@ -441,6 +442,8 @@ def run_ydg(args):
                 "nz_flops_per_element": fl_local, "alg_bytes_per_element": by_local},
         k_nb: {"ms_per_launch": round(avg_neigh, 4), "tflops": round(ach_neigh, 3),
                "frac_peak": round(ach_neigh / peak, 4),
+               "executed_nz_flops_per_element": fl_neigh_exec,
+               "frac_peak_executed": round(ach_neigh * fl_neigh_exec / fl_neigh / peak, 4) if fl_neigh else None,
                "alg_hbm_gbs": round(by_neigh * nloc / (avg_neigh / 1e3) / 1e9, 1),
                "nz_flops_per_element": fl_neigh, "alg_bytes_per_element": by_neigh},
     }

@@ -63,7 +63,10 @@ enum {
                                   dm_flux), 1 fp32 sparse FFMA (ader_*), 2 viscoelastic
                                   tensor-core (vm_local/vm_neigh), 3 generic CSR (gen_*)    */
   YDG_Q_SIMULATIONS = 17,      /* fused simulations S (ydg_set_simulations)                 */
-  YDG_Q_TILE_ELEMENTS = 18     /* elements per tile of the tiled kernels (16 fp64, 32 fp32) */
+  YDG_Q_TILE_ELEMENTS = 18,    /* elements per tile of the tiled kernels (16 fp64, 32 fp32) */
+  YDG_Q_NEIGH_FLOPS_EXEC = 19  /* nonzero flops / element the neighbour kernel executes (the
+                                  fp64 flux kernel lifts local + neighbour flux once per face;
+                                  YDG_Q_NEIGH_FLOPS counts the canonical two lifts)           */
 };
 
 typedef struct ydg_solver ydg_solver; /* opaque, owned by the library */

@@ -1200,6 +1200,10 @@ int ydg_query(ydg_solver* h, int what, double* v) {
       *v = h->P == 27 ? nz_flops_visco(h->N) - nz_flops_visco_local(h->N)
                       : nz_flops_elastic(h->N, false) - nz_flops_local(h->N, h->prec == 8);
       break;
+    case YDG_Q_NEIGH_FLOPS_EXEC:  // the fp64 flux kernel lifts local + neighbour flux once per face
+      *v = h->P == 27 ? nz_flops_visco(h->N) - nz_flops_visco_local(h->N)
+                      : nz_flops_elastic(h->N, h->prec == 8) - nz_flops_local(h->N, h->prec == 8);
+      break;
     default: return fail(h, YDG_ERR_ARG, "unknown query");
   }
   return YDG_OK;
