@@ -63,10 +63,16 @@ enum {
                                   dm_flux), 1 fp32 sparse FFMA (ader_*), 2 viscoelastic
                                   tensor-core (vm_local/vm_neigh), 3 generic CSR (gen_*)    */
   YDG_Q_SIMULATIONS = 17,      /* fused simulations S (ydg_set_simulations)                 */
-  YDG_Q_TILE_ELEMENTS = 18,    /* elements per tile of the tiled kernels (16 fp64, 32 fp32) */
-  YDG_Q_NEIGH_FLOPS_EXEC = 19  /* nonzero flops / element the neighbour kernel executes (the
+  YDG_Q_TILE_ELEMENTS = 18,    /* elements per tile of the tiled kernels (8 fp64, 32 fp32)  */
+  YDG_Q_NEIGH_FLOPS_EXEC = 19, /* nonzero flops / element the neighbour kernel executes (the
                                   fp64 flux kernel lifts local + neighbour flux once per face;
                                   YDG_Q_NEIGH_FLOPS counts the canonical two lifts)           */
+  YDG_Q_GUARD_VIOLATIONS = 20  /* debug: with YDG_GUARD=1 in the environment at ydg_create,
+                                  every device buffer of the mesh and DOFs has 64 KiB guard
+                                  zones of a fill pattern on both sides; this query
+                                  synchronises the device and returns the number of guard
+                                  bytes overwritten (0 = no out-of-bounds store seen), -1 when
+                                  the handle has no guards, -2 on a CUDA error              */
 };
 
 typedef struct ydg_solver ydg_solver; /* opaque, owned by the library */

@@ -82,6 +82,11 @@ struct ydg_solver {
   int64_t lts_n[3] = {0, 0, 0};
   double g_dt = 0;
   int g_n = -1;
+  // YDG_GUARD=1 (debug): every mesh/DOF buffer gets kGuard bytes of a fill pattern on both
+  // sides; ydg_query(YDG_Q_GUARD_VIOLATIONS) counts overwritten guard bytes (an out-of-bounds
+  // store check in place of compute-sanitizer, which this GPU pool does not allow)
+  bool guard = false;
+  std::vector<std::pair<void*, size_t>> guards;  // user pointer, bytes
 };
 
 namespace {
@@ -109,6 +114,20 @@ int elem_bytes(const ydg_solver* h) { return h->prec; }
 // [tile][face][m][q][32].
 int trace_block(const ydg_solver* h) { return h->prec == 8 ? (h->Bt * h->P + 1) / 2 * 2 : 0; }
 
+constexpr size_t kGuard = 64 << 10;
+constexpr unsigned char kGuardByte = 0xA5;
+
+void dfree(ydg_solver* h, void* p) {
+  if (!p) return;
+  for (size_t i = 0; i < h->guards.size(); ++i)
+    if (h->guards[i].first == p) {
+      cudaFree(static_cast<char*>(p) - kGuard);
+      h->guards.erase(h->guards.begin() + static_cast<std::ptrdiff_t>(i));
+      return;
+    }
+  cudaFree(p);
+}
+
 void free_mesh(ydg_solver* h) {
   for (void** p : {&h->Q, &h->traces, &h->star, &h->aplus, &h->aminus, &h->staging, &h->src,
                    reinterpret_cast<void**>(&h->slot_of), reinterpret_cast<void**>(&h->nb_lts[0]),
@@ -117,7 +136,7 @@ void free_mesh(ydg_solver* h) {
                    reinterpret_cast<void**>(&h->lts_lst[2]),
                    reinterpret_cast<void**>(&h->nb), reinterpret_cast<void**>(&h->jh),
                    reinterpret_cast<void**>(&h->nb64), reinterpret_cast<void**>(&h->jh_e)}) {
-    if (*p) cudaFree(*p);
+    dfree(h, *p);
     *p = nullptr;
   }
   h->device_bytes = 0;
@@ -129,14 +148,42 @@ void free_mesh(ydg_solver* h) {
 }
 
 int dalloc(ydg_solver* h, void** p, size_t bytes) {
-  cudaError_t e = cudaMalloc(p, bytes);
+  const size_t g = h->guard ? kGuard : 0;
+  cudaError_t e = cudaMalloc(p, bytes + 2 * g);
   if (e != cudaSuccess) {
     cudaGetLastError();
     *p = nullptr;
     return fail(h, YDG_ERR_OOM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
   }
+  if (g) {
+    char* base = static_cast<char*>(*p);
+    e = cudaMemset(base, kGuardByte, g);
+    if (e == cudaSuccess) e = cudaMemset(base + g + bytes, kGuardByte, g);
+    if (e != cudaSuccess) {
+      cudaFree(base);
+      *p = nullptr;
+      return fail(h, YDG_ERR_CUDA, std::string("guard fill: ") + cudaGetErrorString(e));
+    }
+    *p = base + g;
+    h->guards.emplace_back(*p, bytes);
+  }
   h->device_bytes += bytes;
   return YDG_OK;
+}
+
+// Overwritten guard bytes over all guarded buffers (synchronises the device).
+int64_t guard_violations(ydg_solver* h) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return -2;
+  std::vector<unsigned char> buf(kGuard);
+  int64_t bad = 0;
+  for (const auto& gb : h->guards) {
+    const char* p = static_cast<const char*>(gb.first);
+    for (const char* src : {p - kGuard, p + gb.second}) {
+      if (cudaMemcpy(buf.data(), src, kGuard, cudaMemcpyDeviceToHost) != cudaSuccess) return -2;
+      for (unsigned char c : buf) bad += c != kGuardByte;
+    }
+  }
+  return bad;
 }
 
 int check(ydg_solver* h) {
@@ -548,6 +595,8 @@ int ydg_create(int order, int quantities, int precision, int cuda_device, ydg_so
   h->B = (order + 1) * (order + 2) * (order + 3) / 6;
   h->Bt = (order + 1) * (order + 2) / 2;
   h->generic = generic;
+  const char* gv = std::getenv("YDG_GUARD");
+  h->guard = gv && gv[0] == '1';
   cudaError_t e = cudaSetDevice(cuda_device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) {
@@ -901,12 +950,16 @@ static int upload_tiled(ydg_solver* h, const double* xyz, const double* material
   // grids: resident CTAs per SM x SMs
   int sms = 0, occ_l = 0, occ_n = 0;
   CUDA_OR_FAIL(h, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->dev));
-  occ_l = eb == 8 ? kDmCtasPerSm : 1;  // fp64: 12 warps per SM in kDmCtasPerSm 6-warp groups
+  occ_l = eb == 8 ? kDmCtasPerSm : 1;  // fp64: 12 warps per SM in kDmCtasPerSm work groups
   // fp64 flux kernel: 3-warp groups (8-element halves); four single-group CTAs per SM, or
   // one CTA of kFluxGroups groups
   occ_n = eb == 8 ? (kFluxGroups > 1 ? kFluxGroups : 4) : 1;
   h->grid_local = sms * occ_l;
   h->grid_neigh = sms * occ_n;
+  // YDG_GRID_LOCAL / YDG_GRID_NEIGH (tests): other persistent grid sizes (virtual CTAs), so
+  // that a race between work groups shows up as a bitwise difference of the results
+  if (const char* gl = std::getenv("YDG_GRID_LOCAL")) h->grid_local = std::max(1, std::atoi(gl));
+  if (const char* gn = std::getenv("YDG_GRID_NEIGH")) h->grid_neigh = std::max(1, std::atoi(gn));
   h->have_mesh = true;
   return YDG_OK;
 }
@@ -1178,6 +1231,7 @@ int ydg_query(ydg_solver* h, int what, double* v) {
     case YDG_Q_PROF_NEIGH_MS: *v = h->prof_ms[1]; break;
     case YDG_Q_PROF_LAUNCHES: *v = static_cast<double>(h->prof_launches); break;
     case YDG_Q_SIMULATIONS: *v = static_cast<double>(h->sims); break;
+    case YDG_Q_GUARD_VIOLATIONS: *v = h->guard ? static_cast<double>(guard_violations(h)) : -1.0; break;
     case YDG_Q_TILE_ELEMENTS: *v = static_cast<double>(h->prec == 8 ? kDmLanes : kLanes); break;
     case YDG_Q_N_ELEMENTS: *v = static_cast<double>(h->ne); break;
     case YDG_Q_FIRST_LOCAL: *v = static_cast<double>(h->first); break;

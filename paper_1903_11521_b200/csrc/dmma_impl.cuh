@@ -160,6 +160,17 @@ __device__ __forceinline__ double ld_stream(const double* p) {
   asm("ld.global.nc.L1::evict_first.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
+// star matrices of the tile: read by the star-chunk role at the tile start and again by every
+// sparse-DFMA CK step; YDG_STAR_L1=1 keeps them in L1 (evict_last) between the reads
+#ifndef YDG_STAR_L1
+#define YDG_STAR_L1 0
+#endif
+__device__ __forceinline__ double ld_star(const double* p) {
+  if constexpr (YDG_STAR_L1 == 0) return ld_stream(p);
+  double v;
+  asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
 
 __device__ __forceinline__ int krow(const Ctx& x, unsigned w) { return static_cast<int>((w >> x.sh4) & 0xffu); }
 __device__ __forceinline__ int mrow(const Ctx& x, unsigned long long w) {
@@ -380,6 +391,24 @@ constexpr int kWF = 3;
 constexpr int kTF = kWF * 32;
 constexpr int kHalves = kL / kLF;
 constexpr int kFluxCtas = 4;
+#ifndef YDG_FLUX_LATE_OWN
+#define YDG_FLUX_LATE_OWN 0
+#endif
+constexpr bool kFluxLateOwn = YDG_FLUX_LATE_OWN;
+// YDG_FLUX_PF: L2 prefetch of the next unit's neighbour (bit 1) / own (bit 2) face blocks,
+// issued at face YDG_FLUX_PF_FACE of the current unit
+#ifndef YDG_FLUX_PF
+#define YDG_FLUX_PF 0
+#endif
+#ifndef YDG_FLUX_PF_FACE
+#define YDG_FLUX_PF_FACE 1
+#endif
+constexpr int kFluxPf = YDG_FLUX_PF, kFluxPfFace = YDG_FLUX_PF_FACE;
+// face of the current unit at which the next unit's Q is prefetched into L2 (-1: none)
+#ifndef YDG_FLUX_QPF_FACE
+#define YDG_FLUX_QPF_FACE 3
+#endif
+constexpr int kFluxQpfFace = YDG_FLUX_QPF_FACE;
 __device__ __forceinline__ int swzf(int row, int col) { return row * kRSF + (col ^ ((row & 2) << 1)); }
 __device__ __forceinline__ void smem_bf(const Ctx& x, const double* Y, unsigned w, double (&bf)[kU]) {
   const int row = krow(x, w);
@@ -497,7 +526,7 @@ __device__ __forceinline__ void col_star(const Ctx& x, int ce, int cp, double (&
 #pragma unroll
   for (int c = 0; c < 3; ++c)
 #pragma unroll
-    for (int j = 0; j < 3; ++j) ca[3 * c + j] = ld_stream(x.star + ((c * kP + cp) * 3 + j) * kL + ce);
+    for (int j = 0; j < 3; ++j) ca[3 * c + j] = ld_star(x.star + ((c * kP + cp) * 3 + j) * kL + ce);
 }
 template <Src SRC, int B>
 __device__ __forceinline__ void col_x(const Ctx& x, int l, int ce, const double (&ca)[9], int q0, int q1, int q2,
@@ -631,10 +660,18 @@ __device__ __forceinline__ void stage_frags(const Ctx& x, int F0, int NF) {
 }
 // Called by DG<N>::ck after CK step 0 (which ends with a barrier): the fragment buffer
 // now receives the volume term's fragments.
+// YDG_QPF bit 1: after CK step 0, the tile's Q^n rows >= IROWS (re-read by the traces and the
+// volume's Q update, evicted from L2 since the staging) are prefetched into L2 again;
+// bit 2: again before the volume term
+#ifndef YDG_QPF
+#define YDG_QPF 7  // measured (c1, 8-element tiles): local 14.69 -> 14.11-14.19 ms; bit 1 alone 14.41
+#endif
 template <int N>
 __device__ __forceinline__ void after_ck0(Ctx& x) {
   if constexpr (kLocalFs)
     if (x.tid == 0) stage_frags<N>(x, DG<N>::VOL_F0, DG<N>::VOL_NF < kLocalFsCap ? DG<N>::VOL_NF : kLocalFsCap);
+  if constexpr ((YDG_QPF & 1) != 0)
+    if (x.tid == 32) prefetch_l2(x.Qt + DG<N>::IROWS * kRS, (DG<N>::B - DG<N>::IROWS) * kRS * sizeof(double));
 }
 
 // CK + time integral, face traces R^iT I (stored for the flux kernel) and
@@ -695,7 +732,7 @@ __global__ void __launch_bounds__(kT * kLocalGroups, kLocalGroups == 1 ? kDmCtas
     const int64_t tile = prm.tile0 + it;
     double* Qt = prm.Q + tile * B * kRS;
     YDG_PHASE(0);
-    if (x.tid == 0 && it + vgrid < prm.ntiles) {  // next tile of this CTA -> L2
+    if (x.tid == 0 && (YDG_QPF & 4) == 0 && it + vgrid < prm.ntiles) {  // next tile of this CTA -> L2
       const int64_t nt = tile + vgrid;
       prefetch_l2(prm.Q + nt * B * kRS, B * kRS * sizeof(double));
       prefetch_l2(prm.star + nt * 3 * kP * 3 * kL, 3 * kP * 3 * kL * sizeof(double));
@@ -716,7 +753,7 @@ __global__ void __launch_bounds__(kT * kLocalGroups, kLocalGroups == 1 ? kDmCtas
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
-      for (int j = 0; j < 3; ++j) x.a[3 * c + j] = ld_stream(st + ((c * kP + xp) * 3 + j) * kL);
+      for (int j = 0; j < 3; ++j) x.a[3 * c + j] = ld_star(st + ((c * kP + xp) * 3 + j) * kL);
     cp_async_wait_all();
     if constexpr (kLocalFs) mbar_wait(x.fbar, 0);  // CK step 0 fragments (first of two loads per tile)
     x.sync();
@@ -773,6 +810,14 @@ __global__ void __launch_bounds__(kT * kLocalGroups, kLocalGroups == 1 ? kDmCtas
       mbar_expect_tx(qbar, G::IROWS * kRS * sizeof(double));
       bulk_g2s(x.S, Qt, G::IROWS * kRS * sizeof(double), qbar);
     }
+    if constexpr ((YDG_QPF & 2) != 0)
+      if (x.tid == 32) prefetch_l2(Qt + G::IROWS * kRS, (B - G::IROWS) * kRS * sizeof(double));
+    if constexpr ((YDG_QPF & 4) != 0)  // bit 4: the next tile's Q^n and star matrices -> L2 now
+      if (x.tid == 64 && it + vgrid < prm.ntiles) {
+        const int64_t nt = tile + vgrid;
+        prefetch_l2(prm.Q + nt * B * kRS, B * kRS * sizeof(double));
+        prefetch_l2(prm.star + nt * 3 * kP * 3 * kL, 3 * kP * 3 * kL * sizeof(double));
+      }
     YDG_PHASE(9);
     {
       double acc[G::QMT][kU][2];
@@ -899,6 +944,10 @@ __global__ void __launch_bounds__(kTF * kFluxGroups, kFluxGroups == 1 ? kFluxCta
   // thread roles: rotation (element re, column rp) for threads < 72; Godunov rows
   // m = rp + 12 i of element re
   const int re = tid % kLF, rp = tid / kLF;
+  // YDG_FLUX_LATE_OWN: the rotation takes h from a register (read from the previous item's
+  // j|h copy), so the wait for the own copy moves behind the rotation
+  int hcur = 0;
+  if constexpr (kFluxLateOwn) hcur = prm.jh[(prm.tile0 + vb / kHalves) * 4 * kJH + (vb % kHalves) * kLF + re] >> 2;
   for (int64_t u = vb; u < nitems; u += vgrid) {
     const int64_t tile = prm.tile0 + u / kHalves, half = u % kHalves;
     x.qcol0 = 3 * x.w * kL + half * kLF;
@@ -908,17 +957,24 @@ __global__ void __launch_bounds__(kTF * kFluxGroups, kFluxGroups == 1 ? kFluxCta
       // Y buffer F & 1: last read by the paired lift of faces F-2, F-1 (followed by a barrier)
       double* Y = Y0 + (F & 1) * Bt * kRSF;
       const bool has_next = F < 3 || more;
-      mbar_wait(&bar[0], ph_o);  // own block, coefficients, j|h of this item; slots of the next
-      ph_o ^= 1;
+      if constexpr (!kFluxLateOwn) {
+        mbar_wait(&bar[0], ph_o);  // own block, coefficients, j|h of this item; slots of the next
+        ph_o ^= 1;
+      }
       mbar_wait(&bar[1], ph_n);  // neighbour blocks of this item
       ph_n ^= 1;
       if (tid < kP * kLF) {  // z = f^h t on column rp of element re's neighbour block -> Y
-        const int h = JH[half * kLF + re] >> 2;
+        const int h = kFluxLateOwn ? hcur : JH[half * kLF + re] >> 2;
         const double* zc = NB + re * TS + rp;
         double t[Bt];
 #pragma unroll
         for (int n = 0; n < Bt; ++n) t[n] = zc[n * kP];
         G::rotf(h, t, Y, rp * kLF + re);
+      }
+      if constexpr (kFluxLateOwn) {
+        mbar_wait(&bar[0], ph_o);  // own block, coefficients of this item; slots, j|h of the next
+        ph_o ^= 1;
+        if (has_next) hcur = JHX[(F < 3 ? half : (u + vgrid) % kHalves) * kLF + re] >> 2;
       }
       double fc[kFaceCoeffs];
 #pragma unroll
@@ -927,8 +983,22 @@ __global__ void __launch_bounds__(kTF * kFluxGroups, kFluxGroups == 1 ? kFluxCta
       if (tid == 0 && has_next) {
         const int nhalf = F < 3 ? half : (u + vgrid) % kHalves;
         issue_nb(NBX, JHX + nhalf * kLF);
-      } else if (tid == 32 && F == 3 && more) {  // next unit's Q -> L2
+      } else if (tid == 32 && F == kFluxQpfFace && more) {  // next unit's Q -> L2
         prefetch_l2(prm.Q + (prm.tile0 + (u + vgrid) / kHalves) * B * kRS, B * kRS * sizeof(double));
+      }
+      if constexpr (kFluxPf != 0) {  // the next unit's face blocks -> L2, half a unit ahead
+        if (F == kFluxPfFace && more && tid >= 64) {
+          const int64_t nu = u + vgrid, ntile = prm.tile0 + nu / kHalves, nhalf = nu % kHalves;
+          const int k = tid - 64, f = k / kLF, e = k % kLF;  // 32 threads: (face, element)
+          if (kFluxPf & 1) {  // neighbour blocks
+            const int64_t slot = (ntile * 4 + f) * kL + nhalf * kLF + e;
+            const int64_t nbe = prm.nb[slot];
+            const int jn = prm.jh[(ntile * 4 + f) * kJH + nhalf * kLF + e] & 3;
+            prefetch_l2(prm.traces + ((nbe / kL) * 4 + jn) * FACE + (nbe % kL) * TS, TS * sizeof(double));
+          }
+          if ((kFluxPf & 2) && e == 0)  // own face blocks
+            prefetch_l2(prm.traces + (ntile * 4 + f) * FACE + nhalf * FACEF, FACEF * sizeof(double));
+        }
       }
       {  // Godunov flux of rows m = rp, rp + 12, ... of element re, in place in Y
         const double* T = O + re * TS;

@@ -168,7 +168,7 @@ cudaError_t launch_local(int N, const StepParams<T>& p, int grid, cudaStream_t s
   const void* f = pick_local(N, sizeof(T));
   if (!f) return cudaErrorInvalidValue;
   void* args[] = {const_cast<StepParams<T>*>(&p)};
-  // fp64: grid counts 6-warp groups (virtual CTAs); kLocalGroups of them share one CTA
+  // fp64: grid counts work groups (virtual CTAs); kLocalGroups of them share one CTA
   const int ctas = sizeof(T) == 8 ? (grid + kLocalGroups - 1) / kLocalGroups : grid;
   return cudaLaunchKernel(f, dim3(ctas), dim3(block_threads(sizeof(T))), args, local_smem_bytes(N, sizeof(T)), s);
 }

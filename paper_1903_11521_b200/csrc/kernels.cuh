@@ -6,10 +6,12 @@
 namespace ydg {
 
 constexpr int kLanes = 32;   // elements per tile of the fp32 kernels
-// fp64 tensor-core kernels: elements per tile (8 or 16), warps per CTA (3 per 8 elements),
-// CTAs per SM (12 warps per SM: three per sub-partition)
+// fp64 tensor-core kernels: elements per tile (8 or 16), warps per work group (3 per 8
+// elements), groups per SM (12 warps per SM: three per sub-partition).  Measured (c1): 8-element
+// tiles in four 3-warp groups per CTA 14.69 / 7.60 ms (local / flux) vs 16-element tiles in two
+// 6-warp groups 14.82 / 7.88 ms
 #ifndef YDG_DM_LANES
-#define YDG_DM_LANES 16
+#define YDG_DM_LANES 8
 #endif
 constexpr int kDmLanes = YDG_DM_LANES;
 constexpr int kDmWarps = 3 * (kDmLanes / 8);
@@ -17,10 +19,11 @@ constexpr int kDmCtasPerSm = 12 / kDmWarps;
 // fp64 flux kernel: 3-warp groups (8-element halves) per CTA.  1: one group per CTA, four
 // CTAs per SM; 4: one CTA per SM whose four groups share the lift's A fragments staged in
 // shared memory (named barriers per group).
-// fp64 local kernel: 1: kDmCtasPerSm CTAs per SM; 2: one CTA per SM of two 6-warp groups
+// fp64 local kernel: 1: kDmCtasPerSm CTAs per SM; > 1: one CTA per SM of that many work groups
+// (kDmCtasPerSm of them: four 3-warp groups at 8-element tiles, two 6-warp groups at 16)
 // sharing CK step 0's and (part of) the volume's A fragments in shared memory
 #ifndef YDG_LOCAL_GROUPS
-#define YDG_LOCAL_GROUPS 2
+#define YDG_LOCAL_GROUPS (YDG_DM_LANES == 8 ? 4 : 2)
 #endif
 constexpr int kLocalGroups = YDG_LOCAL_GROUPS;
 #ifndef YDG_FLUX_GROUPS

@@ -151,13 +151,13 @@ def emit_xprod(b, plan, name, til, src, fbase=None, acc="acc"):
         if i + 1 < len(ins):
             afr(i + 1)
         r = kset_rows(ks)
-        b(f"    xcalc<{src}, B>(x, 0, {r[0]}, {r[1]}, {r[2]}, {r[3]});")
+        b(f"    xcalc<{src}, B>(x, {i}, {r[0]}, {r[1]}, {r[2]}, {r[3]});")
         b("    __syncwarp();")
         for c in range(3):
             mine = [(mt, nm) for (cc, mt, tid), nm in zip(plan[i], names[i]) if cc == c]
             if not mine:
                 continue
-            b(f"    {{ double bf[kU]; xb_b(x, 0, {c}, bf);")
+            b(f"    {{ double bf[kU]; xb_b(x, {i}, {c}, bf);")
             for mt, nm in mine:
                 b(f"      dmma3({acc}[{mt}], {nm}, bf);")
             b("    }")
@@ -200,6 +200,9 @@ DFMA_CK_ROWS = int(os.environ.get("YDG_GEN_CKROWS", "20"))
 # faces 0 and 1 traces as sparse DFMA code (else tensor cores); faces 2 and 3 as well
 DFMA_TR01 = os.environ.get("YDG_GEN_TR01", "1") == "1"
 DFMA_TR23 = os.environ.get("YDG_GEN_TR23", "0") == "1"
+# where the sparse-DFMA CK steps load the column's star coefficients: "step" (each step,
+# from global memory), "tail" (once, after CK step 0), "pre" (once, before CK step 0)
+STAR_LOAD = os.environ.get("YDG_GEN_STAR", "step")
 DFMA_TAIL_ROWS = 0   # CK steps d >= 1 from the first with at most this many output rows on:
                      # one warp-synchronous sparse DFMA phase (0 = off: the element-grouped
                      # lanes hit 9-way shared-memory bank conflicts, measured slower)
@@ -220,13 +223,18 @@ def emit_ck_dfma(b, d, K, bi, bo, IROWS):
                     n += 1
     src = "SRC_Q" if d == 0 else "SRC_S"
     b(f"  // CK step d = {d}: rows in {bi}, rows out {bo}; sparse DFMA ({n} nonzeros)")
-    b(f"  static __device__ __forceinline__ void ck{d}(Ctx& x) {{")
+    own_star = STAR_LOAD == "step" or d == 0
+    if own_star:
+        b(f"  static __device__ __forceinline__ void ck{d}(Ctx& x) {{")
+    else:
+        b(f"  static __device__ __forceinline__ void ck{d}(Ctx& x, const double (&ca)[9], int q0, int q1, int q2) {{")
     b(f"    double y[{bo}];")
     b(f"    for (int k = 0; k < {bo}; ++k) y[k] = 0.0;")
     b("    if (x.cc < kRS) {")
-    b("      double ca[9];")
-    b("      int q0, q1, q2;")
-    b("      col_star(x, x.ce, x.cp, ca, q0, q1, q2);")
+    if own_star:
+        b("      double ca[9];")
+        b("      int q0, q1, q2;")
+        b("      col_star(x, x.ce, x.cp, ca, q0, q1, q2);")
     for l in sorted(nz):
         b(f"      {{ double x0, x1, x2; col_x<{src}, B>(x, {l}, x.ce, ca, q0, q1, q2, x0, x1, x2);")
         for c, k, v in nz[l]:
@@ -367,8 +375,16 @@ def gen_order(N):
         b("    x.sync();")
         b("  }")
     b("  static __device__ __forceinline__ void ck(Ctx& x) {")
+    dfma_steps = [d for d in range(1, tail0 if tail0 is not None else N) if comb(N - d + 2, 3) <= DFMA_CK_ROWS]
+    star_args = ""
+    if STAR_LOAD != "step" and dfma_steps:
+        star_args = ", ca, q0, q1, q2"
+        b("    double ca[9];")
+        b("    int q0 = 0, q1 = 0, q2 = 0;")
     for d in range(tail0 if tail0 is not None else N):
-        b(f"    ck{d}(x);")
+        if star_args and ((STAR_LOAD == "pre" and d == 0) or (STAR_LOAD == "tail" and d == dfma_steps[0])):
+            b("    if (x.cc < kRS) col_star(x, x.ce, x.cp, ca, q0, q1, q2);")
+        b(f"    ck{d}(x{star_args if d in dfma_steps else ''});")
         if d == 0:
             b("    after_ck0<" + str(N) + ">(x);  // the fragment buffer is free: stage the volume's")
         b(f"    YDG_PHASE({2 + d});")
