@@ -27,9 +27,8 @@ Emits ``csrc/generated/ydg_dmma_N{n}.cuh``.
 from __future__ import annotations
 
 import os
-from math import comb
 
-from . import tables, tiling
+from . import einsum, tables, tiling
 
 ORDERS = (1, 2, 3, 4, 5, 6)
 PAD = 0xFF
@@ -262,7 +261,7 @@ def emit_ck_tail(b, d0, N, K):
     b("    int q0 = 0, q1 = 0, q2 = 0;")
     b("    if (x.tc >= 0) col_star(x, x.te, x.tp, ca, q0, q1, q2);")
     for d in range(d0, N):
-        bi, bo = comb(N - d + 3, 3), comb(N - d + 2, 3)
+        bi, bo = einsum.ck_dims(N, d)
         nz = {}
         for c in range(3):
             for k in range(bo):
@@ -330,7 +329,7 @@ def gen_order(N):
     t = tables.load(N)
     K, R, f = t["K"], t["R"], t["f"]
     B, Bt = t["B"], t["Bt"]
-    Bv = comb(N + 2, 3)
+    Bv = einsum.vol_dim(N)
     til = tiling.tiling(N)
     tab = Table()
     IROWS = Bv  # time-integral rows in shared memory (rows >= Bv are dt * Q)
@@ -346,7 +345,7 @@ def gen_order(N):
     regions = {}  # products whose A fragments are staged in shared memory: [first, end)
     # ---------------- CK
     for d in range(N):
-        bi, bo = comb(N - d + 3, 3), comb(N - d + 2, 3)
+        bi, bo = einsum.ck_dims(N, d)
         tl = til[f"ck{d}"]
         MT = len(tl["out"])
         mats = [(lambda r, col, c=c: -K[c][col][r]) for c in range(3)]  # Kt^c[r][col] = -K^c[col][r]
@@ -375,7 +374,7 @@ def gen_order(N):
         b("    x.sync();")
         b("  }")
     b("  static __device__ __forceinline__ void ck(Ctx& x) {")
-    dfma_steps = [d for d in range(1, tail0 if tail0 is not None else N) if comb(N - d + 2, 3) <= DFMA_CK_ROWS]
+    dfma_steps = [d for d in range(1, tail0 if tail0 is not None else N) if einsum.ck_dims(N, d)[1] <= DFMA_CK_ROWS]
     star_args = ""
     if STAR_LOAD != "step" and dfma_steps:
         star_args = ", ca, q0, q1, q2"

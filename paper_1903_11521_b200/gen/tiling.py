@@ -23,11 +23,10 @@ import math
 import os
 import random
 import sys
-from math import comb
 
 import numpy as np
 
-from . import tables
+from . import einsum, tables
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CACHE_DIR = os.path.join(HERE, "tilings")
@@ -43,11 +42,11 @@ def products(N):
     K = [np.array(k, dtype=float) != 0 for k in t["K"]]
     R = [np.array(r, dtype=float) != 0 for r in t["R"]]
     B, Bt = t["B"], t["Bt"]
-    Bv = comb(N + 2, 3)
+    Bv = einsum.vol_dim(N)
     irows = Bv  # rows of the time integral held in shared memory
     out = {}
     for d in range(N):
-        bi, bo = comb(N - d + 3, 3), comb(N - d + 2, 3)
+        bi, bo = einsum.ck_dims(N, d)
         out[f"ck{d}"] = ([K[c].T[:bo, :bi] for c in range(3)], [list(range(bi))])
     out["vol"] = ([K[c][:, :Bv] for c in range(3)], [list(range(Bv))])
     for i in range(4):
