@@ -29,7 +29,14 @@ constexpr int kJH = kL < 16 ? 16 : kL;  // bytes of j|h per (tile, face) (padded
 constexpr int kW = kDmWarps;   // warps per CTA (kDmCtasPerSm CTAs per SM: 3 warps per sub-partition)
 constexpr int kT = kW * 32;    // threads per CTA
 constexpr int kU = 3;          // units (8-column tiles) per warp
-constexpr int kXW = 3 * kU * 4 * 8;  // warp-private X buffer: [c][k][row][8 elements]
+// warp-private X buffer: [c][k][row][8 elements], (c, k) blocks kXS doubles apart.  The
+// star-chunk stores of lanes xk = 0, 1, 2 hit the same 16 banks at a block stride of 32
+// doubles (3 wavefronts per store); YDG_XPAD = 8 puts block k + 1 on the other half (2)
+#ifndef YDG_XPAD
+#define YDG_XPAD 0
+#endif
+constexpr int kXS = 4 * 8 + YDG_XPAD;
+constexpr int kXW = 3 * kU * kXS;
 #ifndef YDG_XBUF
 #define YDG_XBUF 1
 #endif
@@ -244,13 +251,13 @@ __device__ __forceinline__ void xcalc(Ctx& x, int buf, int r0, int r1, int r2, i
 #pragma unroll
     for (int r = 0; r < 4; ++r)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) xb[((c * kU + x.xk) * 4 + r) * 8 + (x.lane & 7)] = v[r][c];
+      for (int c = 0; c < 3; ++c) xb[(c * kU + x.xk) * kXS + r * 8 + (x.lane & 7)] = v[r][c];
   }
 }
 __device__ __forceinline__ void xb_b(const Ctx& x, int buf, int c, double (&bf)[kU]) {
   const double* xb = x.xb + (buf % kXBUF) * kXW;
 #pragma unroll
-  for (int k = 0; k < kU; ++k) bf[k] = xb[((c * kU + k) * 4 + (x.lane & 3)) * 8 + (x.lane >> 2)];
+  for (int k = 0; k < kU; ++k) bf[k] = xb[(c * kU + k) * kXS + (x.lane & 3) * 8 + (x.lane >> 2)];
 }
 
 // Gathered B fragments of the own quantity column: lane row = byte (lane & 3) of w.

@@ -75,3 +75,30 @@ def test_fullsize_sampled_one_step(name):
                                lambda ids: np.stack([Qn[e] for e in ids]))
         check_parity(rel_err(got, ref), cfg.precision, f"{name} last step")
     ydg.ydg_destroy(h)
+
+
+def test_fullsize_sampled_c4():
+    """BASELINE configs[4] (12.6 M tetrahedra, N = 5, fp64) on one GPU at its full size -- the
+    largest mesh the library holds (~141 GB of device memory, 64-bit tile offsets): Q^0
+    uploaded in 1 M-element chunks straight from the seeded generator, one step, sampled
+    one-step parity against the oracle."""
+    import paper_1903_11521_b200 as ydg
+    cfg = synth.CONFIGS["c4"]
+    xyz, vid = synth.kuhn_mesh(cfg.nx, cfg.ny, cfg.nz, seed=cfg.seed, jitter=cfg.jitter)
+    mat = synth.material(cfg)
+    h = ydg.ydg_create(cfg.N, cfg.P, cfg.precision)
+    ydg.ydg_upload_mesh(h, xyz, vid, mat)
+    E = cfg.n_elements
+    chunk = 1 << 20
+    for first in range(0, E, chunk):
+        ydg.ydg_upload_dofs(h, first, synth.dofs(cfg, first, min(chunk, E - first)))
+    sel = _samples(cfg)
+    ydg.ydg_step(h, cfg.dt, 1)
+    got = np.stack([ydg.ydg_download_dofs(h, int(e), 1)[0] for e in sel])
+    ydg.ydg_destroy(h)
+
+    def q0(ids):
+        return np.stack([synth.dofs(cfg, int(e), 1)[0] for e in ids])
+
+    ref = _oracle_one_step(cfg, xyz, vid, mat, None, sel, q0(sel), q0)
+    check_parity(rel_err(got, ref), cfg.precision, "c4 n=0")
