@@ -38,7 +38,7 @@ def test_c0_parity_and_tables():
 
 @pytest.mark.parametrize("N", [1, 2, 3, 4, 5])
 def test_orders_fp64_ragged(N):
-    """3x3x3 cubes = 162 elements: 5 full tiles of 32 and a ragged tail of 2."""
+    """3x3x3 cubes = 162 elements: 20 full 8-element tiles (fp64) and a ragged tail of 2."""
     cfg = _cfg("c0", N=N, nx=3, ny=3, nz=3)
     err, *_ = _parity(cfg, nsteps=2)
 
