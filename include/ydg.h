@@ -67,12 +67,15 @@ enum {
   YDG_Q_NEIGH_FLOPS_EXEC = 19, /* nonzero flops / element the neighbour kernel executes (the
                                   fp64 flux kernel lifts local + neighbour flux once per face;
                                   YDG_Q_NEIGH_FLOPS counts the canonical two lifts)           */
-  YDG_Q_GUARD_VIOLATIONS = 20  /* debug: with YDG_GUARD=1 in the environment at ydg_create,
+  YDG_Q_GUARD_VIOLATIONS = 20, /* debug: with YDG_GUARD=1 in the environment at ydg_create,
                                   every device buffer of the mesh and DOFs has 64 KiB guard
                                   zones of a fill pattern on both sides; this query
                                   synchronises the device and returns the number of guard
                                   bytes overwritten (0 = no out-of-bounds store seen), -1 when
                                   the handle has no guards, -2 on a CUDA error              */
+  YDG_Q_MAX_ABS_Q = 21         /* diagnostic: max |Q| over the owned DOFs (a reduction
+                                  kernel on the handle's stream, synchronised); NaN when any
+                                  DOF is NaN or infinite                                     */
 };
 
 typedef struct ydg_solver ydg_solver; /* opaque, owned by the library */

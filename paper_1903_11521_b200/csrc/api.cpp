@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <functional>
 #include <memory>
 #include <string>
@@ -169,6 +170,40 @@ int dalloc(ydg_solver* h, void** p, size_t bytes) {
   }
   h->device_bytes += bytes;
   return YDG_OK;
+}
+
+// max |Q| over the owned DOFs (NaN if any is not finite); synchronises the handle's stream.
+double max_abs_q(ydg_solver* h) {
+  const double nan = std::numeric_limits<double>::quiet_NaN();
+  if (!h->have_mesh || !h->Q) return nan;
+  void* buf = nullptr;
+  if (cudaMalloc(&buf, 16) != cudaSuccess) return nan;
+  cudaStream_t s = h->stream;
+  cudaError_t e = cudaMemsetAsync(buf, 0, 16, s);
+  unsigned long long* out = static_cast<unsigned long long*>(buf);
+  int* bad = reinterpret_cast<int*>(out + 1);
+  const int64_t PB = static_cast<int64_t>(h->P) * h->B;
+  int64_t n, per_tile = 1;
+  int L;
+  if (h->generic) {  // canonical [e][p][k]
+    n = h->nlocal * PB;
+    L = 0;
+  } else {  // tiled [tile][k][p][L]
+    L = h->lanes;
+    per_tile = PB * L;
+    n = h->ntiles * per_tile;
+  }
+  if (e == cudaSuccess)
+    e = h->prec == 8 ? launch_maxabs<double>(static_cast<const double*>(h->Q), n, per_tile, L, PB, h->nlocal, out, bad, s)
+                     : launch_maxabs<float>(static_cast<const float*>(h->Q), n, per_tile, L, PB, h->nlocal, out, bad, s);
+  unsigned long long hv[2] = {0, 0};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hv, buf, 16, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(buf);
+  if (e != cudaSuccess || static_cast<int>(hv[1] & 0xffffffffu) != 0) return nan;
+  double v;
+  std::memcpy(&v, &hv[0], sizeof v);
+  return v;
 }
 
 // Overwritten guard bytes over all guarded buffers (synchronises the device).
@@ -1232,6 +1267,13 @@ int ydg_query(ydg_solver* h, int what, double* v) {
     case YDG_Q_PROF_LAUNCHES: *v = static_cast<double>(h->prof_launches); break;
     case YDG_Q_SIMULATIONS: *v = static_cast<double>(h->sims); break;
     case YDG_Q_GUARD_VIOLATIONS: *v = h->guard ? static_cast<double>(guard_violations(h)) : -1.0; break;
+    case YDG_Q_MAX_ABS_Q: {
+      int rc = check(h);
+      if (rc) return rc;
+      if (!h->have_mesh) return fail(h, YDG_ERR_STATE, "no mesh");
+      *v = max_abs_q(h);
+      break;
+    }
     case YDG_Q_TILE_ELEMENTS: *v = static_cast<double>(h->prec == 8 ? kDmLanes : kLanes); break;
     case YDG_Q_N_ELEMENTS: *v = static_cast<double>(h->ne); break;
     case YDG_Q_FIRST_LOCAL: *v = static_cast<double>(h->first); break;

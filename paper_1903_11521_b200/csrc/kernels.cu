@@ -181,6 +181,44 @@ cudaError_t launch_neigh(int N, const StepParams<T>& p, int grid, cudaStream_t s
   const int ctas = sizeof(T) == 8 ? (grid + kFluxGroups - 1) / kFluxGroups : grid;
   return cudaLaunchKernel(f, dim3(ctas), dim3(flux_threads(sizeof(T))), args, neigh_smem_bytes(N, sizeof(T)), s);
 }
+// max |Q| over the owned elements (diagnostic): L > 0 = tiled layout
+// [tile][k][p][L] (element = tile * L + lane), L = 0 = canonical [e][p][k]; a non-finite
+// value sets *bad.  out holds the bit pattern of a non-negative double (ordered like the
+// value, so atomicMax on the bits is a max on the values).
+template <typename T>
+__global__ void maxabs_kernel(const T* Q, int64_t n, int64_t per_tile, int L, int64_t per_elem, int64_t nlocal,
+                              unsigned long long* out, int* bad) {
+  double m = 0.0;
+  int b = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t e = L > 0 ? (i / per_tile) * L + i % L : i / per_elem;
+    if (e >= nlocal) continue;
+    const double v = static_cast<double>(Q[i]);
+    if (!isfinite(v)) b = 1;
+    else m = fmax(m, fabs(v));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    b |= __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(m)));
+    if (b) atomicOr(bad, 1);
+  }
+}
+template <typename T>
+cudaError_t launch_maxabs(const T* Q, int64_t n, int64_t per_tile, int L, int64_t per_elem, int64_t nlocal,
+                          unsigned long long* out, int* bad, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  maxabs_kernel<T><<<148 * 8, 256, 0, s>>>(Q, n, per_tile, L, per_elem, nlocal, out, bad);
+  return cudaGetLastError();
+}
+template cudaError_t launch_maxabs<double>(const double*, int64_t, int64_t, int, int64_t, int64_t, unsigned long long*,
+                                           int*, cudaStream_t);
+template cudaError_t launch_maxabs<float>(const float*, int64_t, int64_t, int, int64_t, int64_t, unsigned long long*,
+                                          int*, cudaStream_t);
+
 cudaError_t launch_trace_combine(double* traces, const int64_t* lst, int64_t n, int TS, int L, int mode,
                                  cudaStream_t s) {
   if (n <= 0) return cudaSuccess;

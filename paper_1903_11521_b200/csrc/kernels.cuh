@@ -65,6 +65,10 @@ cudaError_t launch_to_canonical(int P, int B, int L, const T* tiled, T* canon, i
 // 2 dst += a (fp64 trace layout [tile][face][lane][TS])
 cudaError_t launch_trace_combine(double* traces, const int64_t* lst, int64_t n, int TS, int L, int mode,
                                  cudaStream_t s);
+// max |Q| over owned elements; L > 0: tiled [tile][k][p][L], L = 0: canonical [e][p][k]
+template <typename T>
+cudaError_t launch_maxabs(const T* Q, int64_t n, int64_t per_tile, int L, int64_t per_elem, int64_t nlocal,
+                          unsigned long long* out, int* bad, cudaStream_t s);
 size_t local_smem_bytes(int N, int elem_bytes);
 size_t sparse_local_smem(int N, int elem_bytes);
 size_t sparse_neigh_smem(int N, int elem_bytes);

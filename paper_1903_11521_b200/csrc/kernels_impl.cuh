@@ -20,6 +20,16 @@ namespace kimpl {
 constexpr int kP = 9;
 constexpr int kRS = kP * kLanes;  // row stride of [row][q][lane]
 
+// YDG_FQPF: the tile's Q rows -> L2 ahead of its read-modify-write (the staging read of the
+// local kernel was ~100 us earlier and has left the L2; the neighbour kernel reads Q last)
+#ifndef YDG_FQPF
+#define YDG_FQPF 1  // measured (c2): ader_neigh 23.40 -> 23.10 ms, ader_local unchanged
+#endif
+__device__ __forceinline__ void q_prefetch_l2(const void* p, unsigned bytes) {
+  if constexpr (YDG_FQPF != 0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // 3-column pattern of star-matrix row p (same table as setup.cpp star_cols)
 static __constant__ int c_star_cols[9][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {6, 7, 7}, {7, 8, 8},
                                              {6, 8, 8}, {0, 3, 5}, {3, 1, 4}, {5, 4, 2}};
@@ -111,6 +121,7 @@ __global__ void __launch_bounds__(kP * kLanes, 1) ader_local(const StepParams<T>
       for (int k = G::Bv; k < B; ++k) S[k * kRS + own] = prm.dt * S[k * kRS + own];
     }
     __syncthreads();
+    if (threadIdx.x == 0) q_prefetch_l2(prm.Q + tile * B * kRS, B * kRS * sizeof(T));
     {
       T acc[B];
 #pragma unroll
@@ -194,6 +205,7 @@ __global__ void __launch_bounds__(kP * kLanes, 1) ader_neigh(const StepParams<T>
   const int own = p * kLanes + lane;
   for (int64_t it = blockIdx.x; it < prm.ntiles; it += gridDim.x) {
     const int64_t tile = prm.tile0 + it;
+    if (threadIdx.x == 0) q_prefetch_l2(prm.Q + tile * B * kRS, B * kRS * sizeof(T));
     neigh_gather<N, T, 0>(prm, tile, p, lane, Z + 0 * Bt * kRS);
     neigh_gather<N, T, 1>(prm, tile, p, lane, Z + 1 * Bt * kRS);
     neigh_gather<N, T, 2>(prm, tile, p, lane, Z + 2 * Bt * kRS);

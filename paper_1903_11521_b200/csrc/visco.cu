@@ -29,6 +29,13 @@ constexpr int SD = P * TE + 1;   // D / I row stride in doubles (odd: consecutiv
 constexpr int TS = 9 * TE + 12;  // trace row stride
 
 
+// measured (c3, vm_local): 41.63 -> 40.78 ms (YDG_VCOMB) -> 39.60 ms (+ YDG_VQB)
+#ifndef YDG_VCOMB
+#define YDG_VCOMB 1
+#endif
+#ifndef YDG_VQB
+#define YDG_VQB 1
+#endif
 // Bulk L2 prefetch of [p, p + bytes), widened to 16-byte alignment (the instruction's rule).
 __device__ __forceinline__ void l2_prefetch(const void* p, int64_t bytes) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(p), a0 = a & ~uintptr_t(15);
@@ -169,10 +176,18 @@ __device__ __forceinline__ double star_row(int p, const double* cs, const double
 __device__ __forceinline__ double source_row(int p, const double* ce, const double (&m)[18]) {
   double sr = 0.0;
   if (p < 3) {
+#if YDG_VCOMB
+    double s3[3];  // three independent chains (one per mechanism): no 9-deep FMA dependency
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+      s3[l] = fma(ce[p * 9 + 3 * l + 2], m[6 * l + 2], fma(ce[p * 9 + 3 * l + 1], m[6 * l + 1], ce[p * 9 + 3 * l] * m[6 * l]));
+    sr = (s3[0] + s3[1]) + s3[2];
+#else
 #pragma unroll
     for (int l = 0; l < 3; ++l)
 #pragma unroll
       for (int t = 0; t < 3; ++t) sr = fma(ce[p * 9 + 3 * l + t], m[6 * l + t], sr);
+#endif
   } else if (p < 6) {
 #pragma unroll
     for (int l = 0; l < 3; ++l) sr = fma(ce[27 + (p - 3) * 3 + l], m[6 * l + p], sr);
@@ -214,6 +229,44 @@ __device__ __forceinline__ void combine(const double* zr, const double* xr, cons
 #pragma unroll
     for (int u = 0; u < 3; ++u) emit(6 + u, v[u]);
   };
+#if YDG_VCOMB
+  // YDG_VCOMB: every coefficient load of a batch before its stores (the emits write shared
+  // memory, which the compiler must assume aliases the coefficient rows): batch A = the
+  // velocity and stress rows, batch B = the memory variables, each a set of independent
+  // chains
+  {
+    double zs[3][6];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int t = 0; t < 6; ++t) zs[c][t] = zr[c * B * ZS + t * TE];
+    double oa[9];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      double z[3][3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int t = 0; t < 3; ++t) z[c][t] = zs[c][cols[u][t]];
+      oa[6 + u] = star_row<B>(6 + u, cs, z);
+    }
+#pragma unroll
+    for (int p = 0; p < 6; ++p) oa[p] = star_row<B>(p, cs, zv) + source_row(p, ce, m);
+#pragma unroll
+    for (int p = 0; p < 9; ++p) emit(p, oa[p]);
+  }
+  {
+    double base[6], ob[18];
+#pragma unroll
+    for (int p = 9; p < 15; ++p) base[p - 9] = star_row<B>(p, cs, zv);
+#pragma unroll
+    for (int p = 9; p < P; ++p)
+      ob[p - 9] = (p < 15 ? base[p - 9] : wr[(p - 9) / 6] * base[(p - 9) % 6]) + source_row(p, ce, m);
+#pragma unroll
+    for (int p = 9; p < P; ++p) emit(p, ob[p - 9]);
+  }
+  return;
+#endif
   if (VEL_FIRST) vel_rows();
   // memory variables: the star rows of mechanism l are omega_l / omega_0 times those of
   // mechanism 0 (A^d rows -omega_l eps(v); checked at upload), so 6 rows are contracted
@@ -457,11 +510,32 @@ __global__ void __launch_bounds__(NTH, 1) vm_local(const GenParams prm) {
           st2(D + rq[mt] * SD + (p0 + u) * TE + ae, qa[mt][u][0], qa[mt][u][1]);
     __syncthreads();
     double* Qw = prm.Q + e0 * P * B;
+#if YDG_VQB
+    {  // YDG_VQB: every Q^n load of the thread in flight at once (one memory latency)
+      constexpr int NQ = (TE * P * B + NTH - 1) / NTH;
+      const int n = ne * P * B;
+      double qv[NQ];
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) {
+        const int i = tid + j * NTH;
+        qv[j] = i < n ? Qw[i] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) {
+        const int i = tid + j * NTH;
+        if (i < n) {
+          const int ee = i / (P * B), r = i - ee * P * B, p = r / B, kk = r - p * B;
+          Qw[i] = qv[j] + D[kk * SD + p * TE + ee];
+        }
+      }
+    }
+#else
 #pragma unroll 4
     for (int i = tid; i < ne * P * B; i += NTH) {
       const int ee = i / (P * B), r = i - ee * P * B, p = r / B, kk = r - p * B;
       Qw[i] += D[kk * SD + p * TE + ee];
     }
+#endif
   }
 }
 

@@ -97,3 +97,33 @@ def test_bitwise_under_grid_sizes(name, monkeypatch):
     for env, o in zip(GRIDS[1:], outs[1:]):
         same = np.array_equal(o.view(np.uint8), outs[0].view(np.uint8))
         assert same, (name, env, np.abs(o - outs[0]).max())
+
+
+@pytest.mark.parametrize("name", ["fp64-N2-ragged", "fp32-N6", "visco-N4", "generic-fp64-N6", "fused-sims-4"])
+def test_max_abs_q_diagnostic(name, monkeypatch):
+    """ydg_query(YDG_Q_MAX_ABS_Q) (the per-step max|Q| diagnostic of SURVEY §5) equals the
+    maximum of the downloaded DOFs exactly, and turns NaN when one DOF is not finite."""
+    import paper_1903_11521_b200 as ydg
+    cfg, nsteps, kw = CASES[name]
+    sims = kw.get("sims", 1)
+    for k in ("YDG_GUARD", "YDG_GRID_LOCAL", "YDG_GRID_NEIGH"):
+        monkeypatch.delenv(k, raising=False)
+    xyz, vid, mat, Q, an = make_inputs(cfg)
+    h = ydg.ydg_create(cfg.N, cfg.P, cfg.precision)
+    try:
+        if sims > 1:
+            ydg.ydg_set_simulations(h, sims)
+        ydg.ydg_upload_mesh(h, xyz, vid, mat, an)
+        n = int(ydg.ydg_query(h, ydg.YDG_Q_N_ELEMENTS))
+        Qs = (np.concatenate([Q] * sims) if sims > 1 else Q).astype(h.dtype)[:n]
+        ydg.ydg_upload_dofs(h, 0, Qs)
+        assert ydg.ydg_query(h, ydg.YDG_Q_MAX_ABS_Q) == float(np.abs(Qs).max())
+        ydg.ydg_step(h, cfg.dt, nsteps)
+        out = ydg.ydg_download_dofs(h, 0, n)
+        assert ydg.ydg_query(h, ydg.YDG_Q_MAX_ABS_Q) == float(np.abs(out).max())
+        bad = out[n // 2: n // 2 + 1].copy()
+        bad[0, 1, 2] = np.nan
+        ydg.ydg_upload_dofs(h, n // 2, bad)
+        assert np.isnan(ydg.ydg_query(h, ydg.YDG_Q_MAX_ABS_Q))
+    finally:
+        ydg.ydg_destroy(h)
