@@ -350,9 +350,13 @@ def run_ydg(args):
     use_graph = world == 1 and (args.graph == "on" or (args.graph == "auto" and cfg.n_elements < 100000))
     step_fn = ydg.ydg_step_graph if use_graph else ydg.ydg_step
 
-    # warm-up
-    for _ in range(args.warmup):
-        step_fn(h, cfg.dt, 1, stream=sptr)
+    # warm-up (one call of W steps on the large workloads: the same launch sequence as the
+    # timed call, fused kernels included)
+    if flush is None:
+        step_fn(h, cfg.dt, args.warmup, stream=sptr)
+    else:
+        for _ in range(args.warmup):
+            step_fn(h, cfg.dt, 1, stream=sptr)
     torch.cuda.synchronize()
     barrier(world)
 
@@ -365,10 +369,9 @@ def run_ydg(args):
     with Clocks(local) as clk:
         torch.cuda.synchronize()
         barrier(world)
-        if flush is None:
+        if flush is None:  # K steps in one call (what a user advancing a simulation does)
             e0.record(stream)
-            for _ in range(args.steps):
-                step_fn(h, cfg.dt, 1, stream=sptr)
+            step_fn(h, cfg.dt, args.steps, stream=sptr)
             e1.record(stream)
         else:  # L2-resident workload: flush L2 between steps, time each step on its own
             evs = []
@@ -390,6 +393,9 @@ def run_ydg(args):
         torch.cuda.synchronize()
     t_local = ydg.ydg_query(h, ydg.YDG_Q_PROF_LOCAL_MS)
     t_neigh = ydg.ydg_query(h, ydg.YDG_Q_PROF_NEIGH_MS)
+    t_fused = ydg.ydg_query(h, ydg.YDG_Q_PROF_FUSED_MS)
+    # fused step kernel (one rank, fp64, K >= 2 steps in one call): local(0), K - 1 fused, flux(K - 1)
+    fused = world == 1 and flush is None and args.steps >= 2 and ydg.ydg_query(h, ydg.YDG_Q_FUSED) == 1.0
     launches = int(ydg.ydg_query(h, ydg.YDG_Q_PROF_LAUNCHES))
     ydg.ydg_profile(h, False)
     ms_max = allmax(ms, world)
@@ -425,7 +431,9 @@ def run_ydg(args):
     ne_total = cfg.n_elements * args.sims  # element-simulations with fused simulations
     value = ne_total * args.steps / (ms_max / 1e3)
     n_launch = args.steps  # launches per kernel kind (single rank: 1 local + 1 neighbour per step)
-    if world > 1:
+    if fused:
+        n_launch = n_launch_local = 1
+    elif world > 1:
         n_launch_local = max(1, launches - args.steps)
     else:
         n_launch_local = n_launch
@@ -440,11 +448,16 @@ def run_ydg(args):
     dominant = k_loc if t_local >= t_neigh else k_nb
     traffic = load_traffic(cfg.name)
     dom_ach = ach_local if dominant == k_loc else ach_neigh
+    dom_fl = fl_local if dominant == k_loc else fl_neigh
+    if fused:  # the fused kernel carries K - 1 of the K steps: it is the dominant kernel
+        avg_fused = t_fused / (args.steps - 1)
+        dominant, dom_fl = "dm_fused", fl_local + fl_neigh
+        dom_ach = dom_fl * nloc / (avg_fused / 1e3) / 1e12
     roofline = {
         "bound": bound, "achieved": round(dom_ach, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
         "frac": round(dom_ach / peak, 4), "traffic": traffic.get(dominant),
         "kernel": dominant, "peak_source": PEAK_SOURCE,
-        "algorithmic_flops_per_element": fl_local if dominant == k_loc else fl_neigh,
+        "algorithmic_flops_per_element": dom_fl,
         "elements_per_launch": nloc,
     }
     kernels = {
@@ -459,6 +472,17 @@ def run_ydg(args):
                "alg_hbm_gbs": round(by_neigh * nloc / (avg_neigh / 1e3) / 1e9, 1),
                "nz_flops_per_element": fl_neigh, "alg_bytes_per_element": by_neigh},
     }
+    if fused:
+        by_fused = ydg.ydg_query(h, ydg.YDG_Q_FUSED_BYTES)
+        kernels["dm_fused"] = {
+            "ms_per_launch": round(avg_fused, 4), "launches": args.steps - 1, "tflops": round(dom_ach, 3),
+            "frac_peak": round(dom_ach / peak, 4),
+            "frac_peak_executed": round(dom_ach * (fl_local + fl_neigh_exec) / dom_fl / peak, 4),
+            "alg_hbm_gbs": round(by_fused * nloc / (avg_fused / 1e3) / 1e9, 1),
+            "nz_flops_per_element": dom_fl, "executed_nz_flops_per_element": fl_local + fl_neigh_exec,
+            "alg_bytes_per_element": by_fused,
+            "what": "flux of step n-1 + local part of step n per tile (one launch per step after the first)"}
+        kernels[k_loc]["launches"] = kernels[k_nb]["launches"] = 1
     hw = load_hw_flops(cfg.name) if args.sims == 1 else {}
     for kname, avg in ((k_loc, avg_local), (k_nb, avg_neigh)):
         f = hw.get(kname)
@@ -496,7 +520,8 @@ def run_ydg(args):
                 "steps_per_call": cfg.steps,
                 "call": "ydg_upload_dofs(pinned host) + %s(dt, %d) + ydg_download_dofs(pinned host)"
                         % ("ydg_step_graph" if use_graph else "ydg_step", cfg.steps)},
-        "gpu_launches": args.steps * per_step_launch, "cuda_graph": use_graph,
+        "gpu_launches": (args.steps + 1 if fused else args.steps * per_step_launch), "cuda_graph": use_graph,
+        "fused_step_kernel": fused,
         "clocks": clocks, "finite": finite, "max_abs_q": max_abs_q, "setup_s": round(setup_s, 1),
     }
     print(json.dumps(line), flush=True)

@@ -73,9 +73,16 @@ enum {
                                   synchronises the device and returns the number of guard
                                   bytes overwritten (0 = no out-of-bounds store seen), -1 when
                                   the handle has no guards, -2 on a CUDA error              */
-  YDG_Q_MAX_ABS_Q = 21         /* diagnostic: max |Q| over the owned DOFs (a reduction
+  YDG_Q_MAX_ABS_Q = 21,        /* diagnostic: max |Q| over the owned DOFs (a reduction
                                   kernel on the handle's stream, synchronised); NaN when any
                                   DOF is NaN or infinite                                     */
+  YDG_Q_FUSED = 22,            /* 1 when ydg_step(nsteps >= 2) runs the fused step kernel
+                                  (opt-in: YDG_FUSED=1 in the environment at mesh upload;
+                                  fp64 elastic tensor-core path, one rank, room for a second
+                                  trace buffer), else 0                                      */
+  YDG_Q_PROF_FUSED_MS = 23,    /* profiling: summed device time of fused-kernel launches    */
+  YDG_Q_FUSED_BYTES = 24       /* algorithmic bytes / element of the fused kernel (Q read
+                                  and written once; traces written, own + neighbour read)    */
 };
 
 typedef struct ydg_solver ydg_solver; /* opaque, owned by the library */
@@ -139,7 +146,11 @@ int ydg_download_dofs_device(ydg_solver* h, int64_t first, int64_t count, void* 
 
 /* Advance all owned elements by nsteps global time steps of size dt.
  * Enqueued on cuda_stream (NULL = the handle's own stream); returns without waiting.
- * Collective over the ranks of ydg_set_comm: all must call with the same dt, nsteps. */
+ * Collective over the ranks of ydg_set_comm: all must call with the same dt, nsteps.
+ * Launches: two per step (local part, flux); with YDG_Q_FUSED = 1 and nsteps >= 2,
+ * nsteps + 1: the local part of step 0, nsteps - 1 fused kernels (flux of step n - 1, then
+ * the local part of step n, per tile; the traces alternate between two buffers) and the
+ * flux of the last step.  Either way Q holds the complete state when the call's work ends. */
 int ydg_step(ydg_solver* h, double dt, int nsteps, void* cuda_stream);
 
 /* Same as ydg_step, launched as one CUDA graph: the 2 * nsteps kernel launches of (dt,

@@ -28,7 +28,8 @@ YDG_OK, YDG_ERR_ARG, YDG_ERR_STATE, YDG_ERR_CUDA, YDG_ERR_NCCL, YDG_ERR_MESH, YD
  YDG_Q_BTILDE, YDG_Q_DEVICE_BYTES, YDG_Q_LAUNCHES_PER_STEP, YDG_Q_LOCAL_BYTES, YDG_Q_NEIGH_BYTES,
  YDG_Q_LOCAL_FLOPS, YDG_Q_NEIGH_FLOPS, YDG_Q_PROF_LOCAL_MS, YDG_Q_PROF_NEIGH_MS,
  YDG_Q_PROF_LAUNCHES, YDG_Q_KERNEL_PATH, YDG_Q_SIMULATIONS, YDG_Q_TILE_ELEMENTS,
- YDG_Q_NEIGH_FLOPS_EXEC, YDG_Q_GUARD_VIOLATIONS, YDG_Q_MAX_ABS_Q) = range(22)
+ YDG_Q_NEIGH_FLOPS_EXEC, YDG_Q_GUARD_VIOLATIONS, YDG_Q_MAX_ABS_Q, YDG_Q_FUSED, YDG_Q_PROF_FUSED_MS,
+ YDG_Q_FUSED_BYTES) = range(25)
 
 EXPORTS = ("ydg_create", "ydg_last_error", "ydg_set_comm", "ydg_set_simulations", "ydg_upload_mesh", "ydg_upload_dofs",
            "ydg_upload_dofs_device", "ydg_download_dofs_device", "ydg_step", "ydg_step_graph", "ydg_set_clusters", "ydg_step_lts", "ydg_synchronize",

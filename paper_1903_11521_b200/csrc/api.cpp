@@ -45,6 +45,8 @@ struct ydg_solver {
   // device buffers
   void* Q = nullptr;
   void* traces = nullptr;
+  void* traces2 = nullptr;  // fused step kernel: the other trace buffer (steps alternate)
+  bool fused = false;       // ydg_step(nsteps >= 2) runs the fused kernel
   void* star = nullptr;
   void* aplus = nullptr;
   void* aminus = nullptr;
@@ -63,11 +65,12 @@ struct ydg_solver {
   int8_t* jh_e = nullptr;   // [e][4]
   std::vector<void*> csr;   // device CSR arrays (freed in ydg_destroy)
   GenParams gp{};
-  // profiling: (start, stop, kind) events of timed launches; kind 0 = local, 1 = neighbour
+  // profiling: (start, stop, kind) events of timed launches; kind 0 = local, 1 = neighbour,
+  // 2 = fused
   bool profiling = false;
   struct Ev { cudaEvent_t a, b; int kind; };
   std::vector<Ev> pending;
-  double prof_ms[2] = {0, 0};
+  double prof_ms[3] = {0, 0, 0};  // local, neighbour, fused
   int64_t prof_launches = 0;
   // ydg_step_graph: the launch sequence of (dt, nsteps) captured once into a CUDA graph
   cudaStream_t cap_stream = nullptr;
@@ -130,7 +133,7 @@ void dfree(ydg_solver* h, void* p) {
 }
 
 void free_mesh(ydg_solver* h) {
-  for (void** p : {&h->Q, &h->traces, &h->star, &h->aplus, &h->aminus, &h->staging, &h->src,
+  for (void** p : {&h->Q, &h->traces, &h->traces2, &h->star, &h->aplus, &h->aminus, &h->staging, &h->src,
                    reinterpret_cast<void**>(&h->slot_of), reinterpret_cast<void**>(&h->nb_lts[0]),
                    reinterpret_cast<void**>(&h->nb_lts[1]), reinterpret_cast<void**>(&h->nb_lts[2]),
                    reinterpret_cast<void**>(&h->lts_lst[0]), reinterpret_cast<void**>(&h->lts_lst[1]),
@@ -143,6 +146,7 @@ void free_mesh(ydg_solver* h) {
   h->device_bytes = 0;
   h->have_mesh = false;
   h->lts = false;
+  h->fused = false;
   if (h->gexec) cudaGraphExecDestroy(h->gexec);  // captured the old buffers
   h->gexec = nullptr;
   h->g_n = -1;
@@ -319,6 +323,13 @@ double alg_bytes_neigh(const ydg_solver* h) {
   return (2 * B * P + 4 * P * P + 4 * Bt * P) * elem_bytes(h) + 4 * (4 + 1);
 }
 
+// fused kernel (fp64): Q read and written once, star, the 4 trace blocks written, own and
+// neighbour trace blocks read, the factored flux solvers, neighbour slots and j|h
+double alg_bytes_fused(const ydg_solver* h) {
+  const double P = h->P, B = h->B;
+  return (2 * B * P + 3 * P * 3 + 4 * kFaceCoeffs + 3 * 4 * trace_block(h)) * elem_bytes(h) + 4 * (4 + 1);
+}
+
 // Wrap a launch with CUDA events when profiling.
 template <typename F>
 cudaError_t timed(ydg_solver* h, int kind, cudaStream_t s, F&& launch) {
@@ -361,6 +372,28 @@ int do_step(ydg_solver* h, double dt, int nsteps, cudaStream_t s) {
   for (int d = 0; d < h->N; ++d) {
     prm.scal[d] = static_cast<T>(dt / (d + 1));
     prm.scal[h->N + d] = static_cast<T>(dt / (d + 2));
+  }
+  if constexpr (sizeof(T) == 8) {
+    if (h->fused && h->nranks == 1 && nsteps >= 2) {
+      // local(0) -> traces A; fused(n) = flux of step n-1 from one buffer + local(n) into the
+      // other; flux of the last step
+      T* tb[2] = {static_cast<T*>(h->traces), static_cast<T*>(h->traces2)};
+      prm.tile0 = 0;
+      prm.ntiles = h->ntiles;
+      const int gl = static_cast<int>(std::min<int64_t>(h->grid_local, prm.ntiles));
+      prm.traces = tb[0];
+      CUDA_OR_FAIL(h, timed(h, 0, s, [&] { return launch_local<T>(h->N, prm, gl, s); }));
+      for (int n = 1; n < nsteps; ++n) {
+        prm.traces_in = tb[(n - 1) & 1];
+        prm.traces = tb[n & 1];
+        CUDA_OR_FAIL(h, timed(h, 2, s, [&] { return launch_fused(h->N, prm, gl, s); }));
+      }
+      prm.traces = tb[(nsteps - 1) & 1];
+      prm.traces_in = nullptr;
+      const int64_t units = prm.ntiles * (h->lanes / 8);
+      CUDA_OR_FAIL(h, timed(h, 1, s, [&] { return launch_neigh<T>(h->N, prm, static_cast<int>(std::min<int64_t>(h->grid_neigh, units)), s); }));
+      return YDG_OK;
+    }
   }
   for (int n = 0; n < nsteps; ++n) {
     if (h->nranks > 1) {
@@ -961,6 +994,19 @@ static int upload_tiled(ydg_solver* h, const double* xyz, const double* material
   if ((rc = dalloc(h, reinterpret_cast<void**>(&h->jh), jh_local.size()))) { free_mesh(h); return rc; }
   CUDA_OR_FAIL(h, cudaMemset(h->Q, 0, q_n * eb));
   CUDA_OR_FAIL(h, cudaMemset(h->traces, 0, tr_n * eb));
+  // fused step kernel (YDG_FUSED=1; measured slower: the two kernels' code
+  // does not fit the SM's instruction cache together): a second trace buffer, if the device
+  // has room for it with 2 GB to spare
+  {
+    const char* fz = std::getenv("YDG_FUSED");
+    size_t fr = 0, tot = 0;
+    if (eb == 8 && h->nranks == 1 && kDmLanes == 8 && fz && std::atoi(fz) == 1 &&
+        cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr > tr_n * eb + (size_t(2) << 30) &&
+        dalloc(h, &h->traces2, tr_n * eb) == YDG_OK) {
+      CUDA_OR_FAIL(h, cudaMemset(h->traces2, 0, tr_n * eb));
+      h->fused = true;
+    }
+  }
   CUDA_OR_FAIL(h, cudaMemcpy(h->nb, nb_local.data(), nb_local.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   CUDA_OR_FAIL(h, cudaMemcpy(h->jh, jh_local.data(), jh_local.size(), cudaMemcpyHostToDevice));
   if (h->lts) {
@@ -1249,14 +1295,14 @@ int ydg_profile(ydg_solver* h, int enable) {
   if (rc) return rc;
   if ((rc = drain_profile(h))) return rc;
   h->profiling = enable != 0;
-  h->prof_ms[0] = h->prof_ms[1] = 0;
+  h->prof_ms[0] = h->prof_ms[1] = h->prof_ms[2] = 0;
   h->prof_launches = 0;
   return YDG_OK;
 }
 
 int ydg_query(ydg_solver* h, int what, double* v) {
   if (!h || !v) return YDG_ERR_ARG;
-  if (what >= YDG_Q_PROF_LOCAL_MS && what <= YDG_Q_PROF_LAUNCHES) {
+  if ((what >= YDG_Q_PROF_LOCAL_MS && what <= YDG_Q_PROF_LAUNCHES) || what == YDG_Q_PROF_FUSED_MS) {
     int rc = check(h);
     if (rc) return rc;
     if ((rc = drain_profile(h))) return rc;
@@ -1265,6 +1311,9 @@ int ydg_query(ydg_solver* h, int what, double* v) {
     case YDG_Q_PROF_LOCAL_MS: *v = h->prof_ms[0]; break;
     case YDG_Q_PROF_NEIGH_MS: *v = h->prof_ms[1]; break;
     case YDG_Q_PROF_LAUNCHES: *v = static_cast<double>(h->prof_launches); break;
+    case YDG_Q_PROF_FUSED_MS: *v = h->prof_ms[2]; break;
+    case YDG_Q_FUSED: *v = h->fused ? 1.0 : 0.0; break;
+    case YDG_Q_FUSED_BYTES: *v = h->prec == 8 && !h->generic ? alg_bytes_fused(h) : 0.0; break;
     case YDG_Q_SIMULATIONS: *v = static_cast<double>(h->sims); break;
     case YDG_Q_GUARD_VIOLATIONS: *v = h->guard ? static_cast<double>(guard_violations(h)) : -1.0; break;
     case YDG_Q_MAX_ABS_Q: {

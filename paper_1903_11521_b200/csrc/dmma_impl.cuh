@@ -77,6 +77,7 @@ struct Ctx {
   double dt;
   int tid, grp;       // thread index within the (group of the) CTA, group index
   int shcap;          // grouped local kernel: fragments held in the shared buffer
+  bool lfs;           // flux: the lift's A fragments are staged in shared memory (x.fs)
   __device__ __forceinline__ void sync() const {  // barrier of the thread's group
     if (kLocalGroups == 1) __syncthreads();
     else asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "n"(kT) : "memory");
@@ -140,7 +141,9 @@ __device__ __forceinline__ double afrag_l(const Ctx& x, int g, int r) {
   if constexpr (kLocalGroups > 1) return afrag(x, g);
   return (kLocalFs && r < kLocalFsCap) ? afrag_s(x, r) : afrag_g(x, g);
 }
-__device__ __forceinline__ double afrag_f(const Ctx& x, int g, int r) { return kFluxFs ? afrag_s(x, r) : afrag_g(x, g); }
+__device__ __forceinline__ double afrag_f(const Ctx& x, int g, int r) {
+  return (kFluxFs && x.lfs) ? afrag_s(x, r) : afrag_g(x, g);
+}
 // L2 eviction hints on the streaming stores (bit mask, build flag): 1 = trace bulk stores of
 // the local kernel, 2 = its Q stores, 4 = the flux kernel's Q stores -- evict_first, so that
 // the Q^n rows a tile re-reads stay in L2
@@ -162,9 +165,11 @@ __device__ __forceinline__ void st_q2(double* p, double2 v) {
     *reinterpret_cast<double2*>(p) = v;
   }
 }
+// Coherent (not .nc): in the fused kernel the tile's Q was written by its own flux phase
+// earlier in the same launch, which the non-coherent read-only path need not observe.
 __device__ __forceinline__ double ld_stream(const double* p) {
   double v;
-  asm("ld.global.nc.L1::evict_first.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  asm volatile("ld.global.L1::evict_first.f64 %0, [%1];" : "=d"(v) : "l"(p));  // volatile: kept after the barriers
   return v;
 }
 // star matrices of the tile: read by the star-chunk role at the tile start and again by every
@@ -585,6 +590,16 @@ struct Layout {
   static constexpr int FLUX = 2 * FACEF + 2 * G::Bt * kRSF + kFaceCoeffs * kLF + 16 + 2;  // + slots, j|h, mbarriers
   static constexpr int FLUXG = (FLUX + 15) & ~15;  // one group's region (128-byte aligned)
   static constexpr int FLUXCTA = kFluxGroups * FLUXG + (kFluxFs ? G::LIFT_NF * 32 : 0);
+  // fused kernel (dm_fused: flux of the previous step, then the local part, per tile): a
+  // group region holds either phase's buffers (FOFF doubles of the local part, FLUXDATA of
+  // the flux part), then four mbarriers (local: fragments, Q rows; flux: own, neighbour);
+  // the shared A-fragment slots (CK step 0, the volume) take the rest of the 227 KB
+  static constexpr int FLUXDATA = 2 * FACEF + 2 * G::Bt * kRSF + kFaceCoeffs * kLF + 16;
+  static constexpr int FBAR = FOFF > FLUXDATA ? FOFF : FLUXDATA;
+  static constexpr int FUSEDG = (FBAR + 4 + 15) & ~15;
+  static constexpr int LSHF0 = (227 * 1024 / 8 - kLocalGroups * FUSEDG) / 32;
+  static constexpr int LSHF = LSHF0 < G::LIFT_F0 ? LSHF0 : G::LIFT_F0;
+  static constexpr int FUSEDCTA = kLocalGroups * FUSEDG + LSHF * 32;
 };
 
 // ---- asynchronous copy helpers (TMA bulk copies + mbarrier, Ampere-style cp.async)
@@ -684,35 +699,50 @@ __device__ __forceinline__ void after_ck0(Ctx& x) {
 // CK + time integral, face traces R^iT I (stored for the flux kernel) and
 // the volume term for 32-element tiles.
 template <int N>
-__global__ void __launch_bounds__(kT * kLocalGroups, kLocalGroups == 1 ? kDmCtasPerSm : 1)
-    dm_local(const __grid_constant__ StepParams<double> prm) {
+__device__ __forceinline__ void flux_tile(Ctx& x, const StepParams<double>& prm, int64_t tile, double* smem,
+                                          unsigned long long* bar, unsigned& ph_o, unsigned& ph_n);
+
+// Body of the local kernel (FUSED = false) and of the fused step kernel (FUSED = true: each
+// tile first receives the flux of the previous step from prm.traces_in -- flux_tile, the
+// flux kernel's per-unit work -- then runs the local part, whose traces go to prm.traces).
+template <int N, bool FUSED>
+__device__ __forceinline__ void local_body(const StepParams<double>& prm) {
   using G = DG<N>;
   using Lay = Layout<N>;
   constexpr int B = G::B;
+  constexpr int GS = FUSED ? Lay::FUSEDG : Lay::LOCALG;  // group region (doubles)
+  static_assert(!FUSED || (kLocalGroups > 1 && kL == kLF), "fused kernel: grouped 8-element tiles");
   extern __shared__ __align__(128) double smem_cta[];
   Ctx x;
   init_ctx(x);
-  double* smem = smem_cta + x.grp * Lay::LOCALG;  // this group's region
+  x.lfs = false;
+  x.qcol0 = 3 * x.w * kL;  // flux phase (8-element tiles: the unit is the tile)
+  double* smem = smem_cta + x.grp * GS;  // this group's region
   // group grp of the CTA works as virtual CTA vb of a grid of vgrid
   const int64_t vb = static_cast<int64_t>(blockIdx.x) * kLocalGroups + x.grp;
   const int64_t vgrid = static_cast<int64_t>(gridDim.x) * kLocalGroups;
-  x.shcap = Lay::LSH;
+  x.shcap = FUSED ? Lay::LSHF : Lay::LSH;
   x.I = smem;
   x.S = smem + G::IROWS * kRS;
   x.xb = smem + Lay::ROWS * kRS + x.w * kXBUF * kXW;
   x.frags = frag_table<N>();
-  x.fs = kLocalGroups > 1 ? smem_cta + kLocalGroups * Lay::LOCALG : smem + Lay::FOFF;
-  x.fbar = reinterpret_cast<unsigned long long*>(smem + Lay::FOFF + Lay::FSMAX * 32);
+  x.fs = kLocalGroups > 1 ? smem_cta + kLocalGroups * GS : smem + Lay::FOFF;
+  x.fbar = reinterpret_cast<unsigned long long*>(smem + (FUSED ? Lay::FBAR : Lay::FOFF + Lay::FSMAX * 32));
   unsigned long long* qbar = x.fbar + 1;
-  unsigned qph = 0;
+  unsigned long long* fxbar = x.fbar + 2;  // fused: the flux phase's own / neighbour copies
+  unsigned qph = 0, ph_o = 0, ph_n = 0;
   if constexpr (kLocalGroups > 1) {  // static fragment buffer: CK step 0, then the volume
     double* fs = const_cast<double*>(x.fs);
-    for (int i = threadIdx.x; i < Lay::LSH * 32; i += kT * kLocalGroups) fs[i] = x.frags[i];
+    for (int i = threadIdx.x; i < x.shcap * 32; i += kT * kLocalGroups) fs[i] = x.frags[i];
     __syncthreads();
   }
   if (x.tid == 0) {
     mbar_init(x.fbar, 1);
     mbar_init(qbar, 1);
+    if constexpr (FUSED) {
+      mbar_init(&fxbar[0], 1);
+      mbar_init(&fxbar[1], 1);
+    }
     if (kLocalFs && vb < prm.ntiles) stage_frags<N>(x, G::CK0_F0, G::CK0_NF < kLocalFsCap ? G::CK0_NF : kLocalFsCap);
   }
   x.sync();
@@ -745,6 +775,12 @@ __global__ void __launch_bounds__(kT * kLocalGroups, kLocalGroups == 1 ? kDmCtas
       prefetch_l2(prm.star + nt * 3 * kP * 3 * kL, 3 * kP * 3 * kL * sizeof(double));
     }
     x.Qt = Qt;
+    if constexpr (FUSED) {  // the previous step's flux into Q (in L2 for the staging below)
+      flux_tile<N>(x, prm, tile, smem, fxbar, ph_o, ph_n);
+      // the Q rows < IROWS are re-read by a bulk copy (async proxy) after the volume term
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      x.sync();
+    }
     {  // stage Q^n of the tile in shared memory (rows of I, continuing into S): 16-byte
        // cp.async chunks, all in flight at once
       constexpr int kChunks = B * kRS / 2;
@@ -806,7 +842,7 @@ __global__ void __launch_bounds__(kT * kLocalGroups, kLocalGroups == 1 ? kDmCtas
       if (x.tid == 0) bulk_s2g(gtr + F * Lay::FACE, stg, Lay::FACE * sizeof(double));
     }
     YDG_PHASE(8);
-    if (prm.tr_only) {  // LTS: the sub-interval traces of a coarse element, no update
+    if (!FUSED && prm.tr_only) {  // LTS: the sub-interval traces of a coarse element, no update
       if (x.tid == 0) bulk_wait_read<0>();
       x.sync();
       continue;
@@ -852,6 +888,21 @@ __global__ void __launch_bounds__(kT * kLocalGroups, kLocalGroups == 1 ? kDmCtas
   if (x.tid == 0) bulk_wait_all();
 }
 
+template <int N>
+__global__ void __launch_bounds__(kT * kLocalGroups, kLocalGroups == 1 ? kDmCtasPerSm : 1)
+    dm_local(const __grid_constant__ StepParams<double> prm) {
+  local_body<N, false>(prm);
+}
+
+// Fused step kernel: per tile, the flux of the previous step (own and neighbour traces from
+// prm.traces_in) added to Q, then CK, time integral, traces (-> prm.traces) and
+// the volume term of this step.  The tile's Q is read from HBM once and written
+// once per step; the flux phases' memory latency overlaps the other groups' tensor-core work.
+template <int N>
+__global__ void __launch_bounds__(kT * kLocalGroups, 1) dm_fused(const __grid_constant__ StepParams<double> prm) {
+  if constexpr (kLocalGroups > 1 && kL == kLF) local_body<N, true>(prm);
+}
+
 // Flux kernel: local and neighbour flux with one lift per face:
 //   Q += sum_i R^i ( T_i A+_i^T + (f^h_i T^nb_(j_i)) A-_i^T ).
 // Per (tile, face) item: one TMA bulk copy of the tile's own face block (buffer O) and one
@@ -886,6 +937,7 @@ __global__ void __launch_bounds__(kTF * kFluxGroups, kFluxGroups == 1 ? kFluxCta
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(JHX + kJH);  // own, nb
   Ctx x;
   x.shcap = 0;  // (the local kernel's shared fragment slots)
+  x.lfs = true;
   x.lane = tid & 31;
   x.w = tid >> 5;
   x.col0 = 3 * x.w * kLF;
@@ -1037,6 +1089,109 @@ __global__ void __launch_bounds__(kTF * kFluxGroups, kFluxGroups == 1 ? kFluxCta
         else G::template lift2<1>(x, Y0, Y0 + Bt * kRSF, Qt);
         gsync();
       }
+    }
+  }
+}
+
+// Flux phase of the fused kernel for one 8-element tile (= one flux unit): the per-face work
+// of dm_flux -- own face block, flux coefficients and j|h by one bulk copy group, the eight
+// neighbour face blocks by another (the next face's copies in flight while this face
+// computes), f^h rotation, Godunov flux, paired lift + Q update -- on this group's region
+// (the local phase's buffers are dead here).  Traces come from prm.traces_in.
+template <int N>
+__device__ __forceinline__ void flux_tile(Ctx& x, const StepParams<double>& prm, int64_t tile, double* smem,
+                                          unsigned long long* bar, unsigned& ph_o, unsigned& ph_n) {
+  using G = DG<N>;
+  using Lay = Layout<N>;
+  constexpr int B = G::B, Bt = G::Bt, TS = G::TS, FACE = Lay::FACE, FACEF = Lay::FACEF;
+  constexpr int FCN = kFaceCoeffs * kLF;
+  const int tid = x.tid;
+  double* O = smem;
+  double* NB = smem + FACEF;
+  double* Y0 = smem + 2 * FACEF;
+  double* FC = Y0 + 2 * Bt * kRSF;
+  int32_t* NBX = reinterpret_cast<int32_t*>(FC + FCN);
+  int8_t* JH = reinterpret_cast<int8_t*>(NBX + kLF);
+  int8_t* JHX = JH + kJH;
+  const double* tin = prm.traces_in;
+  auto issue_own = [&](int F, bool next) {  // thread 0: item (tile, F); slots, j|h of (tile, F + 1)
+    const int64_t item = tile * 4 + F;
+    mbar_expect_tx(&bar[0], (FACEF + FCN) * sizeof(double) + kJH + (next ? kLF * 4 + kJH : 0));
+    bulk_g2s(O, tin + item * FACE, FACEF * sizeof(double), &bar[0]);
+#pragma unroll
+    for (int k = 0; k < kFaceCoeffs; ++k)
+      bulk_g2s(FC + k * kLF, prm.aplus + (item * kFaceCoeffs + k) * kL, kLF * sizeof(double), &bar[0]);
+    bulk_g2s(JH, prm.jh + item * kJH, kJH, &bar[0]);
+    if (next) {
+      bulk_g2s(NBX, prm.nb + (item + 1) * kL, kLF * 4, &bar[0]);
+      bulk_g2s(JHX, prm.jh + (item + 1) * kJH, kJH, &bar[0]);
+    }
+  };
+  auto issue_nb = [&](const int32_t* nbs, const int8_t* jhs) {  // thread 0
+    mbar_expect_tx(&bar[1], FACEF * sizeof(double));
+#pragma unroll
+    for (int e = 0; e < kLF; ++e) {
+      const int64_t nbe = nbs[e];
+      bulk_g2s(NB + e * TS, tin + ((nbe / kL) * 4 + (jhs[e] & 3)) * FACE + (nbe % kL) * TS, TS * sizeof(double),
+               &bar[1]);
+    }
+  };
+  if (tid == 0) {
+    fence_proxy_async();  // the local phase's generic accesses to the region, then the copies
+    int32_t nbs[kLF];
+    int8_t jhs[kLF];
+#pragma unroll
+    for (int e = 0; e < kLF; ++e) {
+      nbs[e] = prm.nb[tile * 4 * kL + e];
+      jhs[e] = prm.jh[tile * 4 * kJH + e];
+    }
+    issue_nb(nbs, jhs);
+    issue_own(0, true);
+  } else if (tid == 32) {
+    prefetch_l2(prm.Q + tile * B * kRS, B * kRS * sizeof(double));  // the lifts' read-modify-write
+  }
+  const int re = tid % kLF, rp = tid / kLF;
+  double* Qt = prm.Q + tile * B * kRS;
+#pragma unroll
+  for (int F = 0; F < 4; ++F) {
+    double* Y = Y0 + (F & 1) * Bt * kRSF;
+    mbar_wait(&bar[0], ph_o);  // own block, coefficients, j|h of this face; slots of the next
+    ph_o ^= 1;
+    mbar_wait(&bar[1], ph_n);  // neighbour blocks of this face
+    ph_n ^= 1;
+    if (tid < kP * kLF) {  // z = f^h t on column rp of element re's neighbour block -> Y
+      const int h = JH[re] >> 2;
+      const double* zc = NB + re * TS + rp;
+      double t[Bt];
+#pragma unroll
+      for (int n = 0; n < Bt; ++n) t[n] = zc[n * kP];
+      G::rotf(h, t, Y, rp * kLF + re);
+    }
+    double fc[kFaceCoeffs];
+#pragma unroll
+    for (int k = 0; k < kFaceCoeffs; ++k) fc[k] = FC[k * kLF + re];
+    x.sync();  // rotated rows visible; every read of NB (and of NBX, JHX) done
+    if (tid == 0 && F < 3) issue_nb(NBX, JHX);
+    {  // Godunov flux of rows m = rp, rp + 12, ... of element re, in place in Y
+      const double* T = O + re * TS;
+#pragma unroll
+      for (int i = 0; i < (Bt + kTF / kLF - 1) / (kTF / kLF); ++i) {
+        const int m = rp + (kTF / kLF) * i;
+        if (m >= Bt) break;
+        double z[kP], y[kP];
+#pragma unroll
+        for (int q = 0; q < kP; ++q) z[q] = Y[swzf(m, q * kLF + re)];
+        godunov_flux(T + m * kP, z, fc, y);
+#pragma unroll
+        for (int q = 0; q < kP; ++q) Y[swzf(m, q * kLF + re)] = y[q];
+      }
+    }
+    x.sync();  // every read of O, FC, JH done; Y complete
+    if (tid == 0 && F < 3) issue_own(F + 1, F + 1 < 3);
+    if (F & 1) {  // lift of the face pair + Q update; the pair's Y buffers are reused after
+      if (F == 1) G::template lift2<0>(x, Y0, Y0 + Bt * kRSF, Qt);
+      else G::template lift2<1>(x, Y0, Y0 + Bt * kRSF, Qt);
+      if (F == 1) x.sync();
     }
   }
 }

@@ -39,6 +39,18 @@ const void* local_fn_N6(int eb);
 const void* neigh_fn_N6(int eb);
 size_t local_smem_N6(int eb);
 size_t neigh_smem_N6(int eb);
+const void* fused_fn_N1();
+size_t fused_smem_N1();
+const void* fused_fn_N2();
+size_t fused_smem_N2();
+const void* fused_fn_N3();
+size_t fused_smem_N3();
+const void* fused_fn_N4();
+size_t fused_smem_N4();
+const void* fused_fn_N5();
+size_t fused_smem_N5();
+const void* fused_fn_N6();
+size_t fused_smem_N6();
 
 namespace {
 
@@ -149,6 +161,29 @@ size_t neigh_smem_bytes(int N, int eb) {
   return 0;
 }
 
+const void* pick_fused(int N) {
+  switch (N) {
+    case 1: return fused_fn_N1();
+    case 2: return fused_fn_N2();
+    case 3: return fused_fn_N3();
+    case 4: return fused_fn_N4();
+    case 5: return fused_fn_N5();
+    case 6: return fused_fn_N6();
+  }
+  return nullptr;
+}
+size_t fused_smem_bytes(int N) {
+  switch (N) {
+    case 1: return fused_smem_N1();
+    case 2: return fused_smem_N2();
+    case 3: return fused_smem_N3();
+    case 4: return fused_smem_N4();
+    case 5: return fused_smem_N5();
+    case 6: return fused_smem_N6();
+  }
+  return 0;
+}
+
 cudaError_t configure_kernels(int N, int eb) {
   const void* fl = pick_local(N, eb);
   const void* fn = pick_neigh(N, eb);
@@ -160,7 +195,21 @@ cudaError_t configure_kernels(int N, int eb) {
   // all of the unified L1 / shared memory as shared memory (two fp64 CTAs per SM)
   if (e == cudaSuccess) e = cudaFuncSetAttribute(fl, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e == cudaSuccess && eb == 8) {
+    const void* ff = pick_fused(N);
+    e = cudaFuncSetAttribute(ff, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fused_smem_bytes(N)));
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(ff, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  }
   return e;
+}
+
+// grid counts work groups (virtual CTAs) as for the local kernel
+cudaError_t launch_fused(int N, const StepParams<double>& p, int grid, cudaStream_t s) {
+  const void* f = pick_fused(N);
+  if (!f) return cudaErrorInvalidValue;
+  void* args[] = {const_cast<StepParams<double>*>(&p)};
+  const int ctas = (grid + kLocalGroups - 1) / kLocalGroups;
+  return cudaLaunchKernel(f, dim3(ctas), dim3(block_threads(8)), args, fused_smem_bytes(N), s);
 }
 
 template <typename T>

@@ -48,6 +48,7 @@ struct StepParams {
   T scal[2 * kMaxN];     // dt/(d+1), d < N ; dt/(d+2), d < N
   T dt;
   int tr_only;           // fp64 local kernel: traces of I only, no volume update (LTS)
+  const T* traces_in;    // fp64 fused kernel: the previous step's traces (its flux phase's input)
 };
 
 // host launchers (kernels.cu)
@@ -55,6 +56,9 @@ template <typename T>
 cudaError_t launch_local(int N, const StepParams<T>& p, int grid, cudaStream_t s);
 template <typename T>
 cudaError_t launch_neigh(int N, const StepParams<T>& p, int grid, cudaStream_t s);
+// fp64 fused step kernel (flux of the previous step + local part of this one, per tile)
+cudaError_t launch_fused(int N, const StepParams<double>& p, int grid, cudaStream_t s);
+size_t fused_smem_bytes(int N);
 template <typename T>
 cudaError_t launch_to_tiled(int P, int B, int L, const T* canon, T* tiled, int64_t first, int64_t count,
                             const int32_t* slot_of, cudaStream_t s);

@@ -328,3 +328,49 @@ def test_lts_rejects_ragged_coarse_cluster():
         ydg.ydg_upload_mesh(h, xyz, vid, mat)
     assert ei.value.code == ydg.YDG_ERR_ARG
     ydg.ydg_destroy(h)
+
+
+@pytest.mark.parametrize("N,cubes,vperm", [(2, 3, True), (3, 3, True), (5, 4, True), (5, 6, False)])
+def test_fused_step_kernel_is_bitwise_two_kernel_steps(monkeypatch, N, cubes, vperm):
+    """With YDG_FUSED=1, ydg_step(nsteps >= 2) on one rank runs the fused kernel (the flux of step n-1, then the
+    local part of step n, per tile; traces in two alternating buffers).  It performs the same
+    operations in the same order as the two-kernel steps (YDG_FUSED=0), so the results are
+    bitwise equal -- over calls of 1, 2 and 5 steps, on meshes with every (i, j, h) face case
+    and a ragged last tile -- and match the oracle."""
+    import paper_1903_11521_b200 as ydg
+    cfg = synth.CONFIGS["c0"].with_(N=N, nx=cubes, ny=cubes, nz=cubes, vperm=vperm, name=f"fused-N{N}")
+    xyz, vid, mat, Q, _ = make_inputs(cfg)
+    outs = []
+    for fz in ("1", "0"):
+        monkeypatch.setenv("YDG_FUSED", fz)
+        h = ydg.ydg_create(cfg.N, 9, 8)
+        ydg.ydg_upload_mesh(h, xyz, vid, mat)
+        assert ydg.ydg_query(h, ydg.YDG_Q_FUSED) == (1.0 if fz == "1" else 0.0)
+        ydg.ydg_upload_dofs(h, 0, Q)
+        for n in (1, 2, 5):
+            ydg.ydg_step(h, cfg.dt, n)
+        outs.append(ydg.ydg_download_dofs(h, 0, cfg.n_elements))
+        ydg.ydg_destroy(h)
+    assert np.array_equal(outs[0], outs[1])
+    ref = run_oracle(cfg, xyz, vid, mat, Q, nsteps=8)
+    check_parity(rel_err(outs[0], ref), 8, cfg.name)
+
+
+def test_fused_kernel_grid_sizes_bitwise(monkeypatch):
+    """The fused kernel's persistent grid (work groups walking tiles) does not change the
+    result: 1, 7 and 592 groups, bitwise."""
+    import paper_1903_11521_b200 as ydg
+    cfg = synth.CONFIGS["c0"].with_(N=5, nx=4, ny=4, nz=4, vperm=True, name="fused-grid")
+    xyz, vid, mat, Q, _ = make_inputs(cfg)
+    outs = []
+    monkeypatch.setenv("YDG_FUSED", "1")
+    for g in ("1", "7", "592"):
+        monkeypatch.setenv("YDG_GRID_LOCAL", g)
+        h = ydg.ydg_create(cfg.N, 9, 8)
+        ydg.ydg_upload_mesh(h, xyz, vid, mat)
+        assert ydg.ydg_query(h, ydg.YDG_Q_FUSED) == 1.0
+        ydg.ydg_upload_dofs(h, 0, Q)
+        ydg.ydg_step(h, cfg.dt, 4)
+        outs.append(ydg.ydg_download_dofs(h, 0, cfg.n_elements))
+        ydg.ydg_destroy(h)
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
