@@ -421,6 +421,10 @@ constexpr int kFluxPf = YDG_FLUX_PF, kFluxPfFace = YDG_FLUX_PF_FACE;
 #define YDG_FLUX_QPF_FACE 3
 #endif
 constexpr int kFluxQpfFace = YDG_FLUX_QPF_FACE;
+#ifndef YDG_FLUX_QEARLY
+#define YDG_FLUX_QEARLY 2  // measured (c1 flux): 0: 7.54, 1: 7.27, 2: 7.19-7.22 ms
+#endif
+constexpr int kFluxQEarly = YDG_FLUX_QEARLY;
 __device__ __forceinline__ int swzf(int row, int col) { return row * kRSF + (col ^ ((row & 2) << 1)); }
 __device__ __forceinline__ void smem_bf(const Ctx& x, const double* Y, unsigned w, double (&bf)[kU]) {
   const int row = krow(x, w);
@@ -1016,6 +1020,11 @@ __global__ void __launch_bounds__(kTF * kFluxGroups, kFluxGroups == 1 ? kFluxCta
       // Y buffer F & 1: last read by the paired lift of faces F-2, F-1 (followed by a barrier)
       double* Y = Y0 + (F & 1) * Bt * kRSF;
       const bool has_next = F < 3 || more;
+      double* Qt = prm.Q + tile * B * kRS;
+      double2 qn[2][kU];
+      // YDG_FLUX_QEARLY: the lift's first Q rows are loaded early, their L2 latency
+      // overlapping the Godunov flux (1) or also the waits and the rotation (2)
+      if (kFluxQEarly == 2 && (F & 1)) G::lift2_pre(x, Qt, qn);
       if constexpr (!kFluxLateOwn) {
         mbar_wait(&bar[0], ph_o);  // own block, coefficients, j|h of this item; slots of the next
         ph_o ^= 1;
@@ -1059,6 +1068,7 @@ __global__ void __launch_bounds__(kTF * kFluxGroups, kFluxGroups == 1 ? kFluxCta
             prefetch_l2(prm.traces + (ntile * 4 + f) * FACE + nhalf * FACEF, FACEF * sizeof(double));
         }
       }
+      if (kFluxQEarly == 1 && (F & 1)) G::lift2_pre(x, Qt, qn);
       {  // Godunov flux of rows m = rp, rp + 12, ... of element re, in place in Y
         const double* T = O + re * TS;
 #pragma unroll
@@ -1084,9 +1094,9 @@ __global__ void __launch_bounds__(kTF * kFluxGroups, kFluxGroups == 1 ? kFluxCta
       // unit's Q stays in L2 across its two updates.  The next pair's rotation rewrites the
       // Y buffers: a barrier after the lift.
       if (F & 1) {
-        double* Qt = prm.Q + tile * B * kRS;
-        if (F == 1) G::template lift2<0>(x, Y0, Y0 + Bt * kRSF, Qt);
-        else G::template lift2<1>(x, Y0, Y0 + Bt * kRSF, Qt);
+        if (kFluxQEarly == 0) G::lift2_pre(x, Qt, qn);
+        if (F == 1) G::template lift2<0>(x, Y0, Y0 + Bt * kRSF, Qt, qn);
+        else G::template lift2<1>(x, Y0, Y0 + Bt * kRSF, Qt, qn);
         gsync();
       }
     }
@@ -1189,8 +1199,10 @@ __device__ __forceinline__ void flux_tile(Ctx& x, const StepParams<double>& prm,
     x.sync();  // every read of O, FC, JH done; Y complete
     if (tid == 0 && F < 3) issue_own(F + 1, F + 1 < 3);
     if (F & 1) {  // lift of the face pair + Q update; the pair's Y buffers are reused after
-      if (F == 1) G::template lift2<0>(x, Y0, Y0 + Bt * kRSF, Qt);
-      else G::template lift2<1>(x, Y0, Y0 + Bt * kRSF, Qt);
+      double2 qn[2][kU];
+      G::lift2_pre(x, Qt, qn);
+      if (F == 1) G::template lift2<0>(x, Y0, Y0 + Bt * kRSF, Qt, qn);
+      else G::template lift2<1>(x, Y0, Y0 + Bt * kRSF, Qt, qn);
       if (F == 1) x.sync();
     }
   }

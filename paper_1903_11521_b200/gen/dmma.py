@@ -445,12 +445,14 @@ def gen_order(N):
     lift0 = len(tab.frags)
     # paired lift: faces 2P and 2P+1 accumulate into the same registers, one Q update per pair
     b(f"  // paired lift + Q update (flux kernel layout): Q += R^(2P) Ya + R^(2P+1) Yb")
-    b(f"  template <int P> static __device__ __forceinline__ void lift2(Ctx& x, const double* Ya, const double* Yb, double* Qt) {{")
+    # lift2_pre: the first m-tile group's Q rows, issued by the caller ahead of the lift
+    g0 = groups[0]
+    b(f"  static __device__ __forceinline__ void lift2_pre(const Ctx& x, const double* Qt, double2 (&qn)[2][kU]) {{")
+    b(f"    load_qf(x, Qt, {row_word64(outs[g0[0]])}, {row_word64(outs[g0[1]]) if len(g0) > 1 else '~0ULL'}, qn);")
+    b("  }")
+    b(f"  template <int P> static __device__ __forceinline__ void lift2(Ctx& x, const double* Ya, const double* Yb, double* Qt, double2 (&qn)[2][kU]) {{")
     for P in range(2):
         b(f"    {'if' if P == 0 else 'else if'} constexpr (P == {P}) {{")
-        b("      double2 qn[2][kU];")
-        g0 = groups[0]
-        b(f"      load_qf(x, Qt, {row_word64(outs[g0[0]])}, {row_word64(outs[g0[1]]) if len(g0) > 1 else '~0ULL'}, qn);")
         for gi, grp in enumerate(groups):
             b("      {")
             b("        double2 qc[2][kU];")
