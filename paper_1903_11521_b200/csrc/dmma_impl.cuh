@@ -336,11 +336,36 @@ __device__ __forceinline__ void q_batch(const Ctx& x, const double* Qt, const do
 // Q += acc over all m-tiles (rows from the words w[]; rows < IR of Q^n are read from the
 // shared copy Qs), two m-tiles per batch, software-pipelined: the next batch's Q loads are
 // issued before the current batch's stores (one memory latency in total, bounded registers).
+// global rows (>= IR) of the first batch, ahead of time (add_q's `pre`)
+template <int MT, int IR>
+__device__ __forceinline__ void q_pre(const Ctx& x, const double* Qt, const unsigned long long (&w)[MT],
+                                      double2 (&v)[2][kU]) {
+#pragma unroll
+  for (int k2 = 0; k2 < 2; ++k2) {
+    const int row = k2 < MT ? mrow(x, w[k2 < MT ? k2 : 0]) : 0xff;
+#pragma unroll
+    for (int k = 0; k < kU; ++k)
+      v[k2][k] = (row == 0xff || row < IR) ? make_double2(0.0, 0.0)
+                                           : *reinterpret_cast<const double2*>(Qt + row * kRS + ccol(x, k));
+  }
+}
 template <int MT, int IR = 0>
 __device__ __forceinline__ void add_q(const Ctx& x, double* Qt, double (&acc)[MT][kU][2],
-                                      const unsigned long long (&w)[MT], const double* Qs = nullptr) {
+                                      const unsigned long long (&w)[MT], const double* Qs = nullptr,
+                                      const double2 (*pre)[kU] = nullptr) {
   double2 vc[2][kU], vn[2][kU];
-  q_batch<MT, IR>(x, Qt, Qs, w, 0, vc);
+  if (pre) {  // global rows preloaded; rows < IR from the shared copy
+#pragma unroll
+    for (int k2 = 0; k2 < 2; ++k2) {
+      const int row = k2 < MT ? mrow(x, w[k2 < MT ? k2 : 0]) : 0xff;
+#pragma unroll
+      for (int k = 0; k < kU; ++k)
+        vc[k2][k] = (row != 0xff && row < IR) ? *reinterpret_cast<const double2*>(Qs + row * kRS + ccol(x, k))
+                                              : pre[k2][k];
+    }
+  } else {
+    q_batch<MT, IR>(x, Qt, Qs, w, 0, vc);
+  }
 #pragma unroll
   for (int m0 = 0; m0 < MT; m0 += 2) {
     if (m0 + 2 < MT) q_batch<MT, IR>(x, Qt, Qs, w, m0 + 2, vn);
@@ -421,6 +446,9 @@ constexpr int kFluxPf = YDG_FLUX_PF, kFluxPfFace = YDG_FLUX_PF_FACE;
 #define YDG_FLUX_QPF_FACE 3
 #endif
 constexpr int kFluxQpfFace = YDG_FLUX_QPF_FACE;
+#ifndef YDG_VOL_QEARLY
+#define YDG_VOL_QEARLY 0  // measured (c1 local): 1 spills (468 B) and runs 14.47 vs 13.74 ms
+#endif
 #ifndef YDG_FLUX_QEARLY
 #define YDG_FLUX_QEARLY 2  // measured (c1 flux): 0: 7.54, 1: 7.27, 2: 7.19-7.22 ms
 #endif
@@ -870,11 +898,14 @@ __device__ __forceinline__ void local_body(const StepParams<double>& prm) {
       double acc[G::QMT][kU][2];
       zero_acc(acc);
       if constexpr (kLocalFs) mbar_wait(x.fbar, 1);  // volume fragments (staged after CK step 0)
+      // YDG_VOL_QEARLY: the Q update's first global rows loaded before the volume product
+      double2 vpre[2][kU];
+      if constexpr (YDG_VOL_QEARLY) G::add_volume_pre(x, Qt, vpre);
       G::volume(x, acc);
       YDG_PHASE(10);
       mbar_wait(qbar, qph);
       qph ^= 1;
-      G::add_volume(x, Qt, acc, x.S);
+      G::add_volume(x, Qt, acc, x.S, YDG_VOL_QEARLY ? vpre : nullptr);
     }
     x.sync();  // before the next tile overwrites the shared regions
     if (kLocalFs && x.tid == 0 && it + vgrid < prm.ntiles)

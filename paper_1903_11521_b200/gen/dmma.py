@@ -401,9 +401,15 @@ def gen_order(N):
     regions["VOL"] = (f0, len(tab.frags))
     counts["vol"] = emit_xprod(b, plan, "vol", tl, "SRC_I", fbase=f0)
     b("  }")
-    b(f"  static __device__ __forceinline__ void add_volume(const Ctx& x, double* Qt, double (&acc)[{QMT}][kU][2], const double* Qs) {{")
+    b(f"  static __device__ __forceinline__ void add_volume(const Ctx& x, double* Qt, double (&acc)[{QMT}][kU][2], const double* Qs,")
+    b("                                                   const double2 (*pre)[kU] = nullptr) {")
     b("    constexpr unsigned long long w[] = {" + ", ".join(row_word64(og) for og in tl["out"]) + "};")
-    b("    add_q<" + str(QMT) + ", IROWS>(x, Qt, acc, w, Qs);")
+    b("    add_q<" + str(QMT) + ", IROWS>(x, Qt, acc, w, Qs, pre);")
+    b("  }")
+    b("  // the first batch's Q rows >= IROWS (global memory), loaded ahead of the volume product")
+    b("  static __device__ __forceinline__ void add_volume_pre(const Ctx& x, const double* Qt, double2 (&v)[2][kU]) {")
+    b("    constexpr unsigned long long w[] = {" + ", ".join(row_word64(og) for og in tl["out"]) + "};")
+    b("    q_pre<" + str(QMT) + ", IROWS>(x, Qt, w, v);")
     b("  }")
     # ---------------- traces T_i = R^iT I
     counts["tr01_dfma"] = emit_trace01_dfma(b, R, B, Bt, IROWS, TS) if DFMA_TR01 else 0
