@@ -5,7 +5,8 @@
 
 One *step* = one global ADER-DG time step of every element of the workload (the whole hot
 path: CK recursion, time integral, volume, local and neighbour flux = BASELINE.json
-north_star), i.e. one ``ydg_step(dt, 1)`` call = two kernel launches.  Metric: element-
+north_star): two kernel launches (local part, flux).  The K timed steps are one
+``ydg_step(dt, K)`` call, as a user advancing a simulation makes it.  Metric: element-
 updates/s (plus nonzero GFLOP/s and the roofline fraction of the dominant kernel).
 
 Workload (BASELINE.json configs[1], "c1"): elastic, N = 5, fp64, 64^3 Kuhn-split cubes =
@@ -16,7 +17,7 @@ z-slab of c1's size (weak scaling; the halo of shared-face traces goes over NCCL
 ydg_step).  --config c4 (BASELINE configs[4]) is strong scaling: the fixed 128^3-cube mesh
 (12,582,912 tetrahedra) split into N z-slabs of 128/N cube layers.
 
-Timing: W untimed warm-up steps, then K steps bracketed by barrier + synchronize, CUDA
+Timing: W untimed warm-up steps (one call), then K steps bracketed by barrier + synchronize, CUDA
 events on the launching stream, max over ranks.  The inputs (6.3 GB of DOFs per GPU) are
 larger than L2, so no flush is needed.  Per-kernel device times come from the library's
 own CUDA events around each launch (ydg_profile) inside the timed region.
