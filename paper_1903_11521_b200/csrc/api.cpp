@@ -309,19 +309,21 @@ int upload_coeffs(ydg_solver* h, const double* xyz, const double* material, cons
 
 // Algorithmic HBM bytes per element of each kernel (each array touched once).
 // fp64 (tensor-core kernels): local reads Q, star, writes Q and the 4 trace blocks; the
-// flux kernel reads Q, own + neighbour trace blocks, the factored flux solvers, writes Q.  fp32 (sparse kernels):
-// the local kernel also reads A+ (local flux), the neighbour kernel reads A- only and the
-// neighbour traces.
+// flux kernel reads Q, own + neighbour trace blocks, the factored flux solvers, writes Q.
+// fp32 (sparse kernels): local reads Q, star, writes Q and the 4 traces; the flux kernel
+// reads Q, A+ and A-, own + neighbour traces, writes Q (both flux terms, one lift per face).
 double alg_bytes_local(const ydg_solver* h) {
   const double P = h->P, B = h->B, Bt = h->Bt;
   if (h->prec == 8) return (2 * B * P + 3 * P * 3 + 4 * trace_block(h)) * elem_bytes(h);
-  return (2 * B * P + 3 * P * 3 + 4 * P * P + 4 * Bt * P) * elem_bytes(h);
+  return (2 * B * P + 3 * P * 3 + 4 * Bt * P) * elem_bytes(h);
 }
 double alg_bytes_neigh(const ydg_solver* h) {
   const double P = h->P, B = h->B, Bt = h->Bt;
   if (h->prec == 8) return (2 * B * P + 4 * kFaceCoeffs + 2 * 4 * trace_block(h)) * elem_bytes(h) + 4 * (4 + 1);
-  return (2 * B * P + 4 * P * P + 4 * Bt * P) * elem_bytes(h) + 4 * (4 + 1);
+  return (2 * B * P + 2 * 4 * P * P + 2 * 4 * Bt * P) * elem_bytes(h) + 4 * (4 + 1);
 }
+// the tiled elastic kernels (fp64 and fp32) lift the local + neighbour flux once per face
+bool shared_lift(const ydg_solver* h) { return h->prec == 8 || !h->generic; }
 
 // fused kernel (fp64): Q read and written once, star, the 4 trace blocks written, own and
 // neighbour trace blocks read, the factored flux solvers, neighbour slots and j|h
@@ -1338,16 +1340,17 @@ int ydg_query(ydg_solver* h, int what, double* v) {
     case YDG_Q_LOCAL_BYTES: *v = alg_bytes_local(h); break;
     case YDG_Q_NEIGH_BYTES: *v = alg_bytes_neigh(h); break;
     case YDG_Q_KERNEL_PATH: *v = h->generic ? (h->visco_tc ? 2 : 3) : (h->prec == 8 ? 0 : 1); break;
-    // fp64: the local kernel runs CK, time integral, volume, traces; both flux terms are in
-    // the flux kernel.  fp32: the local flux is in the local kernel.
-    case YDG_Q_LOCAL_FLOPS: *v = h->P == 27 ? nz_flops_visco_local(h->N) : nz_flops_local(h->N, h->prec == 8); break;
+    // tiled elastic kernels (fp64, fp32): the local kernel runs CK, time integral, volume,
+    // traces; both flux terms are in the flux kernel.  Generic CSR path: the local flux is
+    // in the local kernel.
+    case YDG_Q_LOCAL_FLOPS: *v = h->P == 27 ? nz_flops_visco_local(h->N) : nz_flops_local(h->N, shared_lift(h)); break;
     case YDG_Q_NEIGH_FLOPS:
       *v = h->P == 27 ? nz_flops_visco(h->N) - nz_flops_visco_local(h->N)
-                      : nz_flops_elastic(h->N, false) - nz_flops_local(h->N, h->prec == 8);
+                      : nz_flops_elastic(h->N, false) - nz_flops_local(h->N, shared_lift(h));
       break;
-    case YDG_Q_NEIGH_FLOPS_EXEC:  // the fp64 flux kernel lifts local + neighbour flux once per face
+    case YDG_Q_NEIGH_FLOPS_EXEC:  // the tiled flux kernels lift local + neighbour flux once per face
       *v = h->P == 27 ? nz_flops_visco(h->N) - nz_flops_visco_local(h->N)
-                      : nz_flops_elastic(h->N, h->prec == 8) - nz_flops_local(h->N, h->prec == 8);
+                      : nz_flops_elastic(h->N, shared_lift(h)) - nz_flops_local(h->N, shared_lift(h));
       break;
     default: return fail(h, YDG_ERR_ARG, "unknown query");
   }

@@ -2,8 +2,9 @@
 //
 // Two launches per time step:
 //   ader_local : CK recursion + time integral, volume,
-//                face traces R^iT I, local flux R^i (T_i A+^T)
-//   ader_neigh : neighbour flux R^i ((f^h T^nb) A-^T) (chain order P:1396)
+//                face traces R^iT I
+//   ader_neigh : local + neighbour flux R^i (T A+^T + (f^h T^nb) A-^T), one lift per face
+//                (chain order P:1396)
 // Thread = (element, quantity column); warp = 32 elements (a tile) x one column; CTA =
 // the 9 columns of one tile.  Each nonzero of the global matrices is one FMA with a
 // compile-time constant (generated/ydg_gen_N*.cuh); the per-element 9x9 mixing goes
@@ -133,10 +134,8 @@ int nBt(int N) { return (N + 1) * (N + 2) / 2; }
 
 }  // namespace
 
-size_t sparse_local_smem(int N, int eb) {
-  return static_cast<size_t>(std::max(nB(N), 2 * nBt(N)) + 2 * nBt(N)) * kRS * eb;
-}
-size_t sparse_neigh_smem(int N, int eb) { return static_cast<size_t>(4 * nBt(N)) * kRS * eb; }
+size_t sparse_local_smem(int N, int eb) { return static_cast<size_t>(nB(N)) * kRS * eb; }
+size_t sparse_neigh_smem(int N, int eb) { return static_cast<size_t>(6 * nBt(N)) * kRS * eb; }
 
 size_t local_smem_bytes(int N, int eb) {
   switch (N) {

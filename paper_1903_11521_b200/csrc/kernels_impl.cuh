@@ -34,40 +34,12 @@ __device__ __forceinline__ void q_prefetch_l2(const void* p, unsigned bytes) {
 static __constant__ int c_star_cols[9][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {6, 7, 7}, {7, 8, 8},
                                              {6, 8, 8}, {0, 3, 5}, {3, 1, 4}, {5, 4, 2}};
 
-// y_m = sum_q Z[m][q] A[p][q] for a 9x9 flux solver row held in registers.
-template <int Bt, typename T>
-__device__ __forceinline__ void mix_rows(const T* Z, const T (&arow)[kP], int lane, T (&y)[Bt]) {
-#pragma unroll
-  for (int m = 0; m < Bt; ++m) {
-    asm volatile("" ::: "memory");  // one row of loads in flight: bounded register pressure
-    const T* row = Z + m * kRS + lane;
-    T s = T(0);
-#pragma unroll
-    for (int q = 0; q < kP; ++q) s = fma(row[q * kLanes], arow[q], s);
-    y[m] = s;
-  }
-}
-
 template <typename T>
 __device__ __forceinline__ void load_flux_row(const T* base, int64_t tile, int F, int p, int lane,
                                               T (&arow)[kP]) {
   const T* A = base + ((tile * 4 + F) * kP + p) * kP * kLanes + lane;
 #pragma unroll
   for (int q = 0; q < kP; ++q) arow[q] = A[q * kLanes];
-}
-
-// Replace Z (own column, in shared memory) by Y = Z A_F^T for face F.
-template <int Bt, typename T>
-__device__ __forceinline__ void mix_face(T* Z, const T* flux, int64_t tile, int F, int p, int lane) {
-  T y[Bt];
-  {
-    T arow[kP];
-    load_flux_row(flux, tile, F, p, lane, arow);
-    mix_rows<Bt>(Z, arow, lane, y);
-  }
-  __syncthreads();  // every column of Z has been read
-#pragma unroll
-  for (int m = 0; m < Bt; ++m) Z[m * kRS + p * kLanes + lane] = y[m];
 }
 
 template <typename T, int B>
@@ -81,19 +53,14 @@ __device__ __forceinline__ void add_to_q(T* Qt, const T (&acc)[B]) {
 }
 
 // Local part of the update: CK recursion + time integral, volume
-// (P:1338-1340), traces T_i = R^iT I (stored for the neighbours) and the local flux
-// R^i (T_i A+_i^T).  Shared memory: S [B][9][32] and Z0, Z1 [Bt][9][32].
+// and the traces T_i = R^iT I (stored for the flux kernel).  Shared memory:
+// S [B][9][32].
 template <int N, typename T>
 __global__ void __launch_bounds__(kP * kLanes, 1) ader_local(const StepParams<T> prm) {
   using G = Gen<N>;
   constexpr int B = G::B, Bt = G::Bt;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* S = reinterpret_cast<T*>(smem_raw);  // [max(B, 2Bt)][9][32]
-  constexpr int SR = B > 2 * Bt ? B : 2 * Bt;
-  T* Z0 = S + SR * kRS;                    // [Bt][9][32]
-  T* Z1 = Z0 + Bt * kRS;
-  T* Z2 = S;                                // aliases rows [0, Bt) of S once S is dead
-  T* Z3 = S + Bt * kRS;
+  T* S = reinterpret_cast<T*>(smem_raw);  // [B][9][32]
   const int lane = threadIdx.x & 31, p = threadIdx.x >> 5;
   const int c0 = c_star_cols[p][0], c1 = c_star_cols[p][1], c2 = c_star_cols[p][2];
   const int own = p * kLanes + lane;
@@ -130,9 +97,9 @@ __global__ void __launch_bounds__(kP * kLanes, 1) ader_local(const StepParams<T>
                             acc);
       add_to_q(Qt, acc);
     }
-    // traces of the time integral on the four faces (own column), stored for the
-    // neighbour kernel ([elem][face][m][q]) and staged for the flux solvers
-    // tiled trace layout [tile][face][m][q][32]
+    // traces of the time integral on the four faces (own column), stored for the flux
+    // kernel, tiled trace layout [tile][face][m][q][32]; both flux terms are applied there
+    // (one lift per face, as on the fp64 path)
     T* tr = prm.traces + tile * 4 * Bt * kRS + p * kLanes + lane;
     {
       T ta[Bt], tb[Bt];
@@ -142,38 +109,64 @@ __global__ void __launch_bounds__(kP * kLanes, 1) ader_local(const StepParams<T>
       for (int m = 0; m < Bt; ++m) {
         tr[(0 * Bt + m) * kRS] = ta[m];
         tr[(1 * Bt + m) * kRS] = tb[m];
-        Z0[m * kRS + own] = ta[m];
-        Z1[m * kRS + own] = tb[m];
       }
       G::template trace<2, T>(S + own, ta);
       G::template trace<3, T>(S + own, tb);
-      __syncthreads();  // S (time integral) is dead: stage faces 2, 3 in its rows
 #pragma unroll
       for (int m = 0; m < Bt; ++m) {
         tr[(2 * Bt + m) * kRS] = ta[m];
         tr[(3 * Bt + m) * kRS] = tb[m];
-        Z2[m * kRS + own] = ta[m];
-        Z3[m * kRS + own] = tb[m];
       }
     }
-    __syncthreads();
-    mix_face<Bt>(Z0, prm.aplus, tile, 0, p, lane);
-    mix_face<Bt>(Z1, prm.aplus, tile, 1, p, lane);
-    mix_face<Bt>(Z2, prm.aplus, tile, 2, p, lane);
-    mix_face<Bt>(Z3, prm.aplus, tile, 3, p, lane);
-    __syncthreads();
-    {
-      T acc[B];
-#pragma unroll
-      for (int k = 0; k < B; ++k) acc[k] = T(0);
-      G::template lift<0, T>(Z0 + own, acc);
-      G::template lift<1, T>(Z1 + own, acc);
-      G::template lift<2, T>(Z2 + own, acc);
-      G::template lift<3, T>(Z3 + own, acc);
-      add_to_q(Qt, acc);
-    }
-    __syncthreads();  // before the next tile overwrites S / Z
+    __syncthreads();  // before the next tile overwrites S
   }
+}
+
+// Flux of face F on the own column p (P:1341-1342 with one lift per face, reading R22):
+//   y_m = sum_q T_i[m][q] A+_i[p][q] + sum_q Z_i[m][q] A-_i[p][q]
+// O = the tile's own trace rows of the face (staged in shared memory, [m][q][32]), Z = the
+// rotated neighbour trace (replaced by y).
+template <int Bt, typename T>
+__device__ __forceinline__ void mix_flux(T* Z, const T* O, const T* ap, const T* am, int64_t tile, int F, int p,
+                                         int lane) {
+  T y[Bt];
+  {
+    T rp[kP], rm[kP];
+    load_flux_row(ap, tile, F, p, lane, rp);
+    load_flux_row(am, tile, F, p, lane, rm);
+#pragma unroll
+    for (int m = 0; m < Bt; ++m) {
+      asm volatile("" ::: "memory");  // one row of loads in flight: bounded register pressure
+      const T* row = Z + m * kRS + lane;
+      const T* orow = O + m * kRS + lane;
+      T s = T(0), u = T(0);
+#pragma unroll
+      for (int q = 0; q < kP; ++q) s = fma(row[q * kLanes], rm[q], s);
+#pragma unroll
+      for (int q = 0; q < kP; ++q) u = fma(orow[q * kLanes], rp[q], u);
+      y[m] = s + u;
+    }
+  }
+  __syncthreads();  // every column of Z and O has been read
+#pragma unroll
+  for (int m = 0; m < Bt; ++m) Z[m * kRS + p * kLanes + lane] = y[m];
+}
+
+// the tile's own traces of face F -> O (16-byte cp.async, one commit group)
+template <int Bt, typename T>
+__device__ __forceinline__ void own_copy(const T* traces, int64_t tile, int F, T* O) {
+  constexpr int n = Bt * kRS * static_cast<int>(sizeof(T)) / 16;
+  const char* src = reinterpret_cast<const char*>(traces + (tile * 4 + F) * Bt * kRS);
+  char* dst = reinterpret_cast<char*>(O);
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst + 16 * i))),
+                 "l"(src + 16 * i)
+                 : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int K>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory");
 }
 
 template <int N, typename T, int F>
@@ -193,8 +186,10 @@ __device__ __forceinline__ void neigh_gather(const StepParams<T>& prm, int64_t t
   G::template rot<T>(h, tn, [&](int m, T z) { dst[m * kRS] = z; });
 }
 
-// Neighbour flux (chain order P:1396): Q += sum_i R^i ((f^h_i T^nb_(j_i)) A-_i^T).
-// Shared memory: Z [4][Bt][9][32].
+// Flux kernel (chain order P:1396) with one lift per face (reading R22):
+//   Q += sum_i R^i ( T_i A+_i^T + (f^h_i T^nb_(j_i)) A-_i^T ).
+// Shared memory: Z [4][Bt][9][32] (rotated neighbour traces, then the face fluxes), O
+// [2][Bt][9][32] (the tile's own traces of two faces at a time).
 template <int N, typename T>
 __global__ void __launch_bounds__(kP * kLanes, 1) ader_neigh(const StepParams<T> prm) {
   using G = Gen<N>;
@@ -206,15 +201,26 @@ __global__ void __launch_bounds__(kP * kLanes, 1) ader_neigh(const StepParams<T>
   for (int64_t it = blockIdx.x; it < prm.ntiles; it += gridDim.x) {
     const int64_t tile = prm.tile0 + it;
     if (threadIdx.x == 0) q_prefetch_l2(prm.Q + tile * B * kRS, B * kRS * sizeof(T));
+    T* O0 = Z + 4 * Bt * kRS;
+    T* O1 = O0 + Bt * kRS;
+    own_copy<Bt>(prm.traces, tile, 0, O0);
+    own_copy<Bt>(prm.traces, tile, 1, O1);
     neigh_gather<N, T, 0>(prm, tile, p, lane, Z + 0 * Bt * kRS);
     neigh_gather<N, T, 1>(prm, tile, p, lane, Z + 1 * Bt * kRS);
     neigh_gather<N, T, 2>(prm, tile, p, lane, Z + 2 * Bt * kRS);
     neigh_gather<N, T, 3>(prm, tile, p, lane, Z + 3 * Bt * kRS);
-    __syncthreads();
-    mix_face<Bt>(Z + 0 * Bt * kRS, prm.aminus, tile, 0, p, lane);
-    mix_face<Bt>(Z + 1 * Bt * kRS, prm.aminus, tile, 1, p, lane);
-    mix_face<Bt>(Z + 2 * Bt * kRS, prm.aminus, tile, 2, p, lane);
-    mix_face<Bt>(Z + 3 * Bt * kRS, prm.aminus, tile, 3, p, lane);
+    cp_async_wait_group<0>();
+    __syncthreads();  // rotated neighbour traces, own traces of faces 0, 1 in shared memory
+    mix_flux<Bt>(Z + 0 * Bt * kRS, O0, prm.aplus, prm.aminus, tile, 0, p, lane);
+    own_copy<Bt>(prm.traces, tile, 2, O0);
+    mix_flux<Bt>(Z + 1 * Bt * kRS, O1, prm.aplus, prm.aminus, tile, 1, p, lane);
+    own_copy<Bt>(prm.traces, tile, 3, O1);
+    cp_async_wait_group<1>();
+    __syncthreads();  // face 2's own traces
+    mix_flux<Bt>(Z + 2 * Bt * kRS, O0, prm.aplus, prm.aminus, tile, 2, p, lane);
+    cp_async_wait_group<0>();
+    __syncthreads();  // face 3's own traces
+    mix_flux<Bt>(Z + 3 * Bt * kRS, O1, prm.aplus, prm.aminus, tile, 3, p, lane);
     __syncthreads();
     T acc[B];
 #pragma unroll
