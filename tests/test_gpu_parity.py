@@ -374,3 +374,37 @@ def test_fused_kernel_grid_sizes_bitwise(monkeypatch):
         outs.append(ydg.ydg_download_dofs(h, 0, cfg.n_elements))
         ydg.ydg_destroy(h)
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+@pytest.mark.parametrize("N,prec", [(5, 8), (2, 8), (6, 4), (3, 4)])
+def test_accounting_queries(N, prec):
+    """The bench's roofline inputs: the per-kernel nonzero flops add up to the canonical count
+    of the step (both flux terms with their own lifts), the executed flux count
+    (one lift per face) is below it by the local lifts, and the algorithmic bytes per
+    element follow the arrays each kernel touches once (written out here from the layouts)."""
+    import paper_1903_11521_b200 as ydg
+    cfg = synth.CONFIGS["c0"].with_(N=N, precision=prec, name=f"acct-N{N}")
+    xyz, vid, mat, Q, _ = make_inputs(cfg)
+    h = ydg.ydg_create(N, 9, prec)
+    ydg.ydg_upload_mesh(h, xyz, vid, mat)
+    q = lambda k: ydg.ydg_query(h, k)
+    B, Bt, P = (N + 1) * (N + 2) * (N + 3) // 6, (N + 1) * (N + 2) // 2, 9
+    assert q(ydg.YDG_Q_B) == B and q(ydg.YDG_Q_BTILDE) == Bt
+    nz, loc, nb, nbx = (q(ydg.YDG_Q_NZ_FLOPS), q(ydg.YDG_Q_LOCAL_FLOPS), q(ydg.YDG_Q_NEIGH_FLOPS),
+                        q(ydg.YDG_Q_NEIGH_FLOPS_EXEC))
+    assert loc + nb == nz
+    # one lift per face instead of two: the executed flux count drops by 4 * 9 * nnz(R) FMAs
+    # of the local lifts (2 flops each) -- the same R^i appear in both lifts
+    assert 0 < nbx < nb
+    by_l, by_n = q(ydg.YDG_Q_LOCAL_BYTES), q(ydg.YDG_Q_NEIGH_BYTES)
+    assert q(ydg.YDG_Q_ALG_BYTES) == by_l + by_n
+    # star matrices as stored: 3 directions x 9 rows x 3 columns per element
+    if prec == 4:  # fp32 tiled kernels: traces [m][q] per face, 9x9 A+ and A- per face
+        assert by_l == (2 * B * P + 81 + 4 * Bt * P) * 4
+        assert by_n == (2 * B * P + 8 * P * P + 8 * Bt * P) * 4 + 20
+    else:  # fp64: element-face trace blocks of TS = even(9 Bt) doubles, 12 flux coefficients
+        TS = (9 * Bt + 1) // 2 * 2
+        assert by_l == (2 * B * P + 81 + 4 * TS) * 8
+        assert by_n == (2 * B * P + 48 + 8 * TS) * 8 + 20
+        assert q(ydg.YDG_Q_FUSED_BYTES) == (2 * B * P + 81 + 48 + 12 * TS) * 8 + 20
+    ydg.ydg_destroy(h)
