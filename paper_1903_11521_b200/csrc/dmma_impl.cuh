@@ -68,6 +68,7 @@ struct Ctx {
   double* S;          // [SROWS][288]  D^d, d >= 1
   double* I;          // [IROWS][288]  time integral rows < IROWS
   double* xb;         // warp-private [3][kU][4][8]
+  double* xb2;        // second star-chunk buffer of CK step 0 (YDG_GEN_XPIPE): S rows >= B - IROWS
   const double* Qt;   // Q of this tile in global memory: [B][9][32]
   const double* frags;
   const double* fs;   // shared-memory A-fragment buffer (products staged there)
@@ -258,6 +259,44 @@ __device__ __forceinline__ void xcalc(Ctx& x, int buf, int r0, int r1, int r2, i
 #pragma unroll
       for (int c = 0; c < 3; ++c) xb[(c * kU + x.xk) * kXS + r * 8 + (x.lane & 7)] = v[r][c];
   }
+}
+// Pipelined form (generator YDG_GEN_XPIPE, CK step 0): the chunk of k-set i + 1 is computed
+// in the same basic block as k-set i's DMMAs, into the other of two buffers (x.xb, x.xb2),
+// so that its dependent FP64 waves interleave with those DMMAs.  No branch: lanes xk = 3
+// compute unit 2's values again and only their stores are predicated off.
+template <Src SRC, int B>
+__device__ __forceinline__ void xcalc_to(const Ctx& x, double* xb, int r0, int r1, int r2, int r3) {
+  const int rr[4] = {r0, r1, r2, r3};
+  double d[4][3];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    d[r][0] = load_data<SRC, B>(x, rr[r], x.q0 * kL + x.xe);
+    d[r][1] = load_data<SRC, B>(x, rr[r], x.q1 * kL + x.xe);
+    d[r][2] = load_data<SRC, B>(x, rr[r], x.q2 * kL + x.xe);
+  }
+  double v[4][3];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) v[r][c] = x.a[3 * c] * d[r][0];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) v[r][c] = fma(x.a[3 * c + 1], d[r][1], v[r][c]);
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) v[r][c] = fma(x.a[3 * c + 2], d[r][2], v[r][c]);
+  const bool st = x.xk < kU;
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      if (st) xb[(c * kU + x.xk) * kXS + r * 8 + (x.lane & 7)] = v[r][c];
+}
+__device__ __forceinline__ void xb_from(const double* xb, const Ctx& x, int c, double (&bf)[kU]) {
+#pragma unroll
+  for (int k = 0; k < kU; ++k) bf[k] = xb[(c * kU + k) * kXS + (x.lane & 3) * 8 + (x.lane >> 2)];
 }
 __device__ __forceinline__ void xb_b(const Ctx& x, int buf, int c, double (&bf)[kU]) {
   const double* xb = x.xb + (buf % kXBUF) * kXW;
@@ -757,6 +796,7 @@ __device__ __forceinline__ void local_body(const StepParams<double>& prm) {
   x.I = smem;
   x.S = smem + G::IROWS * kRS;
   x.xb = smem + Lay::ROWS * kRS + x.w * kXBUF * kXW;
+  x.xb2 = x.S + (G::B - G::IROWS) * kRS + x.w * kXW;  // free during CK step 0 (Q^n fills B rows)
   x.frags = frag_table<N>();
   x.fs = kLocalGroups > 1 ? smem_cta + kLocalGroups * GS : smem + Lay::FOFF;
   x.fbar = reinterpret_cast<unsigned long long*>(smem + (FUSED ? Lay::FBAR : Lay::FOFF + Lay::FSMAX * 32));

@@ -133,10 +133,11 @@ def plan_xprod(tab, mats, til):
     return plan
 
 
-def emit_xprod(b, plan, name, til, src, fbase=None, acc="acc"):
+def emit_xprod(b, plan, name, til, src, fbase=None, acc="acc", pipe=False):
     """CK / volume style product: per k-set the warp-private star chunk X^c of the 4 rows
     (uniform across lanes), then per c the DMMAs of that c's nonzero tiles.  A fragments of
-    the next k-set are loaded before the current k-set's work."""
+    the next k-set are loaded before the current k-set's work.  pipe: software-pipelined
+    (the chunk of k-set i + 1 computed beside k-set i's DMMAs, two buffers x.xb / x.xb2)."""
     ins = til["in"][0]
     b(f"    // {name}: {sum(len(t) for t in plan)} tiles, {len(ins)} k-sets, {len(til['out'])} m-tiles")
     names = [[f"a{i}_{j}" for j in range(len(t))] for i, t in enumerate(plan)]
@@ -146,6 +147,27 @@ def emit_xprod(b, plan, name, til, src, fbase=None, acc="acc"):
             b("    const double " + ", ".join(f"{nm} = {afrag_expr(t[2], fbase)}" for nm, t in zip(names[i], plan[i])) + ";")
 
     afr(0)
+    if pipe:
+        buf = lambda i: "x.xb2" if i & 1 else "x.xb"
+        b("    static_assert((B - IROWS) * kRS + kW * kXW <= SROWS * kRS, \"second star-chunk buffer in S\");")
+        r = kset_rows(ins[0])
+        b(f"    xcalc_to<{src}, B>(x, {buf(0)}, {r[0]}, {r[1]}, {r[2]}, {r[3]});")
+        b("    __syncwarp();")
+        for i, ks in enumerate(ins):
+            if i + 1 < len(ins):
+                afr(i + 1)
+                r = kset_rows(ins[i + 1])
+                b(f"    xcalc_to<{src}, B>(x, {buf(i + 1)}, {r[0]}, {r[1]}, {r[2]}, {r[3]});")
+            for c in range(3):
+                mine = [(mt, nm) for (cc, mt, tid), nm in zip(plan[i], names[i]) if cc == c]
+                if not mine:
+                    continue
+                b(f"    {{ double bf[kU]; xb_from({buf(i)}, x, {c}, bf);")
+                for mt, nm in mine:
+                    b(f"      dmma3({acc}[{mt}], {nm}, bf);")
+                b("    }")
+            b("    __syncwarp();")
+        return sum(len(t) for t in plan)
     for i, ks in enumerate(ins):
         if i + 1 < len(ins):
             afr(i + 1)
@@ -199,6 +221,8 @@ DFMA_CK_ROWS = int(os.environ.get("YDG_GEN_CKROWS", "20"))
 # faces 0 and 1 traces as sparse DFMA code (else tensor cores); faces 2 and 3 as well
 DFMA_TR01 = os.environ.get("YDG_GEN_TR01", "1") == "1"
 DFMA_TR23 = os.environ.get("YDG_GEN_TR23", "0") == "1"
+# CK step 0's star chunks software-pipelined against the previous k-set's DMMAs
+XPIPE = os.environ.get("YDG_GEN_XPIPE", "0") == "1"
 # where the sparse-DFMA CK steps load the column's star coefficients: "step" (each step,
 # from global memory), "tail" (once, after CK step 0), "pre" (once, before CK step 0)
 STAR_LOAD = os.environ.get("YDG_GEN_STAR", "step")
@@ -365,7 +389,7 @@ def gen_order(N):
         if d == 0:  # staged in the shared-memory fragment buffer
             regions["CK0"] = (f0, len(tab.frags))
         counts[f"ck{d}"] = emit_xprod(b, plan, f"ck{d}", tl, "SRC_Q" if d == 0 else "SRC_S",
-                                      fbase=f0 if d == 0 else None)
+                                      fbase=f0 if d == 0 else None, pipe=d == 0 and XPIPE)
         b("    x.sync();  // every read of D^d done")
         for mt, og in enumerate(tl["out"]):
             b(f"    ck_wb<{1 if d == 0 else 0}, B>(x, acc[{mt}], {d}, {row_word64(og)});")
