@@ -477,8 +477,8 @@ int upload_csr(ydg_solver* h) {
   struct M { int rows, cols; std::function<double(int, int)> at; const int** ptr; const int** col; const double** val; };
   GenParams& g = h->gp;
   std::vector<M> ms = {
-      {3 * B, B, [](int r, int c) { return -TB::K[r / B][c][r % B]; }, &g.kt_ptr, &g.kt_col, &g.kt_val},
-      {3 * B, B, [](int r, int c) { return TB::K[r / B][r % B][c]; }, &g.kh_ptr, &g.kh_col, &g.kh_val},
+      {3 * B, B, [](int r, int c) { return -kdir(TB::K, r / B, c, r % B); }, &g.kt_ptr, &g.kt_col, &g.kt_val},
+      {3 * B, B, [](int r, int c) { return kdir(TB::K, r / B, r % B, c); }, &g.kh_ptr, &g.kh_col, &g.kh_val},
       {4 * Bt, B, [](int r, int c) { return TB::R[r / Bt][c][r % Bt]; }, &g.rt_ptr, &g.rt_col, &g.rt_val},
       {4 * B, Bt, [](int r, int c) { return TB::R[r / B][r % B][c]; }, &g.r_ptr, &g.r_col, &g.r_val},
       {3 * Bt, Bt, [](int r, int c) { return TB::f[r / Bt][r % Bt][c]; }, &g.f_ptr, &g.f_col, &g.f_val}};

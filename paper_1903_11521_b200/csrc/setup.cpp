@@ -216,6 +216,11 @@ bool element_coeffs(int P, int64_t e0, int64_t n, const double* xyz, const doubl
     Ji[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) / det;
     Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
     Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
+    // star matrices of the kernels' derivative directions (setup.h kDirT): A*'^c =
+    // sum_d kDirTinv[d][c] A*^d, i.e. the rows of kDirTinv^T J^-1 combine the A^d
+    double Jd[3][3];
+    for (int c = 0; c < 3; ++c)
+      for (int d = 0; d < 3; ++d) Jd[c][d] = kDirTinv[0][c] * Ji[0][d] + kDirTinv[1][c] * Ji[1][d] + kDirTinv[2][c] * Ji[2][d];
     const Mat m = material_of(material + e * 3);
     std::vector<double> A(3 * P * P), tmp(P * P), tmp2(P * P), T(P * P), Ti(P * P), G(P * P);
     for (int d = 0; d < 3; ++d) jacobian(P, d, m.rho, m.lam, m.mu, omega, &A[d * P * P]);
@@ -229,7 +234,7 @@ bool element_coeffs(int P, int64_t e0, int64_t n, const double* xyz, const doubl
           for (int kk = 0; kk < k; ++kk) dup |= cols[kk] == cols[k];
           double v = 0.0;
           if (!dup)
-            for (int d = 0; d < 3; ++d) v += Ji[c][d] * A[d * P * P + p * P + cols[k]];
+            for (int d = 0; d < 3; ++d) v += Jd[c][d] * A[d * P * P + p * P + cols[k]];
           out->star[((t * 3 + c) * P + p) * 3 + k] = v;
         }
       }

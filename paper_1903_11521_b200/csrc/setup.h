@@ -34,6 +34,24 @@ struct ElementCoeffs {
 // built from these (dm_flux).
 constexpr int kFaceCoeffs = 12;
 
+// Derivative directions of the CK and volume products ("sparser derivative
+// directions"): the kernels use K'^c = sum_d kDirT[c][d] K^d (reference directions (1,0,0),
+// (0,1,-1), (1,-2,0) of the Dubiner basis: 924 instead of 1,708 nonzeros at N = 5) with the
+// star matrices A*'^c = sum_d kDirTinv[d][c] A*^d, so that sum_c K'^c X A*'^c = sum_c K^c X
+// A*^c exactly (P:1312-1340 unchanged up to rounding).  Keep in sync with gen/tables.py KDIR_T.
+constexpr double kDirT[3][3] = {{1, 0, 0}, {0, 1, -1}, {1, -2, 0}};
+constexpr double kDirTinv[3][3] = {{1, 0, 0}, {0.5, 0, -0.5}, {0.5, -1, -0.5}};
+// K'^c[k][l] from the reference matrices K (exact cancellations -> exact zeros)
+template <class KA>
+inline double kdir(const KA& K, int c, int k, int l) {
+  double v = 0.0, m = 0.0;
+  for (int d = 0; d < 3; ++d) {
+    v += kDirT[c][d] * K[d][k][l];
+    m = m > (K[d][k][l] < 0 ? -K[d][k][l] : K[d][k][l]) ? m : (K[d][k][l] < 0 ? -K[d][k][l] : K[d][k][l]);
+  }
+  return (v < 0 ? -v : v) <= 1e-12 * m ? 0.0 : v;
+}
+
 // Columns of the star-matrix pattern of row p (3 per row; unused slots repeat a column
 // with a zero coefficient).  Valid for P = 9 and P = 27.
 void star_cols(int P, int p, int cols[3]);

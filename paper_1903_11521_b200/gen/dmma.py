@@ -351,7 +351,7 @@ def gen_order(N):
     global POOL
     POOL = Pool(f"cdf_N{N}")
     t = tables.load(N)
-    K, R, f = t["K"], t["R"], t["f"]
+    K, R, f = tables.kdir(t), t["R"], t["f"]  # CK / volume in the sparser directions (tables.KDIR_T)
     B, Bt = t["B"], t["Bt"]
     Bv = einsum.vol_dim(N)
     til = tiling.tiling(N)

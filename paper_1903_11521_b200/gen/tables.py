@@ -196,6 +196,33 @@ def load(N):
     return tables(N)
 
 
+# Derivative directions of the kernels' CK and volume products: K'^c = sum_d KDIR_T[c][d] K^d,
+# with the star matrices combined by the inverse (csrc/setup.h kDirT / kDirTinv, applied in
+# setup.cpp), so that sum_c K'^c X A*'^c = sum_c K^c X A*^c.  The reference directions
+# (1,0,0), (0,1,-1), (1,-2,0) minimise the nonzeros of the three matrices at every order
+# N = 2..6 among integer directions with entries in [-3, 3] (N = 5: 924 instead of 1,708;
+# tests/test_generator.py pins the identity and the counts).
+KDIR_T = ((1, 0, 0), (0, 1, -1), (1, -2, 0))
+
+
+def kdir(t):
+    """K'^c[k][l] = sum_d KDIR_T[c][d] K^d[k][l]; sums that cancel exactly become exact zeros."""
+    K = t["K"]
+    B = len(K[0])
+    out = []
+    for c in range(3):
+        M = []
+        for k in range(B):
+            row = []
+            for l in range(B):
+                v = sum(KDIR_T[c][d] * K[d][k][l] for d in range(3))
+                m = max(abs(K[d][k][l]) for d in range(3))
+                row.append(0.0 if abs(v) <= 1e-12 * m else v)
+            M.append(row)
+        out.append(M)
+    return out
+
+
 def emit_header(path, orders=ORDERS):
     lines = ["// GENERATED by paper_1903_11521_b200/gen/tables.py -- do not edit.",
              "// Reference-element matrices of the ADER-DG scheme (arXiv:1903.11521 Sec. 5.1),",

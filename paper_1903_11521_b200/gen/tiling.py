@@ -39,7 +39,7 @@ def products(N):
     rows < IROWS of the time integral from shared memory and the others, dt * Q, from global
     memory, so a k-set never mixes the two)."""
     t = tables.load(N)
-    K = [np.array(k, dtype=float) != 0 for k in t["K"]]
+    K = [np.array(k, dtype=float) != 0 for k in tables.kdir(t)]  # the kernels' directions (KDIR_T)
     R = [np.array(r, dtype=float) != 0 for r in t["R"]]
     B, Bt = t["B"], t["Bt"]
     Bv = einsum.vol_dim(N)

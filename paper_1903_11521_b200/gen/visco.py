@@ -46,7 +46,7 @@ def _ceil(a, b):
 
 def matrices(N):
     t = tables.load(N)
-    K = [np.array(k, dtype=np.float64) for k in t["K"]]
+    K = [np.array(k, dtype=np.float64) for k in tables.kdir(t)]  # sparser directions (tables.KDIR_T)
     R = [np.array(r, dtype=np.float64) for r in t["R"]]
     B, Bt = K[0].shape[0], R[0].shape[1]
     ck = [-k.T for k in K]                                    # Ktilde^c = -K^cT (M = I)

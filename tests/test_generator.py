@@ -49,7 +49,7 @@ def test_tilings_partition_rows(N):
 @pytest.mark.parametrize("N", [2, 5])
 def test_dmma_fragments_reproduce_the_matrices(N):
     t = tables.load(N)
-    K = [np.array(k) for k in t["K"]]
+    K = [np.array(k) for k in tables.kdir(t)]  # the kernels' derivative directions
     til = tiling.tiling(N)
     from math import comb
     Bv = comb(N + 2, 3)
@@ -67,3 +67,54 @@ def test_dmma_fragments_reproduce_the_matrices(N):
             assert np.array_equal(R, M), name
             assert hits.max() <= 1, name  # no entry covered twice
             assert np.all(hits[M != 0] == 1), name  # every nonzero issued
+
+
+def _setup_h_constants():
+    """kDirT / kDirTinv as compiled into the library (csrc/setup.h)."""
+    import os
+    import re
+    src = open(os.path.join(os.path.dirname(tables.__file__), "..", "csrc", "setup.h")).read()
+    out = {}
+    for name in ("kDirT", "kDirTinv"):
+        body = re.search(name + r"\[3\]\[3\] = \{(.*?)\};", src, re.S).group(1)
+        out[name] = np.array([float(v) for v in re.findall(r"-?\d+(?:\.\d+)?", body)]).reshape(3, 3)
+    return out
+
+
+def test_derivative_directions_are_an_exact_reformulation():
+    """The kernels' K'^c = sum_d T_cd K^d with star matrices A*'^c = sum_d (T^-1)_dc A*^d give
+    sum_c K'^c X A*'^c = sum_c K^c X A*^c for any X and star matrices: the library's
+    constants (setup.h) are T and its inverse, and T equals gen/tables.py KDIR_T."""
+    c = _setup_h_constants()
+    T = np.array(tables.KDIR_T, dtype=float)
+    assert np.array_equal(c["kDirT"], T)
+    assert np.array_equal(c["kDirTinv"] @ T, np.eye(3)) and np.array_equal(T @ c["kDirTinv"], np.eye(3))
+    rng = np.random.default_rng(7)
+    for N in (2, 5):
+        t = tables.load(N)
+        K = np.array(t["K"])
+        Kd = np.array(tables.kdir(t))
+        X = rng.normal(size=(K.shape[1], 9))
+        A = rng.normal(size=(3, 9, 9))
+        Ad = np.einsum("dc,dpq->cpq", c["kDirTinv"], A)
+        ref = sum(K[k] @ X @ A[k].T for k in range(3))
+        got = sum(Kd[k] @ X @ Ad[k].T for k in range(3))
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+        # the CK direction (Ktilde = -K^T) obeys the same identity
+        ref = sum(-K[k].T @ X @ A[k].T for k in range(3))
+        got = sum(-Kd[k].T @ X @ Ad[k].T for k in range(3))
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("N,nnz_ref,nnz_dir", [(2, 46, 29), (3, 202, 119), (4, 647, 364), (5, 1708, 924), (6, 3920, 2058)])
+def test_derivative_directions_cut_the_nonzeros(N, nnz_ref, nnz_dir):
+    """Nonzeros of the three derivative matrices in the reference directions and in KDIR_T's
+    (exact zeros: the cancellations of the Dubiner structure are exact)."""
+    t = tables.load(N)
+    assert sum(int(np.count_nonzero(np.array(k))) for k in t["K"]) == nnz_ref
+    Kd = tables.kdir(t)
+    assert sum(int(np.count_nonzero(np.array(k))) for k in Kd) == nnz_dir
+    # the staircase of the CK recursion survives: K'^c maps degree <= n to degree <= n - 1
+    from math import comb
+    Bv = comb(N + 2, 3)
+    assert all(not np.any(np.array(k)[:, Bv:]) for k in Kd)
