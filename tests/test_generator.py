@@ -118,3 +118,29 @@ def test_derivative_directions_cut_the_nonzeros(N, nnz_ref, nnz_dir):
     from math import comb
     Bv = comb(N + 2, 3)
     assert all(not np.any(np.array(k)[:, Bv:]) for k in Kd)
+
+
+def test_c_annealer_agrees_with_the_tile_count_definition(tmp_path):
+    """tools/anneal.c keeps the tile count incrementally; its reported cost must equal
+    gen/tiling's definition (count of nonzero 8x4 blocks) on the groupings it returns, and
+    reach the cached tile counts of a small order."""
+    import importlib.util
+    import os
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("reanneal", os.path.join(root, "tools", "reanneal.py"))
+    re_ = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(re_)
+    exe = str(tmp_path / "anneal")
+    subprocess.run(["gcc", "-O2", "-o", exe, os.path.join(root, "tools", "anneal.c"), "-lm"], check=True)
+    cached = tiling.tiling(3)
+    for name, pr in tiling.products(3).items():
+        if name not in ("ck0", "vol", "lift"):
+            continue
+        res, costs = re_.solve(name, pr, 200000, 4, exe, 2)  # solve() asserts cost == definition
+        rows = sorted(r for g in res["out"] for r in g)
+        assert rows == list(range(pr[0][0].shape[0]))
+        assert res["tiles"] <= cached[name]["tiles"] + 1
