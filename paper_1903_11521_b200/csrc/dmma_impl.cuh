@@ -757,7 +757,9 @@ __device__ __forceinline__ void stage_frags(const Ctx& x, int F0, int NF) {
 // volume's Q update, evicted from L2 since the staging) are prefetched into L2 again;
 // bit 2: again before the volume term
 #ifndef YDG_QPF
-#define YDG_QPF 7  // measured (c1, 8-element tiles): local 14.69 -> 14.11-14.19 ms; bit 1 alone 14.41
+#define YDG_QPF 6  // measured (c1, 8-element tiles): 7: local 14.69 -> 14.11-14.19 ms, bit 1 alone 14.41;
+                   // with the sparser derivative directions (shorter CK step 0): 7: 12.02-12.03,
+                   // 6: 11.87-11.90, 4: 11.97-11.99, 5: 12.02-12.03, 3: 12.15-12.16, 2: 12.07-12.08 ms
 #endif
 template <int N>
 __device__ __forceinline__ void after_ck0(Ctx& x) {
